@@ -1,0 +1,141 @@
+/*
+ * pcstable_b200.h -- C ABI of the B200-native PC-stable skeleton library
+ * (libpcstable_b200.so, built from paper_1812_08491_b200/csrc/).
+ *
+ * This is the drop-in boundary for the reference's hot path
+ *   stats::compute_correlation  (proj/include/pcstable/stats.hpp:132)
+ *   stats::threshold_tau        (proj/include/pcstable/stats.hpp:120)
+ *   run_pc_stable               (proj/include/pcstable/skeleton.hpp:341)
+ *   stats::ci_test / pseudo_inverse (stats.hpp:366, :172)  -- batch parity helpers
+ * Plain pointers and sizes only.  Buffers are caller-allocated; calls are
+ * synchronous; the library owns device memory for the duration of a call or
+ * session.  include/pcstable_b200.hpp re-creates the reference's C++ names
+ * (pcstable::run_pc_stable, SkeletonResult, ...) on top of this ABI, and maps
+ * the status codes back to the reference's exception classes.
+ *
+ * Matrices: correlation matrices are p x p row-major (symmetric, so identical
+ * to the reference's Eigen column-major storage); data matrices are m x p
+ * column-major exactly like Eigen::MatrixXd in DataMatrix (core.hpp:48-67),
+ * i.e. x[j*m + r] is sample r of variable j.
+ */
+#ifndef PCSTABLE_B200_H
+#define PCSTABLE_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PCS_ABI_VERSION 1
+
+typedef enum {
+    PCS_OK = 0,
+    PCS_EINVAL = 1,       /* std::invalid_argument: config (core.hpp:370-383), m < 4 (skeleton.hpp:344),
+                             DataMatrix / CorrelationMatrix validation (core.hpp:50-95) */
+    PCS_EZEROVAR = 2,     /* pcstable::ZeroVarianceError (core.hpp:23-31); column via zero_var_col */
+    PCS_EOVERFLOW = 3,    /* std::overflow_error from comb::binomial (comb.hpp:43) */
+    PCS_ENAN = 4,         /* std::invalid_argument thrown by stats::fisher_z on NaN (stats.hpp:112) */
+    PCS_ECUDA = 5,        /* CUDA runtime failure or no device */
+    PCS_ENOMEM = 6,
+    PCS_EUNSUPPORTED = 7, /* conditioning level beyond the device path */
+    PCS_ELEVEL = 8        /* pcstable::LevelUnreachableError (core.hpp:41-44): m - ell - 3 < 1 */
+} pcs_status;
+
+/* device variants of the level >= 1 CI-test kernels (both give identical results) */
+enum { PCS_VARIANT_SET = 0 /* cuPC-S, paper Alg. 4 */, PCS_VARIANT_EDGE = 1 /* cuPC-E, paper Alg. 3 */ };
+/* StopReason (skeleton.hpp:22) */
+enum { PCS_STOP_MAX_DEGREE = 0, PCS_STOP_LEVEL_CAP = 1, PCS_STOP_SAMPLE_SIZE = 2 };
+
+/* SkeletonConfig (core.hpp:357-384) + device fields */
+typedef struct {
+    double alpha;              /* (0, 1) */
+    int32_t max_level;         /* -1: no cap */
+    int32_t variant;           /* PCS_VARIANT_* (replaces Strategy) */
+    int32_t edges_per_unit;    /* beta: tuning hint, results never depend on it */
+    int32_t workers_per_edge;  /* gamma: tuning hint */
+    int32_t set_groups;        /* delta: tuning hint */
+    int32_t unit_width;        /* theta: tuning hint */
+    int32_t device;            /* CUDA device ordinal */
+    int32_t shard_index;       /* multi-GPU session: this rank (0 for single GPU) */
+    int32_t shard_count;       /* multi-GPU session: world size (1 for single GPU) */
+    int32_t reserved[5];
+} pcs_config;
+
+/* LevelStats (core.hpp:387-393) + device counters */
+typedef struct {
+    int32_t level;
+    int32_t pad;
+    uint64_t ci_tests;                /* == Strategy::Serial's LevelStats::ci_tests */
+    uint64_t pseudo_inverses;         /* == Strategy::Serial's LevelStats::pseudo_inverses */
+    uint64_t edges_removed;
+    double elapsed_s;                 /* host wall time of the level (includes compaction) */
+    uint64_t device_ci_tests;         /* CI tests the device actually executed */
+    uint64_t device_pseudo_inverses;  /* pseudo-inverses the device actually executed */
+    double kernel_ms;                 /* CUDA-event time of the level's CI-test kernels */
+} pcs_level_stats;
+
+typedef struct pcs_result pcs_result;
+typedef struct pcs_session pcs_session;
+
+const char* pcs_version(void);
+const char* pcs_last_error(void); /* thread-local message of the last failure */
+void pcs_config_default(pcs_config* cfg);
+
+/* stats::threshold_tau (stats.hpp:120-129); PCS_EINVAL for bad alpha/ell, PCS_ELEVEL for m - ell - 3 < 1 */
+pcs_status pcs_threshold_tau(double alpha, int32_t m, int32_t ell, double* tau);
+
+/* stats::compute_correlation (stats.hpp:132-156) on the device.  x: m x p column-major host buffer. */
+pcs_status pcs_correlation(const double* x, int32_t m, int32_t p, double* c_out, int32_t* zero_var_col);
+
+/* run_pc_stable (skeleton.hpp:341-391).  c: p x p host correlation matrix, validated and normalised
+   exactly like the CorrelationMatrix constructor (core.hpp:73-95). */
+pcs_status pcs_run_pc_stable(const double* c, int32_t p, int32_t m, const pcs_config* cfg, pcs_result** out);
+/* compute_correlation + run_pc_stable from m x p column-major host data (one device pipeline) */
+pcs_status pcs_run_pc_stable_data(const double* x, int32_t m, int32_t p, const pcs_config* cfg, pcs_result** out,
+                                  int32_t* zero_var_col);
+/* same as pcs_run_pc_stable with the correlation matrix already in device memory (row stride ldc) */
+pcs_status pcs_run_pc_stable_device(const double* d_c, int64_t ldc, int32_t p, int32_t m, const pcs_config* cfg,
+                                    pcs_result** out);
+
+/* SkeletonResult accessors (skeleton.hpp:33-40) */
+int32_t pcs_result_p(const pcs_result* r);
+int32_t pcs_result_levels(const pcs_result* r, pcs_level_stats* out, int32_t cap);
+int32_t pcs_result_stop_reason(const pcs_result* r);
+void pcs_result_adjacency(const pcs_result* r, uint8_t* out /* p*p, row-major */);
+int64_t pcs_result_edge_count(const pcs_result* r);
+void pcs_result_edge_list(const pcs_result* r, int32_t* out /* 2*edge_count, (i<j) ascending */);
+int64_t pcs_result_member_total(const pcs_result* r);
+/* per unordered pair, triangular slot index of core.hpp:329-335: level (-1 = kept), offset into members */
+void pcs_result_sepsets(const pcs_result* r, int32_t* level, int64_t* offset, int32_t* members);
+double pcs_result_device_seconds(const pcs_result* r); /* CUDA-event time of the whole device pipeline */
+void pcs_result_free(pcs_result* r);
+
+/* stats::ci_test for n tests of one level ell on the device (parity helper).
+   ij: 2n ints, sets: n*ell ints (ascending members).  Outputs per test. */
+pcs_status pcs_ci_test_batch(const double* c, int32_t p, int32_t ell, int64_t n, const int32_t* ij,
+                             const int32_t* sets, double tau, uint8_t* independent, double* z, double* rho,
+                             uint8_t* degenerate);
+/* stats::pseudo_inverse for n row-major ell x ell blocks on the device (parity helper) */
+pcs_status pcs_pseudo_inverse_batch(const double* a, int32_t ell, int64_t n, double* out);
+
+/* Level-stepped session: the building block of multi-GPU runs (one process per GPU, the caller
+   all-reduces the per-level key array with MIN between passes).  pcs_run_pc_stable is a session
+   with shard_count = 1. */
+pcs_status pcs_session_create(const double* c, int32_t p, int32_t m, const pcs_config* cfg, pcs_session** out);
+pcs_status pcs_session_create_device(const double* d_c, int64_t ldc, int32_t p, int32_t m, const pcs_config* cfg,
+                                     pcs_session** out);
+/* starts the next level; *running = 0 once the loop has stopped (stop reason recorded) */
+pcs_status pcs_session_level_begin(pcs_session* s, int32_t* running, int32_t* ell, int64_t* num_keys);
+/* pass 0: edges tested from their lower endpoint's row; pass 1: from the upper endpoint's row */
+pcs_status pcs_session_level_pass(pcs_session* s, int32_t pass);
+/* device pointer to the level's int64 key array (num_keys entries; MIN-reduce across ranks) */
+pcs_status pcs_session_keys(pcs_session* s, void** device_ptr, int64_t* count);
+pcs_status pcs_session_level_end(pcs_session* s);
+pcs_status pcs_session_finish(pcs_session* s, pcs_result** out);
+void pcs_session_free(pcs_session* s);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PCSTABLE_B200_H */

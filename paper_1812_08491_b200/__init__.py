@@ -1,0 +1,479 @@
+"""pcstable_b200 -- B200-native PC-stable skeleton discovery (cuPC), Python host side.
+
+Mirrors the reference C++ API of proj/include/pcstable (same names, argument
+meaning and error behaviour) on top of the C ABI in include/pcstable_b200.h,
+implemented by the in-tree CUDA library libpcstable_b200.so (sm_100a).  There
+is no CPU fallback: every call below runs the device path and raises if the
+library or a GPU is missing.
+
+    compute_correlation(data)          stats.hpp:132   (FP64 DMMA Gram on the device)
+    threshold_tau(alpha, m, ell)       stats.hpp:120
+    run_pc_stable(c, m, cfg)           skeleton.hpp:341 -> SkeletonResult
+    run_pc_stable_data(data, cfg)      correlation + skeleton in one device pipeline
+    ci_test_batch / pseudo_inverse_batch   stats.hpp:366 / :172 on the device (parity helpers)
+    Session                            per-level stepping used by the multi-GPU driver
+"""
+from __future__ import annotations
+
+import ctypes as ct
+import enum
+import os
+from dataclasses import dataclass, field
+from typing import Iterator, Optional
+
+import numpy as np
+
+__all__ = [
+    "Strategy", "StopReason", "SkeletonConfig", "LevelStats", "SkeletonResult", "AdjacencyMatrix",
+    "SeparationSets", "ZeroVarianceError", "LevelUnreachableError", "PcsError", "compute_correlation",
+    "threshold_tau", "run_pc_stable", "run_pc_stable_data", "ci_test_batch", "pseudo_inverse_batch",
+    "Session", "library", "LIB_PATH",
+]
+
+PKG_DIR = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(PKG_DIR, "libpcstable_b200.so")
+
+# ----------------------------------------------------------------- errors
+PCS_OK, PCS_EINVAL, PCS_EZEROVAR, PCS_EOVERFLOW, PCS_ENAN, PCS_ECUDA, PCS_ENOMEM, PCS_EUNSUPPORTED, PCS_ELEVEL = range(9)
+
+
+class PcsError(RuntimeError):
+    """Device-side failure (CUDA error, out of memory, unsupported level)."""
+
+    def __init__(self, code: int, msg: str):
+        super().__init__(msg)
+        self.code = code
+
+
+class ZeroVarianceError(RuntimeError):
+    """pcstable::ZeroVarianceError (core.hpp:23-31)."""
+
+    def __init__(self, column: int, msg: str):
+        super().__init__(msg)
+        self.column = column
+
+
+class LevelUnreachableError(RuntimeError):
+    """pcstable::LevelUnreachableError (core.hpp:41-44)."""
+
+
+def _raise(code: int, column: int = -1):
+    msg = library().pcs_last_error().decode()
+    if code == PCS_EINVAL or code == PCS_ENAN:
+        raise ValueError(msg)  # std::invalid_argument
+    if code == PCS_EZEROVAR:
+        raise ZeroVarianceError(column, msg)
+    if code == PCS_EOVERFLOW:
+        raise OverflowError(msg)  # std::overflow_error
+    if code == PCS_ELEVEL:
+        raise LevelUnreachableError(msg)
+    raise PcsError(code, msg)
+
+
+# ----------------------------------------------------------------- ABI structs
+class _Config(ct.Structure):
+    _fields_ = [
+        ("alpha", ct.c_double), ("max_level", ct.c_int32), ("variant", ct.c_int32),
+        ("edges_per_unit", ct.c_int32), ("workers_per_edge", ct.c_int32), ("set_groups", ct.c_int32),
+        ("unit_width", ct.c_int32), ("device", ct.c_int32), ("shard_index", ct.c_int32),
+        ("shard_count", ct.c_int32), ("reserved", ct.c_int32 * 5),
+    ]
+
+
+class _Level(ct.Structure):
+    _fields_ = [
+        ("level", ct.c_int32), ("pad", ct.c_int32), ("ci_tests", ct.c_uint64), ("pseudo_inverses", ct.c_uint64),
+        ("edges_removed", ct.c_uint64), ("elapsed_s", ct.c_double), ("device_ci_tests", ct.c_uint64),
+        ("device_pseudo_inverses", ct.c_uint64), ("kernel_ms", ct.c_double),
+    ]
+
+
+_lib = None
+
+
+def library():
+    """Loads libpcstable_b200.so; raises if it was not built (no fallback)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} is missing: run __graft_entry__.build() (no CPU fallback exists)")
+    L = ct.CDLL(LIB_PATH)
+    dp, ip, vp = ct.POINTER(ct.c_double), ct.POINTER(ct.c_int32), ct.c_void_p
+    u8p = ct.POINTER(ct.c_uint8)
+    L.pcs_version.restype = ct.c_char_p
+    L.pcs_last_error.restype = ct.c_char_p
+    L.pcs_config_default.argtypes = [ct.POINTER(_Config)]
+    L.pcs_threshold_tau.argtypes = [ct.c_double, ct.c_int32, ct.c_int32, dp]
+    L.pcs_correlation.argtypes = [dp, ct.c_int32, ct.c_int32, dp, ip]
+    L.pcs_run_pc_stable.argtypes = [dp, ct.c_int32, ct.c_int32, ct.POINTER(_Config), ct.POINTER(vp)]
+    L.pcs_run_pc_stable_data.argtypes = [dp, ct.c_int32, ct.c_int32, ct.POINTER(_Config), ct.POINTER(vp), ip]
+    L.pcs_run_pc_stable_device.argtypes = [vp, ct.c_int64, ct.c_int32, ct.c_int32, ct.POINTER(_Config),
+                                           ct.POINTER(vp)]
+    L.pcs_result_p.argtypes = [vp]
+    L.pcs_result_levels.argtypes = [vp, ct.POINTER(_Level), ct.c_int32]
+    L.pcs_result_stop_reason.argtypes = [vp]
+    L.pcs_result_adjacency.argtypes = [vp, u8p]
+    L.pcs_result_edge_count.argtypes = [vp]
+    L.pcs_result_edge_count.restype = ct.c_int64
+    L.pcs_result_edge_list.argtypes = [vp, ip]
+    L.pcs_result_member_total.argtypes = [vp]
+    L.pcs_result_member_total.restype = ct.c_int64
+    L.pcs_result_sepsets.argtypes = [vp, ip, ct.POINTER(ct.c_int64), ip]
+    L.pcs_result_device_seconds.argtypes = [vp]
+    L.pcs_result_device_seconds.restype = ct.c_double
+    L.pcs_result_free.argtypes = [vp]
+    L.pcs_ci_test_batch.argtypes = [dp, ct.c_int32, ct.c_int32, ct.c_int64, ip, ip, ct.c_double, u8p, dp, dp, u8p]
+    L.pcs_pseudo_inverse_batch.argtypes = [dp, ct.c_int32, ct.c_int64, dp]
+    L.pcs_session_create.argtypes = [dp, ct.c_int32, ct.c_int32, ct.POINTER(_Config), ct.POINTER(vp)]
+    L.pcs_session_create_device.argtypes = [vp, ct.c_int64, ct.c_int32, ct.c_int32, ct.POINTER(_Config),
+                                            ct.POINTER(vp)]
+    L.pcs_session_level_begin.argtypes = [vp, ip, ip, ct.POINTER(ct.c_int64)]
+    L.pcs_session_level_pass.argtypes = [vp, ct.c_int32]
+    L.pcs_session_keys.argtypes = [vp, ct.POINTER(vp), ct.POINTER(ct.c_int64)]
+    L.pcs_session_level_end.argtypes = [vp]
+    L.pcs_session_finish.argtypes = [vp, ct.POINTER(vp)]
+    L.pcs_session_free.argtypes = [vp]
+    _lib = L
+    return L
+
+
+def version() -> str:
+    return library().pcs_version().decode()
+
+
+# ----------------------------------------------------------------- config / results
+class Strategy(enum.Enum):
+    """core.hpp:341.  Every strategy yields the Serial strategy's skeleton, sepsets and counters on the
+    device; EdgeParallel selects the cuPC-E kernels, SetShared (and Serial) the cuPC-S kernels."""
+    Serial = "serial"
+    EdgeParallel = "edge"
+    SetShared = "set"
+
+
+class StopReason(enum.Enum):  # skeleton.hpp:22-31
+    MaxDegreeReached = "max-degree"
+    LevelCapReached = "level-cap"
+    SampleSizeExhausted = "sample-size"
+
+
+_STOP = {0: StopReason.MaxDegreeReached, 1: StopReason.LevelCapReached, 2: StopReason.SampleSizeExhausted}
+
+
+@dataclass
+class SkeletonConfig:  # core.hpp:357-384
+    alpha: float = 0.05
+    max_level: Optional[int] = None
+    strategy: Strategy = Strategy.SetShared
+    edges_per_unit: int = 2
+    workers_per_edge: int = 32
+    set_groups: int = 2
+    unit_width: int = 64
+    worker_count: int = 1           # CPU knob of the reference; inert on the device
+    schedule_seed: Optional[int] = None  # inert: device results never depend on schedule
+    device: int = 0
+
+    def validate(self):  # core.hpp:370-383
+        if not (0.0 < self.alpha < 1.0):
+            raise ValueError("SkeletonConfig: alpha must lie in (0, 1)")
+        if self.max_level is not None and self.max_level < 0:
+            raise ValueError("SkeletonConfig: max_level must be >= 0")
+        for name in ("edges_per_unit", "workers_per_edge", "set_groups", "unit_width", "worker_count"):
+            if getattr(self, name) < 1:
+                raise ValueError(f"SkeletonConfig: {name} must be >= 1")
+
+    def _abi(self, shard_index: int = 0, shard_count: int = 1) -> _Config:
+        self.validate()
+        c = _Config()
+        library().pcs_config_default(ct.byref(c))
+        c.alpha = self.alpha
+        c.max_level = -1 if self.max_level is None else int(self.max_level)
+        c.variant = 1 if Strategy(self.strategy) == Strategy.EdgeParallel else 0
+        c.edges_per_unit, c.workers_per_edge = self.edges_per_unit, self.workers_per_edge
+        c.set_groups, c.unit_width = self.set_groups, self.unit_width
+        c.device, c.shard_index, c.shard_count = self.device, shard_index, shard_count
+        return c
+
+
+@dataclass
+class LevelStats:  # core.hpp:387-393 (+ device counters)
+    level: int
+    ci_tests: int
+    pseudo_inverses: int
+    edges_removed: int
+    elapsed_s: float
+    device_ci_tests: int = 0
+    device_pseudo_inverses: int = 0
+    kernel_ms: float = 0.0
+
+
+class AdjacencyMatrix:
+    """Read-only view with the reference's accessors (core.hpp:109-194)."""
+
+    def __init__(self, cells: np.ndarray):
+        self.cells = cells
+
+    def size(self) -> int:
+        return self.cells.shape[0]
+
+    def at(self, i: int, j: int) -> bool:
+        return bool(self.cells[i, j])
+
+    def edge_count(self) -> int:
+        return int(np.triu(self.cells, 1).sum())
+
+    def __eq__(self, other) -> bool:
+        return isinstance(other, AdjacencyMatrix) and np.array_equal(self.cells, other.cells)
+
+
+class SeparationSets:
+    """Sepsets keyed by unordered pair (core.hpp:267-339)."""
+
+    def __init__(self, n: int, sets: dict):
+        self.n = n
+        self._sets = sets
+
+    def size(self) -> int:
+        return self.n
+
+    def find(self, i: int, j: int):
+        if i == j or not (0 <= i < self.n and 0 <= j < self.n):
+            raise ValueError("SeparationSets: invalid vertex pair")
+        return self._sets.get((min(i, j), max(i, j)))
+
+    def stored_count(self) -> int:
+        return len(self._sets)
+
+    def for_each(self) -> Iterator:
+        for k in sorted(self._sets):
+            yield k[0], k[1], self._sets[k]
+
+    def as_dict(self) -> dict:
+        return dict(self._sets)
+
+
+@dataclass
+class SkeletonResult:  # skeleton.hpp:33-40
+    skeleton: AdjacencyMatrix
+    sepsets: SeparationSets
+    levels: list = field(default_factory=list)
+    stop_reason: StopReason = StopReason.MaxDegreeReached
+    device_seconds: float = 0.0
+
+    def levels_run(self) -> int:
+        return len(self.levels)
+
+    def edge_set(self):
+        iu = np.argwhere(np.triu(self.skeleton.cells, 1))
+        return [tuple(map(int, e)) for e in iu]
+
+
+def _dp(a):
+    return a.ctypes.data_as(ct.POINTER(ct.c_double))
+
+
+def _ip(a):
+    return a.ctypes.data_as(ct.POINTER(ct.c_int32))
+
+
+def _collect(h, with_sepsets: bool = True) -> SkeletonResult:
+    L = library()
+    p = L.pcs_result_p(h)
+    lv = (_Level * 256)()
+    n = L.pcs_result_levels(h, lv, 256)
+    levels = [LevelStats(lv[k].level, lv[k].ci_tests, lv[k].pseudo_inverses, lv[k].edges_removed, lv[k].elapsed_s,
+                         lv[k].device_ci_tests, lv[k].device_pseudo_inverses, lv[k].kernel_ms) for k in range(n)]
+    adj = np.empty((p, p), np.uint8)
+    L.pcs_result_adjacency(h, adj.ctypes.data_as(ct.POINTER(ct.c_uint8)))
+    sets = {}
+    if with_sepsets:
+        ns = p * (p - 1) // 2
+        tot = L.pcs_result_member_total(h)
+        lvl = np.empty(ns, np.int32)
+        off = np.empty(ns, np.int64)
+        mem = np.empty(max(tot, 1), np.int32)
+        L.pcs_result_sepsets(h, _ip(lvl), off.ctypes.data_as(ct.POINTER(ct.c_int64)), _ip(mem))
+        iu, ju = np.triu_indices(p, 1)
+        for s in np.nonzero(lvl >= 0)[0]:
+            sets[(int(iu[s]), int(ju[s]))] = tuple(int(v) for v in mem[off[s]:off[s] + lvl[s]])
+    return SkeletonResult(AdjacencyMatrix(adj), SeparationSets(p, sets), levels, _STOP[L.pcs_result_stop_reason(h)],
+                          L.pcs_result_device_seconds(h))
+
+
+# ----------------------------------------------------------------- API
+def threshold_tau(alpha: float, m: int, ell: int) -> float:
+    out = ct.c_double()
+    rc = library().pcs_threshold_tau(alpha, m, ell, ct.byref(out))
+    if rc:
+        _raise(rc)
+    return out.value
+
+
+def _data_colmajor(data) -> tuple[np.ndarray, int, int]:
+    """data: (m, p) samples x variables, like DataMatrix (core.hpp:48-67)."""
+    x = np.asarray(data, np.float64)
+    if x.ndim != 2:
+        raise ValueError("DataMatrix: need a 2-D array (samples x variables)")
+    m, p = x.shape
+    return np.asfortranarray(x), m, p
+
+
+def compute_correlation(data) -> np.ndarray:
+    """stats::compute_correlation on the device; returns the p x p correlation matrix."""
+    x, m, p = _data_colmajor(data)
+    c = np.empty((p, p), np.float64)
+    col = ct.c_int32(-1)
+    rc = library().pcs_correlation(_dp(x), m, p, _dp(c), ct.byref(col))
+    if rc:
+        _raise(rc, col.value)
+    return c
+
+
+def run_pc_stable(c, sample_count: int, cfg: Optional[SkeletonConfig] = None, with_sepsets: bool = True
+                  ) -> SkeletonResult:
+    """run_pc_stable (skeleton.hpp:341-391) on the device."""
+    cfg = cfg or SkeletonConfig()
+    c = np.ascontiguousarray(c, np.float64)
+    if c.ndim != 2 or c.shape[0] != c.shape[1]:
+        raise ValueError("CorrelationMatrix: need a square matrix, n >= 2")
+    abi = cfg._abi()
+    h = ct.c_void_p()
+    rc = library().pcs_run_pc_stable(_dp(c), c.shape[0], int(sample_count), ct.byref(abi), ct.byref(h))
+    if rc:
+        _raise(rc)
+    try:
+        return _collect(h, with_sepsets)
+    finally:
+        library().pcs_result_free(h)
+
+
+def run_pc_stable_data(data, cfg: Optional[SkeletonConfig] = None, with_sepsets: bool = True) -> SkeletonResult:
+    """compute_correlation + run_pc_stable in one device pipeline (bench.hpp:107-113 shape)."""
+    cfg = cfg or SkeletonConfig()
+    x, m, p = _data_colmajor(data)
+    abi = cfg._abi()
+    h = ct.c_void_p()
+    col = ct.c_int32(-1)
+    rc = library().pcs_run_pc_stable_data(_dp(x), m, p, ct.byref(abi), ct.byref(h), ct.byref(col))
+    if rc:
+        _raise(rc, col.value)
+    try:
+        return _collect(h, with_sepsets)
+    finally:
+        library().pcs_result_free(h)
+
+
+def run_pc_stable_device(c_ptr: int, ldc: int, p: int, sample_count: int, cfg: Optional[SkeletonConfig] = None,
+                         with_sepsets: bool = False) -> SkeletonResult:
+    """run_pc_stable on a correlation matrix already resident in device memory."""
+    cfg = cfg or SkeletonConfig()
+    abi = cfg._abi()
+    h = ct.c_void_p()
+    rc = library().pcs_run_pc_stable_device(ct.c_void_p(c_ptr), ldc, p, int(sample_count), ct.byref(abi),
+                                            ct.byref(h))
+    if rc:
+        _raise(rc)
+    try:
+        return _collect(h, with_sepsets)
+    finally:
+        library().pcs_result_free(h)
+
+
+def ci_test_batch(c, ell: int, ij, sets, tau: float):
+    """stats::ci_test for many (i, j | S) of one level on the device.
+    Returns (independent, z, rho, degenerate) arrays."""
+    c = np.ascontiguousarray(c, np.float64)
+    ij = np.ascontiguousarray(ij, np.int32).reshape(-1, 2)
+    n = ij.shape[0]
+    sets = np.ascontiguousarray(sets if ell > 0 else np.zeros((n, 1)), np.int32).reshape(n, max(ell, 1))
+    ind = np.empty(n, np.uint8)
+    deg = np.empty(n, np.uint8)
+    z = np.empty(n, np.float64)
+    rho = np.empty(n, np.float64)
+    u8 = ct.POINTER(ct.c_uint8)
+    rc = library().pcs_ci_test_batch(_dp(c), c.shape[0], ell, n, _ip(ij), _ip(sets), tau, ind.ctypes.data_as(u8),
+                                     _dp(z), _dp(rho), deg.ctypes.data_as(u8))
+    if rc:
+        _raise(rc)
+    return ind.astype(bool), z, rho, deg.astype(bool)
+
+
+def pseudo_inverse_batch(a) -> np.ndarray:
+    """stats::pseudo_inverse for a stack (n, ell, ell) on the device."""
+    a = np.ascontiguousarray(a, np.float64)
+    if a.ndim == 2:
+        a = a[None]
+    n, ell, _ = a.shape
+    out = np.empty_like(a)
+    rc = library().pcs_pseudo_inverse_batch(_dp(a), ell, n, _dp(out))
+    if rc:
+        _raise(rc)
+    return out
+
+
+class Session:
+    """Level-stepped skeleton run (pcs_session_*).  Multi-GPU: every rank creates a session with
+    shard_index/shard_count, runs each pass on its shard, and MIN-all-reduces keys() in between
+    (see paper_1812_08491_b200/multigpu.py)."""
+
+    def __init__(self, c=None, sample_count: int = 0, cfg: Optional[SkeletonConfig] = None, shard_index: int = 0,
+                 shard_count: int = 1, device_ptr: Optional[int] = None, ldc: Optional[int] = None,
+                 p: Optional[int] = None):
+        cfg = cfg or SkeletonConfig()
+        abi = cfg._abi(shard_index, shard_count)
+        self._h = ct.c_void_p()
+        L = library()
+        if device_ptr is not None:
+            rc = L.pcs_session_create_device(ct.c_void_p(device_ptr), ldc, p, int(sample_count), ct.byref(abi),
+                                             ct.byref(self._h))
+        else:
+            c = np.ascontiguousarray(c, np.float64)
+            rc = L.pcs_session_create(_dp(c), c.shape[0], int(sample_count), ct.byref(abi), ct.byref(self._h))
+        if rc:
+            self._h = None
+            _raise(rc)
+
+    def level_begin(self) -> tuple[bool, int, int]:
+        running, ell, nk = ct.c_int32(), ct.c_int32(), ct.c_int64()
+        rc = library().pcs_session_level_begin(self._h, ct.byref(running), ct.byref(ell), ct.byref(nk))
+        if rc:
+            _raise(rc)
+        return bool(running.value), ell.value, nk.value
+
+    def level_pass(self, pass_index: int):
+        rc = library().pcs_session_level_pass(self._h, pass_index)
+        if rc:
+            _raise(rc)
+
+    def keys(self) -> tuple[int, int]:
+        ptr, n = ct.c_void_p(), ct.c_int64()
+        rc = library().pcs_session_keys(self._h, ct.byref(ptr), ct.byref(n))
+        if rc:
+            _raise(rc)
+        return ptr.value or 0, n.value
+
+    def level_end(self):
+        rc = library().pcs_session_level_end(self._h)
+        if rc:
+            _raise(rc)
+
+    def finish(self, with_sepsets: bool = True) -> SkeletonResult:
+        h = ct.c_void_p()
+        rc = library().pcs_session_finish(self._h, ct.byref(h))
+        if rc:
+            _raise(rc)
+        try:
+            return _collect(h, with_sepsets)
+        finally:
+            library().pcs_result_free(h)
+
+    def close(self):
+        if self._h:
+            library().pcs_session_free(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

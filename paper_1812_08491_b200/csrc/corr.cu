@@ -1,0 +1,193 @@
+// corr.cu -- correlation build (stats::compute_correlation, stats.hpp:132-156) and
+// CorrelationMatrix validation (core.hpp:73-95) on the device.
+//
+//   colmean_kernel   column means of the m x p (Eigen column-major) data + finiteness
+//   center_kernel    Xc = X - mean  (the centred temporary of stats.hpp:136)
+//   gram_dmma_kernel G = Xc' Xc on the FP64 tensor cores (mma.sync m8n8k4 f64 ->
+//                    SASS DMMA), upper-triangular 64x64 tiles only (SYRK)
+//   corr_finalize    sd = sqrt(diag G) (ZeroVarianceError), c = clamp(g/(sd_i sd_j))
+//   normalize_kernel CorrelationMatrix ctor for user-supplied correlation input
+#include "pcs_internal.h"
+
+namespace pcs {
+
+// err flag bits
+constexpr int kErrNonFinite = 1;
+constexpr int kErrDiag = 2;
+constexpr int kErrAsym = 4;
+constexpr int kErrRange = 8;
+
+// ------------------------------------------------ CorrelationMatrix ctor
+__global__ void normalize_kernel(double* C, long long ldc, int p, int* err) {
+    const long long n = (long long)p * p;
+    for (long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += (long long)gridDim.x * blockDim.x) {
+        const int i = (int)(k / p), j = (int)(k % p);
+        if (i == j) {
+            if (fabs(C[(size_t)i * ldc + i] - 1.0) > 1e-12) atomicOr(err, kErrDiag);
+            continue;
+        }
+        if (i > j) continue;
+        const double a = C[(size_t)i * ldc + j], b = C[(size_t)j * ldc + i];
+        if (!isfinite(a) || !isfinite(b) || fabs(a - b) > 1e-12) { atomicOr(err, kErrAsym); continue; }
+        double v = 0.5 * (a + b);
+        if (fabs(v) > 1.0 + 1e-12) { atomicOr(err, kErrRange); continue; }
+        v = v < -1.0 ? -1.0 : (v > 1.0 ? 1.0 : v);
+        C[(size_t)i * ldc + j] = v;
+        C[(size_t)j * ldc + i] = v;
+    }
+}
+
+__global__ void set_diag_kernel(double* C, long long ldc, int p) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < p) C[(size_t)i * ldc + i] = 1.0;
+}
+
+void launch_normalize_corr(double* C, long long ldc, int p, int* err, cudaStream_t s) {
+    long long n = (long long)p * p;
+    long long blocks = (n + 255) / 256;
+    if (blocks > 148 * 16) blocks = 148 * 16;
+    normalize_kernel<<<(int)blocks, 256, 0, s>>>(C, ldc, p, err);
+    set_diag_kernel<<<(p + 255) / 256, 256, 0, s>>>(C, ldc, p);
+}
+
+// ------------------------------------------------ correlation build
+__global__ void colmean_kernel(const double* __restrict__ X, int m, int p, double* mean, int* err) {
+    const int j = blockIdx.x;
+    const double* col = X + (size_t)j * m;
+    double s = 0.0;
+    bool bad = false;
+    for (int r = threadIdx.x; r < m; r += blockDim.x) {
+        const double v = col[r];
+        bad |= !isfinite(v);
+        s += v;
+    }
+    __shared__ double red[256];
+    red[threadIdx.x] = s;
+    __syncthreads();
+    for (int d = blockDim.x / 2; d > 0; d >>= 1) {
+        if (threadIdx.x < d) red[threadIdx.x] += red[threadIdx.x + d];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) mean[j] = red[0] / m;
+    if (bad) atomicOr(err, kErrNonFinite);
+}
+
+// Xc row-major p x ldk (ldk = m rounded up to the k-tile; the tail is zero)
+__global__ void center_kernel(const double* __restrict__ X, int m, int p, const double* __restrict__ mean,
+                              double* __restrict__ Xc, int ldk) {
+    const long long n = (long long)p * ldk;
+    for (long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += (long long)gridDim.x * blockDim.x) {
+        const int j = (int)(k / ldk), r = (int)(k % ldk);
+        Xc[k] = r < m ? X[(size_t)j * m + r] - mean[j] : 0.0;
+    }
+}
+
+constexpr int kGT = 64;      // output tile
+constexpr int kGK = 32;      // k chunk
+constexpr int kGPad = 36;    // smem row stride (doubles): 4 mod 16 -> conflict-free 8x4 fragment loads
+
+__device__ __forceinline__ void dmma_8x8x4(double (&d)[2], double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                 : "+d"(d[0]), "+d"(d[1])
+                 : "d"(a), "d"(b));
+}
+
+// 4 warps (2 x 2), each owning a 32 x 32 sub-tile = 4 x 4 DMMA tiles of 8 x 8.
+__global__ void __launch_bounds__(128) gram_dmma_kernel(const double* __restrict__ Xc, int p, int ldk,
+                                                        double* __restrict__ G, long long ldg) {
+    const int bi = blockIdx.y, bj = blockIdx.x;
+    if (bi > bj) return;  // symmetric: upper tiles only
+    __shared__ __align__(16) double sA[kGT * kGPad];
+    __shared__ __align__(16) double sB[kGT * kGPad];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int wm = warp >> 1, wn = warp & 1;
+    const int g = lane >> 2, t = lane & 3;
+    const int i0 = bi * kGT, j0 = bj * kGT;
+    double acc[4][4][2];
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+    for (int k0 = 0; k0 < ldk; k0 += kGK) {
+        // 64 rows x 32 doubles per operand = 1024 double2; 8 per thread
+#pragma unroll
+        for (int v = 0; v < 8; ++v) {
+            const int idx = tid + v * 128;
+            const int r = idx >> 4, c = (idx & 15) * 2;
+            double2 xa = make_double2(0.0, 0.0), xb = make_double2(0.0, 0.0);
+            if (i0 + r < p) xa = *reinterpret_cast<const double2*>(Xc + (size_t)(i0 + r) * ldk + k0 + c);
+            if (j0 + r < p) xb = *reinterpret_cast<const double2*>(Xc + (size_t)(j0 + r) * ldk + k0 + c);
+            *reinterpret_cast<double2*>(sA + r * kGPad + c) = xa;
+            *reinterpret_cast<double2*>(sB + r * kGPad + c) = xb;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int kk = 0; kk < kGK; kk += 4) {
+            double fa[4], fb[4];
+#pragma unroll
+            for (int a = 0; a < 4; ++a) fa[a] = sA[(wm * 32 + a * 8 + g) * kGPad + kk + t];
+#pragma unroll
+            for (int b = 0; b < 4; ++b) fb[b] = sB[(wn * 32 + b * 8 + g) * kGPad + kk + t];
+#pragma unroll
+            for (int a = 0; a < 4; ++a)
+#pragma unroll
+                for (int b = 0; b < 4; ++b) dmma_8x8x4(acc[a][b], fa[a], fb[b]);
+        }
+        __syncthreads();
+    }
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+            const int r = i0 + wm * 32 + a * 8 + g;
+            const int c = j0 + wn * 32 + b * 8 + 2 * t;
+            if (r < p && c < p) G[(size_t)r * ldg + c] = acc[a][b][0];
+            if (r < p && c + 1 < p) G[(size_t)r * ldg + c + 1] = acc[a][b][1];
+        }
+}
+
+// sd, ZeroVarianceError (lowest column index wins, like the reference loop), clamp
+__global__ void corr_sd_kernel(const double* G, long long ldg, int p, double* sd, int* zero_col) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= p) return;
+    const double ss = G[(size_t)i * ldg + i];
+    if (!(ss > 0.0)) atomicMin(zero_col, i);
+    sd[i] = sqrt(ss);
+}
+
+__global__ void corr_finalize_kernel(const double* __restrict__ G, long long ldg, int p, const double* __restrict__ sd,
+                                     double* __restrict__ C, long long ldc) {
+    const long long n = (long long)p * p;
+    for (long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += (long long)gridDim.x * blockDim.x) {
+        const int i = (int)(k / p), j = (int)(k % p);
+        double v;
+        if (i == j) v = 1.0;
+        else {
+            const int a = i < j ? i : j, b = i < j ? j : i;  // gram(i, j) with i < j (stats.hpp:150)
+            v = G[(size_t)a * ldg + b] / (sd[a] * sd[b]);
+            v = v < -1.0 ? -1.0 : (v > 1.0 ? 1.0 : v);
+        }
+        C[(size_t)i * ldc + j] = v;
+    }
+}
+
+// X: m x p column-major (device).  Scratch: Xc (p x ldk), G (p x ldg), mean (p), err_flags[2] = {flags, zero_col}
+void launch_correlation(const double* X, int m, int p, double* Xc, double* G, long long ldg, double* mean, double* C,
+                        long long ldc, int* err_flags, cudaStream_t s) {
+    const int ldk = (m + kGK - 1) / kGK * kGK;
+    colmean_kernel<<<p, 256, 0, s>>>(X, m, p, mean, err_flags);
+    long long n = (long long)p * ldk;
+    long long blocks = (n + 255) / 256;
+    if (blocks > 148 * 32) blocks = 148 * 32;
+    center_kernel<<<(int)blocks, 256, 0, s>>>(X, m, p, mean, Xc, ldk);
+    const int nb = (p + kGT - 1) / kGT;
+    gram_dmma_kernel<<<dim3(nb, nb), 128, 0, s>>>(Xc, p, ldk, G, ldg);
+    double* sd = mean;  // mean is dead after centring
+    corr_sd_kernel<<<(p + 255) / 256, 256, 0, s>>>(G, ldg, p, sd, err_flags + 1);
+    n = (long long)p * p;
+    blocks = (n + 255) / 256;
+    if (blocks > 148 * 32) blocks = 148 * 32;
+    corr_finalize_kernel<<<(int)blocks, 256, 0, s>>>(G, ldg, p, sd, C, ldc);
+}
+
+}  // namespace pcs

@@ -1,0 +1,814 @@
+// host.cu -- host driver and C ABI of libpcstable_b200.so.
+//
+// The level loop of run_pc_stable (skeleton.hpp:341-391) runs on the host; every
+// level's work runs on the device:
+//   level 0   : level0_kernel (bitmask)                               skeleton.hpp:262-288
+//   level >= 1: snapshot (degree, scan, fill, edge index)             core.hpp:227-239
+//               pass 0 / pass 1 CI-test kernels (keys, atomicMin)     skeleton.hpp:131-222
+//               commit (removals, sepsets, serial-equivalent counts)  skeleton.hpp:123-129
+// Stop conditions in the reference's order: level cap, sample size, max degree
+// (skeleton.hpp:353-373).
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/pcstable_b200.h"
+#include "pcs_internal.h"
+
+using namespace pcs;
+
+namespace {
+
+thread_local std::string g_err;
+
+pcs_status fail(pcs_status st, const std::string& msg) {
+    g_err = msg;
+    return st;
+}
+
+#define CUDA_TRY(expr)                                                                      \
+    do {                                                                                    \
+        cudaError_t e_ = (expr);                                                            \
+        if (e_ != cudaSuccess)                                                              \
+            return fail(PCS_ECUDA, std::string(#expr) + ": " + cudaGetErrorString(e_));     \
+    } while (0)
+
+double now_s() {
+    return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+
+// ----------------------------------------------------------- stats on the host
+// Wichura AS 241, same coefficients and Horner order as stats.hpp:19-108
+const double kA[8] = {3.3871328727963666080e0, 1.3314166789178437745e2, 1.9715909503065514427e3,
+                      1.3731693765509461125e4, 4.5921953931549871457e4, 6.7265770927008700853e4,
+                      3.3430575583588128105e4, 2.5090809287301226727e3};
+const double kB[8] = {1.0, 4.2313330701600911252e1, 6.8718700749205790830e2, 5.3941960214247511077e3,
+                      2.1213794301586595867e4, 3.9307895800092710610e4, 2.8729085735721942674e4,
+                      5.2264952788528545610e3};
+const double kC[8] = {1.42343711074968357734e0, 4.63033784615654529590e0, 5.76949722146069140550e0,
+                      3.64784832476320460504e0, 1.27045825245236838258e0, 2.41780725177450611770e-1,
+                      2.27238449892691845833e-2, 7.74545014278341407640e-4};
+const double kD[8] = {1.0, 2.05319162663775882187e0, 1.67638483018380384940e0, 6.89767334985100004550e-1,
+                      1.48103976427480074590e-1, 1.51986665636164571966e-2, 5.47593808499534494600e-4,
+                      1.05075007164441684324e-9};
+const double kE[8] = {6.65790464350110377720e0, 5.46378491116411436990e0, 1.78482653991729133580e0,
+                      2.96560571828504891230e-1, 2.65321895265761230930e-2, 1.24266094738807843860e-3,
+                      2.71155556874348757815e-5, 2.01033439929228813265e-7};
+const double kF[8] = {1.0, 5.99832206555887937690e-1, 1.36929880922735805310e-1, 1.48753612908506148525e-2,
+                      7.86869131145613259100e-4, 1.84631831751005468180e-5, 1.42151175831644588870e-7,
+                      2.04426310338993978564e-15};
+
+double horner7(const double* k, double r) {
+    double acc = k[7] * r + k[6];
+    for (int d = 5; d >= 0; --d) acc = acc * r + k[d];
+    return acc;
+}
+
+double normal_quantile(double p) {  // caller guarantees 0 < p < 1
+    const double q = p - 0.5;
+    if (std::fabs(q) <= 0.425) {
+        const double r = 0.180625 - q * q;
+        return q * horner7(kA, r) / horner7(kB, r);
+    }
+    double r = q < 0.0 ? p : 1.0 - p;
+    r = std::sqrt(-std::log(r));
+    double z;
+    if (r <= 5.0) {
+        r -= 1.6;
+        z = horner7(kC, r) / horner7(kD, r);
+    } else {
+        r -= 5.0;
+        z = horner7(kE, r) / horner7(kF, r);
+    }
+    return q < 0.0 ? -z : z;
+}
+
+pcs_status threshold_tau(double alpha, int m, int ell, double* tau) {
+    if (!(alpha > 0.0 && alpha <= 1.0)) return fail(PCS_EINVAL, "threshold_tau: alpha must lie in (0, 1]");
+    if (ell < 0) return fail(PCS_EINVAL, "threshold_tau: ell must be >= 0");
+    const double dof = static_cast<double>(m) - ell - 3;
+    if (dof < 1.0)
+        return fail(PCS_ELEVEL, "threshold_tau: need m - ell - 3 >= 1, got m = " + std::to_string(m) +
+                                    ", ell = " + std::to_string(ell));
+    *tau = normal_quantile(1.0 - alpha / 2.0) / std::sqrt(dof);
+    return PCS_OK;
+}
+
+// Certain-decision bands around tanh(tau): z <= tau - delta  <=>  |rho| <= tanh(tau - delta).
+Thresholds make_thresholds(double tau) {
+    Thresholds th;
+    th.tau = tau;
+    const long double delta = std::max<long double>(1e-9L * tau, 1e-14L);
+    const long double tl = (long double)tau - delta, tu = (long double)tau + delta;
+    const long double zclamp = 0.5L * std::log((2.0L - 1e-12L) / 1e-12L);  // z at the rho clamp
+    if (tl > 0) {
+        const long double t = std::tanh(tl);
+        th.lo = (double)t;
+        th.lo2 = (double)(t * t);
+    } else {
+        th.lo = -1.0;
+        th.lo2 = -1.0;
+    }
+    if (tu < zclamp - 1e-6L) {
+        const long double t = std::tanh(tu);
+        th.hi = (double)t;
+        th.hi2 = (double)(t * t);
+    } else {
+        th.hi = INFINITY;
+        th.hi2 = INFINITY;
+    }
+    return th;
+}
+
+// exact C(n, k) with overflow report (comb.hpp:35-46)
+bool binomial_exact(int n, int k, unsigned long long* out) {
+    if (k < 0 || k > n) { *out = 0; return true; }
+    if (n - k < k) k = n - k;
+    unsigned __int128 r = 1;
+    for (int i = 1; i <= k; ++i) {
+        r = r * (unsigned)(n - k + i) / (unsigned)i;
+        if (r > (unsigned __int128)UINT64_MAX) return false;
+    }
+    *out = (unsigned long long)r;
+    return true;
+}
+
+}  // namespace
+
+// ================================================================ result
+struct pcs_result {
+    int p = 0;
+    int W = 0;
+    int stop_reason = PCS_STOP_MAX_DEGREE;
+    std::vector<pcs_level_stats> levels;
+    std::vector<uint32_t> adj;                 // final live bitmask, p x W
+    std::vector<int32_t> recs;                 // flattened (a, b, ell, members...) of level >= 1 removals
+    double device_seconds = 0.0;
+};
+
+// ================================================================ session
+struct pcs_session {
+    int p = 0, m = 0, W = 0;
+    long long ldc = 0;
+    pcs_config cfg{};
+    int device = 0, num_sms = 148;
+    cudaStream_t st = nullptr;
+    cudaEvent_t ev_begin = nullptr, ev_end = nullptr, ev_k0 = nullptr, ev_k1 = nullptr;
+    bool own_c = true;
+    double* dC = nullptr;
+    uint32_t* dAdj = nullptr;
+    int32_t *dDeg = nullptr, *dLow = nullptr, *dOff = nullptr, *dUp = nullptr;
+    SnapInfo* dInfo = nullptr;
+    Counters* dCnt = nullptr;
+    unsigned long long* dPrefix = nullptr;
+    int32_t *dNbr = nullptr, *dEid = nullptr;
+    long long capDir = 0;
+    int32_t *dEuA = nullptr, *dEuQa = nullptr, *dEuQb = nullptr;
+    unsigned long long* dKeys = nullptr;
+    long long capUnd = 0;
+    int32_t* dRec = nullptr;
+    long long capRec = 0;
+    unsigned long long* dBinom = nullptr;
+    size_t capBinom = 0;
+    // level state
+    int ell = -1;
+    bool stopped = false, in_level = false;
+    int stop_reason = PCS_STOP_MAX_DEGREE;
+    SnapInfo info{};
+    Thresholds th{};
+    int binom_stride = 0;
+    double t_level = 0.0;
+    float kernel_ms = 0.f;
+    bool kernel_timing = false;
+    std::vector<pcs_level_stats> levels;
+    std::vector<int32_t> recs;
+};
+
+namespace {
+
+void free_session(pcs_session* s) {
+    if (!s) return;
+    cudaSetDevice(s->device);
+    if (s->st) cudaStreamSynchronize(s->st);
+    if (s->own_c) cudaFree(s->dC);
+    cudaFree(s->dAdj); cudaFree(s->dDeg); cudaFree(s->dLow); cudaFree(s->dOff); cudaFree(s->dUp);
+    cudaFree(s->dInfo); cudaFree(s->dCnt); cudaFree(s->dPrefix); cudaFree(s->dNbr); cudaFree(s->dEid);
+    cudaFree(s->dEuA); cudaFree(s->dEuQa); cudaFree(s->dEuQb); cudaFree(s->dKeys); cudaFree(s->dRec);
+    cudaFree(s->dBinom);
+    if (s->ev_begin) cudaEventDestroy(s->ev_begin);
+    if (s->ev_end) cudaEventDestroy(s->ev_end);
+    if (s->ev_k0) cudaEventDestroy(s->ev_k0);
+    if (s->ev_k1) cudaEventDestroy(s->ev_k1);
+    if (s->st) cudaStreamDestroy(s->st);
+    delete s;
+}
+
+pcs_status validate_config(const pcs_config* c) {  // core.hpp:370-383
+    if (!c) return fail(PCS_EINVAL, "null config");
+    if (!(c->alpha > 0.0 && c->alpha < 1.0)) return fail(PCS_EINVAL, "SkeletonConfig: alpha must lie in (0, 1)");
+    if (c->max_level < -1) return fail(PCS_EINVAL, "SkeletonConfig: max_level must be >= 0");
+    if (c->edges_per_unit < 1) return fail(PCS_EINVAL, "SkeletonConfig: edges_per_unit must be >= 1");
+    if (c->workers_per_edge < 1) return fail(PCS_EINVAL, "SkeletonConfig: workers_per_edge must be >= 1");
+    if (c->set_groups < 1) return fail(PCS_EINVAL, "SkeletonConfig: set_groups must be >= 1");
+    if (c->unit_width < 1) return fail(PCS_EINVAL, "SkeletonConfig: unit_width must be >= 1");
+    if (c->variant != PCS_VARIANT_SET && c->variant != PCS_VARIANT_EDGE)
+        return fail(PCS_EINVAL, "SkeletonConfig: unknown device variant");
+    if (c->shard_count < 1 || c->shard_index < 0 || c->shard_index >= c->shard_count)
+        return fail(PCS_EINVAL, "SkeletonConfig: bad shard index/count");
+    return PCS_OK;
+}
+
+template <class T>
+pcs_status realloc_dev(T** ptr, long long n) {
+    cudaFree(*ptr);
+    *ptr = nullptr;
+    CUDA_TRY(cudaMalloc(ptr, sizeof(T) * (size_t)std::max<long long>(n, 1)));
+    return PCS_OK;
+}
+
+pcs_status session_alloc(pcs_session* s) {
+    const int p = s->p;
+    s->W = (p + 31) / 32;
+    CUDA_TRY(cudaStreamCreateWithFlags(&s->st, cudaStreamNonBlocking));
+    CUDA_TRY(cudaEventCreate(&s->ev_begin));
+    CUDA_TRY(cudaEventCreate(&s->ev_end));
+    CUDA_TRY(cudaEventCreate(&s->ev_k0));
+    CUDA_TRY(cudaEventCreate(&s->ev_k1));
+    CUDA_TRY(cudaMalloc(&s->dAdj, sizeof(uint32_t) * (size_t)p * s->W));
+    CUDA_TRY(cudaMalloc(&s->dDeg, sizeof(int32_t) * (size_t)(p + 1)));
+    CUDA_TRY(cudaMalloc(&s->dLow, sizeof(int32_t) * (size_t)(p + 1)));
+    CUDA_TRY(cudaMalloc(&s->dOff, sizeof(int32_t) * (size_t)(p + 1)));
+    CUDA_TRY(cudaMalloc(&s->dUp, sizeof(int32_t) * (size_t)(p + 1)));
+    CUDA_TRY(cudaMalloc(&s->dInfo, sizeof(SnapInfo)));
+    CUDA_TRY(cudaMalloc(&s->dCnt, sizeof(Counters)));
+    CUDA_TRY(cudaMalloc(&s->dPrefix, sizeof(unsigned long long) * (size_t)(p + 1)));
+    return PCS_OK;
+}
+
+pcs_status session_new(int p, int m, const pcs_config* cfg, pcs_session** out) {
+    *out = nullptr;
+    pcs_status st = validate_config(cfg);
+    if (st) return st;
+    if (m < 4) return fail(PCS_EINVAL, "run_pc_stable: need at least 4 samples");
+    if (p < 2) return fail(PCS_EINVAL, "CorrelationMatrix: need a square matrix, n >= 2");
+    if (p > 46340) return fail(PCS_EINVAL, "AdjacencyMatrix: n * n must fit Index (int32), n <= 46340");
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) return fail(PCS_ECUDA, "no CUDA device available");
+    if (cfg->device < 0 || cfg->device >= ndev) return fail(PCS_EINVAL, "bad CUDA device ordinal");
+    CUDA_TRY(cudaSetDevice(cfg->device));
+    auto* s = new pcs_session();
+    s->p = p;
+    s->m = m;
+    s->cfg = *cfg;
+    s->device = cfg->device;
+    cudaDeviceGetAttribute(&s->num_sms, cudaDevAttrMultiProcessorCount, s->device);
+    st = session_alloc(s);
+    if (st) { free_session(s); return st; }
+    *out = s;
+    return PCS_OK;
+}
+
+pcs_status check_level_errors(pcs_session* s, const Counters& c) {
+    if (c.err_nan) return fail(PCS_ENAN, "fisher_z: rho must lie in (-1, 1)");
+    (void)s;
+    return PCS_OK;
+}
+
+pcs_status build_binomials(pcs_session* s, int ell, int maxw) {
+    const int stride = maxw + 1;
+    std::vector<unsigned long long> t((size_t)(ell + 1) * stride, 0ull);
+    for (int n = 0; n < stride; ++n) t[n] = 1ull;
+    for (int k = 1; k <= ell; ++k)
+        for (int n = 1; n < stride; ++n) {
+            const unsigned long long a = t[(size_t)(k - 1) * stride + n - 1], b = t[(size_t)k * stride + n - 1];
+            t[(size_t)k * stride + n] = (a > UINT64_MAX - b) ? UINT64_MAX : a + b;
+        }
+    if (t.size() > s->capBinom) {
+        pcs_status st = realloc_dev(&s->dBinom, (long long)t.size());
+        if (st) return st;
+        s->capBinom = t.size();
+    }
+    CUDA_TRY(cudaMemcpyAsync(s->dBinom, t.data(), sizeof(unsigned long long) * t.size(), cudaMemcpyHostToDevice,
+                             s->st));
+    s->binom_stride = stride;
+    return PCS_OK;
+}
+
+LevelArgs level_args(pcs_session* s) {
+    LevelArgs A{};
+    A.C = s->dC;
+    A.ldc = s->ldc;
+    A.p = s->p;
+    A.ell = s->ell;
+    A.off = s->dOff;
+    A.nbr = s->dNbr;
+    A.lowcnt = s->dLow;
+    A.upoff = s->dUp;
+    A.eid = s->dEid;
+    A.eu_a = s->dEuA;
+    A.eu_qa = s->dEuQa;
+    A.eu_qb = s->dEuQb;
+    A.keys = s->dKeys;
+    A.binom.t = s->dBinom;
+    A.binom.stride = s->binom_stride;
+    A.th = s->th;
+    A.cnt = s->dCnt;
+    return A;
+}
+
+void stop(pcs_session* s, int reason) {
+    s->stopped = true;
+    s->stop_reason = reason;
+}
+
+}  // namespace
+
+// ================================================================ C ABI
+extern "C" {
+
+const char* pcs_version(void) { return "pcstable_b200 0.1 (sm_100a, abi 1)"; }
+const char* pcs_last_error(void) { return g_err.c_str(); }
+
+void pcs_config_default(pcs_config* cfg) {  // core.hpp:357-368
+    std::memset(cfg, 0, sizeof *cfg);
+    cfg->alpha = 0.05;
+    cfg->max_level = -1;
+    cfg->variant = PCS_VARIANT_SET;
+    cfg->edges_per_unit = 2;
+    cfg->workers_per_edge = 32;
+    cfg->set_groups = 2;
+    cfg->unit_width = 64;
+    cfg->device = 0;
+    cfg->shard_index = 0;
+    cfg->shard_count = 1;
+}
+
+pcs_status pcs_threshold_tau(double alpha, int32_t m, int32_t ell, double* tau) {
+    return threshold_tau(alpha, m, ell, tau);
+}
+
+static pcs_status session_upload_corr(pcs_session* s, const double* c) {
+    s->ldc = (s->p + 3) / 4 * 4;
+    CUDA_TRY(cudaMalloc(&s->dC, sizeof(double) * (size_t)s->p * s->ldc));
+    CUDA_TRY(cudaEventRecord(s->ev_begin, s->st));
+    CUDA_TRY(cudaMemcpy2DAsync(s->dC, sizeof(double) * s->ldc, c, sizeof(double) * s->p, sizeof(double) * s->p, s->p,
+                               cudaMemcpyHostToDevice, s->st));
+    int* dErr = nullptr;
+    CUDA_TRY(cudaMalloc(&dErr, sizeof(int)));
+    CUDA_TRY(cudaMemsetAsync(dErr, 0, sizeof(int), s->st));
+    launch_normalize_corr(s->dC, s->ldc, s->p, dErr, s->st);
+    int err = 0;
+    CUDA_TRY(cudaMemcpyAsync(&err, dErr, sizeof(int), cudaMemcpyDeviceToHost, s->st));
+    CUDA_TRY(cudaStreamSynchronize(s->st));
+    cudaFree(dErr);
+    if (err & 2) return fail(PCS_EINVAL, "CorrelationMatrix: diagonal must be 1");
+    if (err & 4) return fail(PCS_EINVAL, "CorrelationMatrix: matrix must be symmetric");
+    if (err & 8) return fail(PCS_EINVAL, "CorrelationMatrix: entries must lie in [-1, 1]");
+    return PCS_OK;
+}
+
+pcs_status pcs_session_create(const double* c, int32_t p, int32_t m, const pcs_config* cfg, pcs_session** out) {
+    pcs_session* s = nullptr;
+    pcs_status st = session_new(p, m, cfg, &s);
+    if (st) return st;
+    st = session_upload_corr(s, c);
+    if (st) { free_session(s); return st; }
+    *out = s;
+    return PCS_OK;
+}
+
+pcs_status pcs_session_create_device(const double* d_c, int64_t ldc, int32_t p, int32_t m, const pcs_config* cfg,
+                                     pcs_session** out) {
+    pcs_session* s = nullptr;
+    pcs_status st = session_new(p, m, cfg, &s);
+    if (st) return st;
+    s->own_c = false;
+    s->dC = const_cast<double*>(d_c);
+    s->ldc = ldc;
+    cudaEventRecord(s->ev_begin, s->st);
+    *out = s;
+    return PCS_OK;
+}
+
+pcs_status pcs_session_level_begin(pcs_session* s, int32_t* running, int32_t* ell_out, int64_t* num_keys) {
+    if (!s) return fail(PCS_EINVAL, "null session");
+    CUDA_TRY(cudaSetDevice(s->device));
+    *running = 0;
+    *num_keys = 0;
+    if (s->stopped) { *ell_out = s->ell; return PCS_OK; }
+    if (s->in_level) return fail(PCS_EINVAL, "level already started");
+    const int ell = s->ell + 1;
+    *ell_out = ell;
+    if (s->cfg.max_level >= 0 && ell > s->cfg.max_level) { stop(s, PCS_STOP_LEVEL_CAP); return PCS_OK; }
+    double tau;
+    pcs_status st = threshold_tau(s->cfg.alpha, s->m, ell, &tau);
+    if (st == PCS_ELEVEL) { stop(s, PCS_STOP_SAMPLE_SIZE); return PCS_OK; }
+    if (st) return st;
+    s->ell = ell;
+    s->th = make_thresholds(tau);
+    s->t_level = now_s();
+    s->kernel_timing = false;
+    CUDA_TRY(cudaMemsetAsync(s->dCnt, 0, sizeof(Counters), s->st));
+    if (ell == 0) {
+        CUDA_TRY(cudaEventRecord(s->ev_k0, s->st));
+        launch_level0(s->dC, s->ldc, s->p, s->W, s->dAdj, s->th, s->dCnt, s->st);
+        CUDA_TRY(cudaEventRecord(s->ev_k1, s->st));
+        s->kernel_timing = true;
+        CUDA_TRY(cudaGetLastError());
+        s->in_level = true;
+        *running = 1;
+        return PCS_OK;
+    }
+    // snapshot of the live graph (compact(), core.hpp:227-239)
+    launch_snapshot_degrees(s->dAdj, s->p, s->W, s->dDeg, s->dLow, s->st);
+    launch_snapshot_scan(s->dDeg, s->dLow, s->p, s->dOff, s->dUp, s->dInfo, s->st);
+    CUDA_TRY(cudaMemcpyAsync(&s->info, s->dInfo, sizeof(SnapInfo), cudaMemcpyDeviceToHost, s->st));
+    CUDA_TRY(cudaStreamSynchronize(s->st));
+    const int maxw = s->info.max_width;
+    if (maxw - 1 < ell) {  // skeleton.hpp:370-373 (level not recorded)
+        s->ell = ell - 1;
+        stop(s, PCS_STOP_MAX_DEGREE);
+        return PCS_OK;
+    }
+    unsigned long long tmp;
+    if (!binomial_exact(maxw - 1, ell, &tmp)) return fail(PCS_EOVERFLOW, "binomial: C(n, k) exceeds 64 bits");
+    if (!binomial_exact(maxw, ell, &tmp) || tmp >= (1ull << 62))
+        return fail(PCS_EUNSUPPORTED, "level " + std::to_string(ell) + ": C(" + std::to_string(maxw) + ", " +
+                                          std::to_string(ell) + ") conditioning sets per row exceed 2^62");
+    if (ell > kMaxTemplLevel)
+        return fail(PCS_EUNSUPPORTED, "conditioning level " + std::to_string(ell) + " > " +
+                                          std::to_string(kMaxTemplLevel) + " not yet supported on the device");
+    if (s->info.e_dir > s->capDir) {
+        if ((st = realloc_dev(&s->dNbr, s->info.e_dir))) return st;
+        if ((st = realloc_dev(&s->dEid, s->info.e_dir))) return st;
+        s->capDir = s->info.e_dir;
+    }
+    if (s->info.e_und > s->capUnd) {
+        if ((st = realloc_dev(&s->dEuA, s->info.e_und))) return st;
+        if ((st = realloc_dev(&s->dEuQa, s->info.e_und))) return st;
+        if ((st = realloc_dev(&s->dEuQb, s->info.e_und))) return st;
+        if ((st = realloc_dev(&s->dKeys, s->info.e_und))) return st;
+        s->capUnd = s->info.e_und;
+    }
+    if (s->info.e_und * (2 + ell) > s->capRec) {
+        if ((st = realloc_dev(&s->dRec, s->info.e_und * (2 + ell)))) return st;
+        s->capRec = s->info.e_und * (2 + ell);
+    }
+    if ((st = build_binomials(s, ell, maxw))) return st;
+    launch_snapshot_fill(s->dAdj, s->p, s->W, s->dOff, s->dNbr, s->st);
+    LevelArgs A = level_args(s);
+    launch_edge_index(A, s->dEid, s->dEuA, s->dEuQa, s->dEuQb, s->st);
+    launch_fill_keys(s->dKeys, s->info.e_und, s->st);
+    CUDA_TRY(cudaGetLastError());
+    s->in_level = true;
+    *running = 1;
+    *num_keys = s->info.e_und;
+    return PCS_OK;
+}
+
+pcs_status pcs_session_level_pass(pcs_session* s, int32_t pass) {
+    if (!s || !s->in_level) return fail(PCS_EINVAL, "no level in progress");
+    if (pass != 0 && pass != 1) return fail(PCS_EINVAL, "pass must be 0 or 1");
+    if (s->ell == 0) return PCS_OK;
+    CUDA_TRY(cudaSetDevice(s->device));
+    LevelArgs A = level_args(s);
+    const int shard = s->cfg.shard_index, nsh = s->cfg.shard_count;
+    if (!s->kernel_timing) { CUDA_TRY(cudaEventRecord(s->ev_k0, s->st)); }
+    if (s->cfg.variant == PCS_VARIANT_SET || s->ell == 1) {
+        launch_row_work(A, pass, s->cfg.variant, 0, s->p, s->dPrefix, s->st);
+        unsigned long long total = 0;
+        CUDA_TRY(cudaMemcpyAsync(&total, s->dPrefix + s->p, sizeof(total), cudaMemcpyDeviceToHost, s->st));
+        CUDA_TRY(cudaStreamSynchronize(s->st));
+        const unsigned long long u0 = (unsigned long long)((__int128)total * shard / nsh);
+        const unsigned long long u1 = (unsigned long long)((__int128)total * (shard + 1) / nsh);
+        if (u1 > u0) {
+            if (s->ell == 1) {
+                launch_level1(A, pass, s->dPrefix, u0, u1, s->st);
+            } else {
+                if (launch_level_set(A, pass, s->dPrefix, u0, u1, s->num_sms, s->st))
+                    return fail(PCS_EUNSUPPORTED, "level not supported by the set kernel");
+            }
+        }
+    } else {
+        const long long E = s->info.e_und;
+        const long long e0 = (long long)((__int128)E * shard / nsh), e1 = (long long)((__int128)E * (shard + 1) / nsh);
+        if (e1 > e0 && launch_level_edge(A, pass, e0, e1, s->num_sms, s->st))
+            return fail(PCS_EUNSUPPORTED, "level not supported by the edge kernel");
+    }
+    CUDA_TRY(cudaGetLastError());
+    CUDA_TRY(cudaEventRecord(s->ev_k1, s->st));
+    s->kernel_timing = true;
+    return PCS_OK;
+}
+
+pcs_status pcs_session_keys(pcs_session* s, void** device_ptr, int64_t* count) {
+    if (!s) return fail(PCS_EINVAL, "null session");
+    *device_ptr = s->dKeys;
+    *count = (s->in_level && s->ell >= 1) ? s->info.e_und : 0;
+    CUDA_TRY(cudaStreamSynchronize(s->st));  // keys are complete when the caller reduces them
+    return PCS_OK;
+}
+
+pcs_status pcs_session_level_end(pcs_session* s) {
+    if (!s || !s->in_level) return fail(PCS_EINVAL, "no level in progress");
+    CUDA_TRY(cudaSetDevice(s->device));
+    LevelArgs A = level_args(s);
+    if (s->ell >= 1) launch_commit(A, s->dAdj, s->W, s->info.e_und, s->dRec, s->st);
+    Counters c{};
+    CUDA_TRY(cudaMemcpyAsync(&c, s->dCnt, sizeof(Counters), cudaMemcpyDeviceToHost, s->st));
+    CUDA_TRY(cudaStreamSynchronize(s->st));
+    CUDA_TRY(cudaGetLastError());
+    pcs_status st = check_level_errors(s, c);
+    if (st) return st;
+    pcs_level_stats L{};
+    L.level = s->ell;
+    if (s->ell == 0) {
+        const unsigned long long p = (unsigned long long)s->p;
+        L.ci_tests = p * (p - 1) / 2;  // skeleton.hpp:274-276
+        L.pseudo_inverses = 0;
+        L.device_ci_tests = L.ci_tests;
+    } else {
+        L.ci_tests = c.ci_serial;
+        L.pseudo_inverses = c.ci_serial;  // skeleton.hpp:151-152
+        L.device_ci_tests = c.gpu_tests;
+        L.device_pseudo_inverses = c.gpu_pinv;
+        if (c.rec_count) {
+            const size_t w = (size_t)(2 + s->ell);
+            std::vector<int32_t> r(c.rec_count * w);
+            CUDA_TRY(cudaMemcpy(r.data(), s->dRec, sizeof(int32_t) * r.size(), cudaMemcpyDeviceToHost));
+            for (unsigned long long k = 0; k < c.rec_count; ++k) {
+                s->recs.push_back(r[k * w]);
+                s->recs.push_back(r[k * w + 1]);
+                s->recs.push_back(s->ell);
+                for (int q = 0; q < s->ell; ++q) s->recs.push_back(r[k * w + 2 + q]);
+            }
+        }
+    }
+    L.edges_removed = c.removed;
+    if (s->kernel_timing) {
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, s->ev_k0, s->ev_k1);
+        L.kernel_ms = ms;
+    }
+    L.elapsed_s = now_s() - s->t_level;
+    s->levels.push_back(L);
+    s->in_level = false;
+    return PCS_OK;
+}
+
+pcs_status pcs_session_finish(pcs_session* s, pcs_result** out) {
+    if (!s) return fail(PCS_EINVAL, "null session");
+    CUDA_TRY(cudaSetDevice(s->device));
+    auto* r = new pcs_result();
+    r->p = s->p;
+    r->W = s->W;
+    r->stop_reason = s->stop_reason;
+    r->levels = s->levels;
+    r->recs = s->recs;
+    r->adj.resize((size_t)s->p * s->W);
+    CUDA_TRY(cudaMemcpyAsync(r->adj.data(), s->dAdj, sizeof(uint32_t) * r->adj.size(), cudaMemcpyDeviceToHost, s->st));
+    CUDA_TRY(cudaEventRecord(s->ev_end, s->st));
+    CUDA_TRY(cudaStreamSynchronize(s->st));
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, s->ev_begin, s->ev_end);
+    r->device_seconds = ms * 1e-3;
+    *out = r;
+    return PCS_OK;
+}
+
+void pcs_session_free(pcs_session* s) { free_session(s); }
+
+static pcs_status run_session(pcs_session* s, pcs_result** out) {
+    for (;;) {
+        int32_t running = 0, ell = 0;
+        int64_t nk = 0;
+        pcs_status st = pcs_session_level_begin(s, &running, &ell, &nk);
+        if (st) return st;
+        if (!running) break;
+        if ((st = pcs_session_level_pass(s, 0))) return st;
+        if ((st = pcs_session_level_pass(s, 1))) return st;
+        if ((st = pcs_session_level_end(s))) return st;
+    }
+    return pcs_session_finish(s, out);
+}
+
+pcs_status pcs_run_pc_stable(const double* c, int32_t p, int32_t m, const pcs_config* cfg, pcs_result** out) {
+    *out = nullptr;
+    pcs_session* s = nullptr;
+    pcs_status st = pcs_session_create(c, p, m, cfg, &s);
+    if (st) return st;
+    st = run_session(s, out);
+    free_session(s);
+    return st;
+}
+
+pcs_status pcs_run_pc_stable_device(const double* d_c, int64_t ldc, int32_t p, int32_t m, const pcs_config* cfg,
+                                    pcs_result** out) {
+    *out = nullptr;
+    pcs_session* s = nullptr;
+    pcs_status st = pcs_session_create_device(d_c, ldc, p, m, cfg, &s);
+    if (st) return st;
+    st = run_session(s, out);
+    free_session(s);
+    return st;
+}
+
+static pcs_status correlation_device(cudaStream_t stream, const double* x, int m, int p, double* dC, long long ldc,
+                                     int32_t* zero_var_col) {
+    if (m < 4) return fail(PCS_EINVAL, "DataMatrix: need at least 4 samples, got " + std::to_string(m));
+    if (p < 2) return fail(PCS_EINVAL, "DataMatrix: need at least 2 variables, got " + std::to_string(p));
+    const int ldk = (m + 31) / 32 * 32;
+    const long long ldg = (p + 3) / 4 * 4;
+    double *dX = nullptr, *dXc = nullptr, *dG = nullptr, *dMean = nullptr;
+    int* dErr = nullptr;
+    pcs_status st = PCS_OK;
+    auto cleanup = [&]() { cudaFree(dX); cudaFree(dXc); cudaFree(dG); cudaFree(dMean); cudaFree(dErr); };
+    if (cudaMalloc(&dX, sizeof(double) * (size_t)m * p) || cudaMalloc(&dXc, sizeof(double) * (size_t)p * ldk) ||
+        cudaMalloc(&dG, sizeof(double) * (size_t)p * ldg) || cudaMalloc(&dMean, sizeof(double) * (size_t)p) ||
+        cudaMalloc(&dErr, sizeof(int) * 2)) {
+        cleanup();
+        return fail(PCS_ENOMEM, "cudaMalloc failed in compute_correlation");
+    }
+    int init[2] = {0, INT32_MAX};
+    cudaMemcpyAsync(dX, x, sizeof(double) * (size_t)m * p, cudaMemcpyHostToDevice, stream);
+    cudaMemcpyAsync(dErr, init, sizeof(init), cudaMemcpyHostToDevice, stream);
+    launch_correlation(dX, m, p, dXc, dG, ldg, dMean, dC, ldc, dErr, stream);
+    int err[2];
+    cudaMemcpyAsync(err, dErr, sizeof(err), cudaMemcpyDeviceToHost, stream);
+    cudaError_t ce = cudaStreamSynchronize(stream);
+    cleanup();
+    if (ce != cudaSuccess) return fail(PCS_ECUDA, std::string("compute_correlation: ") + cudaGetErrorString(ce));
+    if (err[0] & 1) st = fail(PCS_EINVAL, "DataMatrix: values must be finite");
+    else if (err[1] != INT32_MAX) {
+        if (zero_var_col) *zero_var_col = err[1];
+        st = fail(PCS_EZEROVAR, "compute_correlation: column " + std::to_string(err[1]) + " has zero variance");
+    }
+    return st;
+}
+
+pcs_status pcs_correlation(const double* x, int32_t m, int32_t p, double* c_out, int32_t* zero_var_col) {
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) return fail(PCS_ECUDA, "no CUDA device available");
+    cudaStream_t stream;
+    CUDA_TRY(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
+    double* dC = nullptr;
+    if (cudaMalloc(&dC, sizeof(double) * (size_t)p * p) != cudaSuccess) {
+        cudaStreamDestroy(stream);
+        return fail(PCS_ENOMEM, "cudaMalloc failed");
+    }
+    pcs_status st = correlation_device(stream, x, m, p, dC, p, zero_var_col);
+    if (!st) {
+        cudaError_t ce = cudaMemcpy(c_out, dC, sizeof(double) * (size_t)p * p, cudaMemcpyDeviceToHost);
+        if (ce != cudaSuccess) st = fail(PCS_ECUDA, cudaGetErrorString(ce));
+    }
+    cudaFree(dC);
+    cudaStreamDestroy(stream);
+    return st;
+}
+
+pcs_status pcs_run_pc_stable_data(const double* x, int32_t m, int32_t p, const pcs_config* cfg, pcs_result** out,
+                                  int32_t* zero_var_col) {
+    *out = nullptr;
+    pcs_session* s = nullptr;
+    pcs_status st = session_new(p, m, cfg, &s);
+    if (st) return st;
+    s->ldc = (p + 3) / 4 * 4;
+    if (cudaMalloc(&s->dC, sizeof(double) * (size_t)p * s->ldc) != cudaSuccess) {
+        free_session(s);
+        return fail(PCS_ENOMEM, "cudaMalloc failed");
+    }
+    cudaEventRecord(s->ev_begin, s->st);
+    st = correlation_device(s->st, x, m, p, s->dC, s->ldc, zero_var_col);
+    if (!st) st = run_session(s, out);
+    free_session(s);
+    return st;
+}
+
+int32_t pcs_result_p(const pcs_result* r) { return r->p; }
+int32_t pcs_result_levels(const pcs_result* r, pcs_level_stats* out, int32_t cap) {
+    const int32_t n = (int32_t)r->levels.size();
+    for (int32_t k = 0; k < n && k < cap; ++k) out[k] = r->levels[k];
+    return n;
+}
+int32_t pcs_result_stop_reason(const pcs_result* r) { return r->stop_reason; }
+static inline bool res_at(const pcs_result* r, int i, int j) {
+    return (r->adj[(size_t)i * r->W + (j >> 5)] >> (j & 31)) & 1u;
+}
+void pcs_result_adjacency(const pcs_result* r, uint8_t* out) {
+    for (int i = 0; i < r->p; ++i)
+        for (int j = 0; j < r->p; ++j) out[(size_t)i * r->p + j] = res_at(r, i, j);
+}
+int64_t pcs_result_edge_count(const pcs_result* r) {
+    int64_t n = 0;
+    for (int i = 0; i < r->p; ++i)
+        for (int j = i + 1; j < r->p; ++j) n += res_at(r, i, j);
+    return n;
+}
+void pcs_result_edge_list(const pcs_result* r, int32_t* out) {
+    int64_t k = 0;
+    for (int i = 0; i < r->p; ++i)
+        for (int j = i + 1; j < r->p; ++j)
+            if (res_at(r, i, j)) { out[2 * k] = i; out[2 * k + 1] = j; ++k; }
+}
+int64_t pcs_result_member_total(const pcs_result* r) {
+    int64_t tot = 0;
+    for (size_t k = 0; k < r->recs.size();) {
+        const int ell = r->recs[k + 2];
+        tot += ell;
+        k += 3 + (size_t)ell;
+    }
+    return tot;
+}
+void pcs_result_sepsets(const pcs_result* r, int32_t* level, int64_t* offset, int32_t* members) {
+    const int p = r->p;
+    const size_t ns = (size_t)p * (p - 1) / 2;
+    // slot -> record index (levels >= 1); other removed pairs were removed at level 0 with the empty set
+    std::vector<int64_t> rec_at(ns, -1);
+    for (size_t k = 0; k < r->recs.size();) {
+        int a = r->recs[k], b = r->recs[k + 1];
+        if (a > b) std::swap(a, b);
+        const size_t slot = (size_t)a * (2 * (size_t)p - a - 1) / 2 + (size_t)(b - a - 1);
+        rec_at[slot] = (int64_t)k;
+        k += 3 + (size_t)r->recs[k + 2];
+    }
+    int64_t at = 0;
+    size_t slot = 0;
+    for (int i = 0; i < p; ++i)
+        for (int j = i + 1; j < p; ++j, ++slot) {
+            offset[slot] = at;
+            if (res_at(r, i, j)) { level[slot] = -1; continue; }
+            const int64_t k = rec_at[slot];
+            if (k < 0) { level[slot] = 0; continue; }
+            const int ell = r->recs[k + 2];
+            level[slot] = ell;
+            for (int q = 0; q < ell; ++q) members[at + q] = r->recs[k + 3 + q];
+            at += ell;
+        }
+}
+double pcs_result_device_seconds(const pcs_result* r) { return r->device_seconds; }
+void pcs_result_free(pcs_result* r) { delete r; }
+
+pcs_status pcs_ci_test_batch(const double* c, int32_t p, int32_t ell, int64_t n, const int32_t* ij,
+                             const int32_t* sets, double tau, uint8_t* independent, double* z, double* rho,
+                             uint8_t* degenerate) {
+    if (ell < 0 || ell > kMaxTemplLevel) return fail(PCS_EUNSUPPORTED, "ci_test_batch: ell out of range");
+    pcs_config cfg;
+    pcs_config_default(&cfg);
+    pcs_session* s = nullptr;
+    pcs_status st = pcs_session_create(c, p, 4, &cfg, &s);
+    if (st) return st;
+    int32_t *dIJ = nullptr, *dS = nullptr;
+    uint8_t *dInd = nullptr, *dDeg = nullptr;
+    double *dZ = nullptr, *dR = nullptr;
+    int* dErr = nullptr;
+    const size_t nn = (size_t)std::max<int64_t>(n, 1);
+    cudaMalloc(&dIJ, sizeof(int32_t) * 2 * nn);
+    cudaMalloc(&dS, sizeof(int32_t) * nn * std::max(ell, 1));
+    cudaMalloc(&dInd, nn);
+    cudaMalloc(&dDeg, nn);
+    cudaMalloc(&dZ, sizeof(double) * nn);
+    cudaMalloc(&dR, sizeof(double) * nn);
+    cudaMalloc(&dErr, sizeof(int));
+    cudaMemcpy(dIJ, ij, sizeof(int32_t) * 2 * n, cudaMemcpyHostToDevice);
+    if (ell > 0) cudaMemcpy(dS, sets, sizeof(int32_t) * n * ell, cudaMemcpyHostToDevice);
+    cudaMemset(dErr, 0, sizeof(int));
+    launch_ci_batch(s->dC, s->ldc, p, ell, n, dIJ, dS, tau, dInd, dZ, dR, dDeg, dErr, s->st);
+    cudaStreamSynchronize(s->st);
+    int err = 0;
+    cudaMemcpy(independent, dInd, n, cudaMemcpyDeviceToHost);
+    cudaMemcpy(degenerate, dDeg, n, cudaMemcpyDeviceToHost);
+    cudaMemcpy(z, dZ, sizeof(double) * n, cudaMemcpyDeviceToHost);
+    cudaMemcpy(rho, dR, sizeof(double) * n, cudaMemcpyDeviceToHost);
+    cudaMemcpy(&err, dErr, sizeof(int), cudaMemcpyDeviceToHost);
+    cudaError_t ce = cudaGetLastError();
+    cudaFree(dIJ); cudaFree(dS); cudaFree(dInd); cudaFree(dDeg); cudaFree(dZ); cudaFree(dR); cudaFree(dErr);
+    free_session(s);
+    if (ce != cudaSuccess) return fail(PCS_ECUDA, cudaGetErrorString(ce));
+    if (err) return fail(PCS_ENAN, "fisher_z: rho must lie in (-1, 1)");
+    return PCS_OK;
+}
+
+pcs_status pcs_pseudo_inverse_batch(const double* a, int32_t ell, int64_t n, double* out) {
+    if (ell < 1 || ell > kMaxTemplLevel) return fail(PCS_EUNSUPPORTED, "pseudo_inverse_batch: ell out of range");
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) return fail(PCS_ECUDA, "no CUDA device available");
+    for (int64_t q = 0; q < n * ell * ell; ++q)
+        if (!std::isfinite(a[q])) return fail(PCS_EINVAL, "pseudo_inverse: entries must be finite");
+    double *dA = nullptr, *dO = nullptr;
+    const size_t bytes = sizeof(double) * (size_t)std::max<int64_t>(n, 1) * ell * ell;
+    CUDA_TRY(cudaMalloc(&dA, bytes));
+    CUDA_TRY(cudaMalloc(&dO, bytes));
+    cudaMemcpy(dA, a, sizeof(double) * n * ell * ell, cudaMemcpyHostToDevice);
+    launch_pinv_batch(dA, ell, n, dO, 0);
+    cudaError_t ce = cudaMemcpy(out, dO, sizeof(double) * n * ell * ell, cudaMemcpyDeviceToHost);
+    cudaFree(dA);
+    cudaFree(dO);
+    if (ce != cudaSuccess) return fail(PCS_ECUDA, cudaGetErrorString(ce));
+    return PCS_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,754 @@
+// level.cu -- per-level kernels of the B200 PC-stable skeleton.
+//
+//   level0_kernel       Alg. 2 / run_level_zero (skeleton.hpp:262-288) -> live bitmask
+//   snapshot_*          compact() (core.hpp:227-239) as popc + scan + warp-ballot fill
+//   edge_index_kernel   undirected edge ids of the snapshot (key / sepset slots)
+//   level1_kernel       ell = 1, cuPC-S arrangement (skeleton.hpp:175-222) specialised:
+//                       M2^+ = [1] exactly, so only the closed form is evaluated
+//   level_set_kernel<L> ell >= 2, cuPC-S: 32 conditioning sets per warp, one
+//                       pseudo-inverse per lane, shared by every target of the row
+//   level_edge_kernel<L> ell >= 2, cuPC-E (skeleton.hpp:135-170): warp per edge,
+//                       lanes over ranks, per-test pseudo-inverse, ballot early exit
+//   commit_kernel       claim_removal (skeleton.hpp:123-129): apply removals, decode
+//                       sepsets, serial-equivalent counters
+//
+// Keys: key[e] = (dir << 62) | full-row rank of the first separating set found for
+// undirected edge e (dir 0 = row a, dir 1 = row b, a < b); atomicMin keeps the
+// serial strategy's choice regardless of schedule.
+//
+// Compiled with -fmad=false: decisions are bit-identical to oracle/pcs_oracle.c.
+#include "pcs_internal.h"
+
+namespace pcs {
+
+namespace {
+
+__device__ __forceinline__ unsigned long long warp_sum(unsigned long long v) {
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) v += __shfl_xor_sync(0xffffffffu, v, d);
+    return v;
+}
+
+__device__ __forceinline__ void add_counter(unsigned long long* dst, unsigned long long v) {
+    v = warp_sum(v);
+    if ((threadIdx.x & 31) == 0 && v) atomicAdd(dst, v);
+}
+
+// largest r in [0, n) with prefix[r] <= u (prefix non-decreasing, prefix[0] = 0)
+__device__ __forceinline__ int find_row(const unsigned long long* prefix, int n, unsigned long long u) {
+    int lo = 0, hi = n - 1;
+    while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (__ldg(prefix + mid) <= u) lo = mid; else hi = mid - 1;
+    }
+    return lo;
+}
+
+// ---- runtime-ell unrank/rank (commit path; ell up to kMaxKeyLevel)
+constexpr int kMaxKeyLevel = 64;
+__device__ void unrank_rt(const BinomTable& C, int w, int ell, unsigned long long t, int* pos) {
+    int start = 0;
+    for (int c = 0; c < ell; ++c) {
+        const int k = ell - c;
+        const unsigned long long total = C(w - start, k);
+        const unsigned long long need = total - t;
+        int lo = start, hi = w - k;
+        while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if (C(w - mid, k) >= need) lo = mid; else hi = mid - 1;
+        }
+        pos[c] = lo;
+        t -= total - C(w - lo, k);
+        start = lo + 1;
+    }
+}
+__device__ unsigned long long rank_rt(const BinomTable& C, int w, int ell, const int* pos) {
+    unsigned long long s = 0;
+    for (int a = 0; a < ell; ++a) s += C(w - 1 - pos[a], ell - a);
+    return C(w, ell) - 1ull - s;
+}
+
+}  // namespace
+
+// =========================================================== level 0
+__global__ void level0_kernel(const double* __restrict__ C, long long ldc, int p, int W, uint32_t* __restrict__ adj,
+                              Thresholds th, Counters* cnt) {
+    const int lane = threadIdx.x & 31;
+    const long long warp = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const long long nwarps = ((long long)gridDim.x * blockDim.x) >> 5;
+    unsigned long long removed = 0;
+    int nan = 0;
+    for (long long item = warp; item < (long long)p * W; item += nwarps) {
+        const int i = (int)(item / W), w = (int)(item % W);
+        const int j = w * 32 + lane;
+        bool live = false;
+        if (j < p && j != i) {
+            const int d = decide0(__ldg(C + (size_t)i * ldc + j), th);
+            nan |= d == kNanError;
+            live = d == kDependent;
+            if (j > i && d == kIndependent) ++removed;
+        }
+        const unsigned word = __ballot_sync(0xffffffffu, live);
+        if (lane == 0) adj[(size_t)i * W + w] = word;
+    }
+    add_counter(&cnt->removed, removed);
+    if (nan) atomicOr(&cnt->err_nan, 1);
+}
+
+void launch_level0(const double* C, long long ldc, int p, int W, uint32_t* adj, Thresholds th, Counters* cnt,
+                   cudaStream_t s) {
+    const long long items = (long long)p * W;
+    long long blocks = (items * 32 + 255) / 256;
+    if (blocks > 148 * 16) blocks = 148 * 16;
+    level0_kernel<<<(int)blocks, 256, 0, s>>>(C, ldc, p, W, adj, th, cnt);
+}
+
+// =========================================================== snapshot
+__global__ void snapshot_degree_kernel(const uint32_t* __restrict__ adj, int p, int W, int32_t* deg,
+                                       int32_t* lowcnt) {
+    const int lane = threadIdx.x & 31;
+    const int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    if (i >= p) return;
+    int d = 0, lc = 0;
+    const int wi = i >> 5;
+    for (int w = lane; w < W; w += 32) {
+        const uint32_t x = adj[(size_t)i * W + w];
+        d += __popc(x);
+        if (w < wi) lc += __popc(x);
+        else if (w == wi) lc += __popc(x & ((1u << (i & 31)) - 1u));
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        d += __shfl_xor_sync(0xffffffffu, d, o);
+        lc += __shfl_xor_sync(0xffffffffu, lc, o);
+    }
+    if (lane == 0) { deg[i] = d; lowcnt[i] = lc; }
+}
+
+void launch_snapshot_degrees(const uint32_t* adj, int p, int W, int32_t* deg, int32_t* lowcnt, cudaStream_t s) {
+    snapshot_degree_kernel<<<(p * 32 + 255) / 256, 256, 0, s>>>(adj, p, W, deg, lowcnt);
+}
+
+// single-block exclusive scans of deg and (deg - lowcnt); p <= 46340
+__global__ void snapshot_scan_kernel(const int32_t* __restrict__ deg, const int32_t* __restrict__ lowcnt, int p,
+                                     int32_t* off, int32_t* upoff, SnapInfo* info) {
+    __shared__ long long s1[1024], s2[1024];
+    __shared__ int smax[1024];
+    const int t = threadIdx.x, nt = blockDim.x;
+    const int per = (p + nt - 1) / nt;
+    const int beg = min(t * per, p), end = min(beg + per, p);
+    long long a = 0, b = 0;
+    int mx = 0;
+    for (int k = beg; k < end; ++k) {
+        a += deg[k];
+        b += deg[k] - lowcnt[k];
+        mx = max(mx, deg[k]);
+    }
+    s1[t] = a; s2[t] = b; smax[t] = mx;
+    __syncthreads();
+    for (int d = 1; d < nt; d <<= 1) {  // Hillis-Steele inclusive scan
+        long long x1 = 0, x2 = 0;
+        int xm = 0;
+        if (t >= d) { x1 = s1[t - d]; x2 = s2[t - d]; xm = smax[t - d]; }
+        __syncthreads();
+        if (t >= d) { s1[t] += x1; s2[t] += x2; smax[t] = max(smax[t], xm); }
+        __syncthreads();
+    }
+    long long r1 = s1[t] - a, r2 = s2[t] - b;
+    for (int k = beg; k < end; ++k) {
+        off[k] = (int32_t)r1;
+        upoff[k] = (int32_t)r2;
+        r1 += deg[k];
+        r2 += deg[k] - lowcnt[k];
+    }
+    if (t == nt - 1) {
+        off[p] = (int32_t)s1[t];
+        upoff[p] = (int32_t)s2[t];
+        info->e_dir = s1[t];
+        info->e_und = s2[t];
+        info->max_width = smax[t];
+    }
+}
+
+void launch_snapshot_scan(const int32_t* deg, const int32_t* lowcnt, int p, int32_t* off, int32_t* upoff,
+                          SnapInfo* info, cudaStream_t s) {
+    snapshot_scan_kernel<<<1, 1024, 0, s>>>(deg, lowcnt, p, off, upoff, info);
+}
+
+__global__ void snapshot_fill_kernel(const uint32_t* __restrict__ adj, int p, int W, const int32_t* __restrict__ off,
+                                     int32_t* __restrict__ nbr) {
+    const int lane = threadIdx.x & 31;
+    const int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    if (i >= p) return;
+    int base = off[i];
+    for (int w0 = 0; w0 < W; w0 += 32) {
+        const int w = w0 + lane;
+        uint32_t x = w < W ? adj[(size_t)i * W + w] : 0u;
+        const int c = __popc(x);
+        int incl = c;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, incl, d);
+            if (lane >= d) incl += y;
+        }
+        int at = base + incl - c;
+        while (x) {
+            const int bit = __ffs(x) - 1;
+            nbr[at++] = w * 32 + bit;
+            x &= x - 1;
+        }
+        base += __shfl_sync(0xffffffffu, incl, 31);
+    }
+}
+
+void launch_snapshot_fill(const uint32_t* adj, int p, int W, const int32_t* off, int32_t* nbr, cudaStream_t s) {
+    snapshot_fill_kernel<<<(p * 32 + 255) / 256, 256, 0, s>>>(adj, p, W, off, nbr);
+}
+
+__global__ void edge_index_kernel(LevelArgs A, int32_t* eid, int32_t* eu_a, int32_t* eu_qa, int32_t* eu_qb) {
+    const int lane = threadIdx.x & 31;
+    const int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    if (i >= A.p) return;
+    const int oi = A.off[i], w = A.off[i + 1] - oi, lci = A.lowcnt[i];
+    for (int q = lane; q < w; q += 32) {
+        const int j = A.nbr[oi + q];
+        if (j > i) {
+            const int e = A.upoff[i] + (q - lci);
+            eid[oi + q] = e;
+            eu_a[e] = i;
+            eu_qa[e] = q;
+        } else {  // entry (i -> j), j < i: position of i among row j's upper part
+            const int oj = A.off[j];
+            int lo = A.lowcnt[j], hi = A.off[j + 1] - oj - 1;
+            while (lo < hi) {
+                const int mid = (lo + hi) >> 1;
+                if (A.nbr[oj + mid] < i) lo = mid + 1; else hi = mid;
+            }
+            const int e = A.upoff[j] + (lo - A.lowcnt[j]);
+            eid[oi + q] = e;
+            eu_qb[e] = q;
+        }
+    }
+}
+
+void launch_edge_index(const LevelArgs& A, int32_t* eid, int32_t* eu_a, int32_t* eu_qa, int32_t* eu_qb,
+                       cudaStream_t s) {
+    edge_index_kernel<<<(A.p * 32 + 255) / 256, 256, 0, s>>>(A, eid, eu_a, eu_qa, eu_qb);
+}
+
+__global__ void fill_keys_kernel(unsigned long long* keys, long long n) {
+    for (long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += (long long)gridDim.x * blockDim.x)
+        keys[k] = (unsigned long long)kNoneKey;
+}
+void launch_fill_keys(unsigned long long* keys, long long n, cudaStream_t s) {
+    if (n <= 0) return;
+    long long blocks = (n + 255) / 256;
+    if (blocks > 148 * 8) blocks = 148 * 8;
+    fill_keys_kernel<<<(int)blocks, 256, 0, s>>>(keys, n);
+}
+
+// =========================================================== work prefix
+constexpr int kL1Threads = 128;   // targets per ell=1 tile
+constexpr int kSetBand = 32;      // conditioning sets per ell>=2 unit
+
+__global__ void row_work_kernel(LevelArgs A, int pass, int variant, int row_begin, int row_end,
+                                unsigned long long* units) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= A.p) return;
+    unsigned long long u = 0;
+    const int w = A.off[i + 1] - A.off[i];
+    const int lc = A.lowcnt[i];
+    const int ntar = pass == 0 ? w - lc : lc;
+    if (i >= row_begin && i < row_end && w >= A.ell + 1 && ntar > 0) {
+        if (A.ell == 1) u = (unsigned long long)((ntar + kL1Threads - 1) / kL1Threads);
+        else u = (A.binom(w, A.ell) + kSetBand - 1) / kSetBand;
+    }
+    units[i] = u;
+}
+
+// exclusive scan in place over n+1 entries (entry n receives the total); one block
+__global__ void scan_u64_kernel(unsigned long long* a, int n) {
+    __shared__ unsigned long long s[1024];
+    const int t = threadIdx.x, nt = blockDim.x;
+    const int per = (n + nt - 1) / nt;
+    const int beg = min(t * per, n), end = min(beg + per, n);
+    unsigned long long x = 0;
+    for (int k = beg; k < end; ++k) x += a[k];
+    s[t] = x;
+    __syncthreads();
+    for (int d = 1; d < nt; d <<= 1) {
+        unsigned long long y = t >= d ? s[t - d] : 0ull;
+        __syncthreads();
+        s[t] += y;
+        __syncthreads();
+    }
+    unsigned long long r = s[t] - x;
+    for (int k = beg; k < end; ++k) {
+        const unsigned long long v = a[k];
+        a[k] = r;
+        r += v;
+    }
+    if (t == nt - 1) a[n] = s[t];
+}
+
+void launch_row_work(const LevelArgs& A, int pass, int variant, int row_begin, int row_end,
+                     unsigned long long* prefix, cudaStream_t s) {
+    row_work_kernel<<<(A.p + 255) / 256, 256, 0, s>>>(A, pass, variant, row_begin, row_end, prefix);
+    scan_u64_kernel<<<1, 1024, 0, s>>>(prefix, A.p);
+}
+
+// =========================================================== ell = 1
+// One block = one row i and a tile of up to 128 targets q (threads).  The row's
+// candidate sets {row[s]} are staged in shared memory in chunks; every thread
+// walks s in ascending order and stops at its first separating s, which is the
+// serial strategy's first passing rank for that edge direction.
+constexpr int kL1Chunk = 1024;
+constexpr int kL1Unroll = 8;
+
+__global__ void __launch_bounds__(kL1Threads) level1_kernel(LevelArgs A, int pass, const unsigned long long* prefix,
+                                                            unsigned long long tile_base) {
+    __shared__ int s_k[kL1Chunk];
+    __shared__ double s_cik[kL1Chunk];
+    __shared__ double s_h00[kL1Chunk];
+    const unsigned long long tile = tile_base + blockIdx.x;
+    const int i = find_row(prefix, A.p, tile);
+    const int t_in_row = (int)(tile - prefix[i]);
+    const int oi = A.off[i], w = A.off[i + 1] - oi, lc = A.lowcnt[i];
+    const int qbeg = pass == 0 ? lc : 0, qend = pass == 0 ? w : lc;
+    const int q = qbeg + t_in_row * kL1Threads + threadIdx.x;
+    const double* __restrict__ C = A.C;
+    const long long ldc = A.ldc;
+    bool active = q < qend;
+    int j = 0, e = 0;
+    double cij = 0.0;
+    if (active) {
+        j = A.nbr[oi + q];
+        e = A.eid[oi + q];
+        cij = __ldg(C + (size_t)i * ldc + j);
+        if (pass == 1 && A.keys[e] != (unsigned long long)kNoneKey) active = false;
+    }
+    const unsigned long long dirbits = (unsigned long long)pass << kDirShift;
+    unsigned long long tests = 0;
+    int nan = 0;
+    const double* __restrict__ Cj = C + j;
+    for (int s0 = 0; s0 < w; s0 += kL1Chunk) {
+        if (!__syncthreads_or(active)) break;
+        const int n = min(kL1Chunk, w - s0);
+        for (int t = threadIdx.x; t < n; t += kL1Threads) {
+            const int k = A.nbr[oi + s0 + t];
+            const double cik = __ldg(C + (size_t)i * ldc + k);
+            s_k[t] = k;
+            s_cik[t] = cik;
+            s_h00[t] = 1.0 - cik * cik;
+        }
+        __syncthreads();
+        if (active) {
+            for (int t = 0; t < n && active; t += kL1Unroll) {
+                double cjk[kL1Unroll];
+#pragma unroll
+                for (int u = 0; u < kL1Unroll; ++u)
+                    cjk[u] = (t + u < n) ? __ldg(Cj + (size_t)s_k[t + u] * ldc) : 0.0;
+#pragma unroll
+                for (int u = 0; u < kL1Unroll; ++u) {
+                    const int s = s0 + t + u;
+                    if (!active || t + u >= n || s == q) continue;
+                    const double h11 = 1.0 - cjk[u] * cjk[u];
+                    const double h01 = cij - s_cik[t + u] * cjk[u];
+                    const double denom = s_h00[t + u] * h11;
+                    const int d = decide_fast(h01, denom, A.th);
+                    ++tests;
+                    if (d != kDependent) {
+                        active = false;
+                        if (d == kNanError) nan = 1;
+                        else atomicMin(A.keys + e, dirbits | (unsigned long long)s);
+                    }
+                }
+            }
+        }
+        __syncthreads();
+    }
+    add_counter(&A.cnt->gpu_tests, tests);
+    if (nan) atomicOr(&A.cnt->err_nan, 1);
+}
+
+void launch_level1(const LevelArgs& A, int pass, const unsigned long long* prefix, unsigned long long u_begin,
+                   unsigned long long u_end, cudaStream_t s) {
+    // one block per target tile in [u_begin, u_end); sliced to respect the grid limit
+    const unsigned long long kMaxGrid = 1ull << 30;
+    for (unsigned long long base = u_begin; base < u_end; base += kMaxGrid) {
+        const unsigned long long n = u_end - base < kMaxGrid ? u_end - base : kMaxGrid;
+        level1_kernel<<<(unsigned)n, kL1Threads, 0, s>>>(A, pass, prefix, base);
+    }
+}
+
+// =========================================================== ell >= 2, cuPC-S
+template <int L>
+struct SetSlot {
+    double minv[L * L];
+    double ciS[L];
+    double p0[L];
+    double h00;
+    int pos[L];
+    int mem[L];
+};
+
+constexpr int kSetWarps = 4;
+
+template <int L>
+__global__ void __launch_bounds__(kSetWarps * 32) level_set_kernel(LevelArgs A, int pass,
+                                                                  const unsigned long long* prefix,
+                                                                  unsigned long long u_begin,
+                                                                  unsigned long long u_end) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    SetSlot<L>* slots = reinterpret_cast<SetSlot<L>*>(smem_raw) + wib * 32;
+    const double* __restrict__ C = A.C;
+    const long long ldc = A.ldc;
+    const unsigned long long dirbits = (unsigned long long)pass << kDirShift;
+    unsigned long long tests = 0, pinvs = 0;
+    int nan = 0;
+    unsigned long long* cursor = &A.cnt->units[pass];
+    for (;;) {
+        unsigned long long u = 0;
+        if (lane == 0) u = u_begin + atomicAdd(cursor, 1ull);
+        u = __shfl_sync(0xffffffffu, u, 0);
+        if (u >= u_end) break;
+        const int i = find_row(prefix, A.p, u);
+        const unsigned long long t0 = (u - prefix[i]) * kSetBand;
+        const int oi = A.off[i], w = A.off[i + 1] - oi, lc = A.lowcnt[i];
+        const int qbeg = pass == 0 ? lc : 0, qend = pass == 0 ? w : lc;
+        const unsigned long long K0 = dirbits | t0;
+        // any target of this row still open at rank t0?
+        bool open = false;
+        for (int q = qbeg + lane; q < qend; q += 32) open |= A.keys[A.eid[oi + q]] > K0;
+        if (!__any_sync(0xffffffffu, open)) continue;
+        // lane-parallel pseudo-inverses of the band's 32 sets
+        const unsigned long long total = A.binom(w, L);
+        const unsigned long long t = t0 + lane;
+        const bool valid = t < total;
+        if (valid) {
+            int pos[L];
+            unrank<L>(A.binom, w, t, pos);
+            double m2[L * L], minv[L * L], ciS[L], p0[L], h00;
+#pragma unroll
+            for (int a = 0; a < L; ++a) {
+                slots[lane].pos[a] = pos[a];
+                const int ma = A.nbr[oi + pos[a]];
+                slots[lane].mem[a] = ma;
+                ciS[a] = __ldg(C + (size_t)i * ldc + ma);
+            }
+#pragma unroll
+            for (int a = 0; a < L; ++a)
+#pragma unroll
+                for (int b = 0; b < L; ++b)
+                    m2[a * L + b] = __ldg(C + (size_t)slots[lane].mem[a] * ldc + slots[lane].mem[b]);
+            pinv<L>(m2, minv);
+            p0_terms<L>(minv, ciS, p0, h00);
+#pragma unroll
+            for (int q = 0; q < L * L; ++q) slots[lane].minv[q] = minv[q];
+#pragma unroll
+            for (int a = 0; a < L; ++a) { slots[lane].ciS[a] = ciS[a]; slots[lane].p0[a] = p0[a]; }
+            slots[lane].h00 = h00;
+        }
+        const int nvalid = __popc(__ballot_sync(0xffffffffu, valid));
+        if (lane == 0) pinvs += nvalid;
+        __syncwarp();
+        // every open target of the row against the band's sets, in rank order
+        for (int qc = qbeg; qc < qend; qc += 32) {
+            const int q = qc + lane;
+            bool live = q < qend;
+            int j = 0, e = 0;
+            unsigned long long key = 0;
+            double cij = 0.0;
+            if (live) {
+                j = A.nbr[oi + q];
+                e = A.eid[oi + q];
+                key = A.keys[e];
+                live = key > K0;
+                if (live) cij = __ldg(C + (size_t)i * ldc + j);
+            }
+            if (!__any_sync(0xffffffffu, live)) continue;
+            for (int sg = 0; sg < nvalid; ++sg) {
+                if (!live) break;
+                const SetSlot<L>& S = slots[sg];
+                const unsigned long long Kc = dirbits | (t0 + sg);
+                if (key <= Kc) { live = false; break; }
+                bool member = false;
+#pragma unroll
+                for (int a = 0; a < L; ++a) member |= S.pos[a] == q;
+                if (member) continue;
+                double cjS[L];
+#pragma unroll
+                for (int a = 0; a < L; ++a) cjS[a] = __ldg(C + (size_t)S.mem[a] * ldc + j);
+                double h01, denom;
+                h_terms<L>(S.minv, S.ciS, S.p0, S.h00, cjS, cij, h01, denom);
+                const int d = decide_fast(h01, denom, A.th);
+                ++tests;
+                if (d != kDependent) {
+                    live = false;
+                    if (d == kNanError) nan = 1;
+                    else atomicMin(A.keys + e, Kc);
+                }
+            }
+        }
+        __syncwarp();
+    }
+    add_counter(&A.cnt->gpu_tests, tests);
+    if (lane == 0 && pinvs) atomicAdd(&A.cnt->gpu_pinv, pinvs);
+    if (nan) atomicOr(&A.cnt->err_nan, 1);
+}
+
+template <int L>
+static int launch_set_L(const LevelArgs& A, int pass, const unsigned long long* prefix, unsigned long long u_begin,
+                        unsigned long long u_end, int num_sms, cudaStream_t s) {
+    const size_t smem = sizeof(SetSlot<L>) * 32 * kSetWarps;
+    static bool attr_set = false;
+    if (!attr_set) {
+        cudaFuncSetAttribute(level_set_kernel<L>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        attr_set = true;
+    }
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, level_set_kernel<L>, kSetWarps * 32, smem);
+    if (per_sm < 1) per_sm = 1;
+    level_set_kernel<L><<<num_sms * per_sm, kSetWarps * 32, smem, s>>>(A, pass, prefix, u_begin, u_end);
+    return 0;
+}
+
+int launch_level_set(const LevelArgs& A, int pass, const unsigned long long* prefix, unsigned long long u_begin,
+                     unsigned long long u_end, int num_sms, cudaStream_t s) {
+    switch (A.ell) {
+        case 2: return launch_set_L<2>(A, pass, prefix, u_begin, u_end, num_sms, s);
+        case 3: return launch_set_L<3>(A, pass, prefix, u_begin, u_end, num_sms, s);
+        case 4: return launch_set_L<4>(A, pass, prefix, u_begin, u_end, num_sms, s);
+        case 5: return launch_set_L<5>(A, pass, prefix, u_begin, u_end, num_sms, s);
+        case 6: return launch_set_L<6>(A, pass, prefix, u_begin, u_end, num_sms, s);
+        case 7: return launch_set_L<7>(A, pass, prefix, u_begin, u_end, num_sms, s);
+        case 8: return launch_set_L<8>(A, pass, prefix, u_begin, u_end, num_sms, s);
+        default: return -1;
+    }
+}
+
+// =========================================================== ell >= 2, cuPC-E
+template <int L>
+__global__ void __launch_bounds__(128) level_edge_kernel(LevelArgs A, int pass, long long e_begin, long long e_end) {
+    const int lane = threadIdx.x & 31;
+    const double* __restrict__ C = A.C;
+    const long long ldc = A.ldc;
+    const unsigned long long dirbits = (unsigned long long)pass << kDirShift;
+    unsigned long long tests = 0, pinvs = 0;
+    int nan = 0;
+    unsigned long long* cursor = &A.cnt->units[pass];
+    for (;;) {
+        unsigned long long ue = 0;
+        if (lane == 0) ue = atomicAdd(cursor, 1ull);
+        ue = __shfl_sync(0xffffffffu, ue, 0);
+        const long long e = e_begin + (long long)ue;
+        if (e >= e_end) break;
+        if (pass == 1 && A.keys[e] != (unsigned long long)kNoneKey) continue;
+        const int a = A.eu_a[e], qa = A.eu_qa[e];
+        const int b = A.nbr[A.off[a] + qa];
+        const int i = pass == 0 ? a : b;
+        const int q = pass == 0 ? qa : A.eu_qb[e];
+        const int j = pass == 0 ? b : a;
+        const int oi = A.off[i], w = A.off[i + 1] - oi;
+        if (w < L + 1) continue;
+        const unsigned long long total = A.binom(w - 1, L);
+        const double cij = __ldg(C + (size_t)i * ldc + j);
+        for (unsigned long long base = 0; base < total; base += 32) {
+            const unsigned long long t = base + lane;
+            const bool valid = t < total;
+            int d = kDependent;
+            int pos[L];
+            if (valid) {
+                unrank<L>(A.binom, w - 1, t, pos);
+                int mem[L];
+                double ciS[L], cjS[L], m2[L * L], minv[L * L], p0[L], h00, h01, denom;
+#pragma unroll
+                for (int k = 0; k < L; ++k) {
+                    pos[k] += pos[k] >= q;  // skip the target position (skeleton.hpp:146-149)
+                    mem[k] = A.nbr[oi + pos[k]];
+                    ciS[k] = __ldg(C + (size_t)i * ldc + mem[k]);
+                    cjS[k] = __ldg(C + (size_t)j * ldc + mem[k]);
+                }
+#pragma unroll
+                for (int x = 0; x < L; ++x)
+#pragma unroll
+                    for (int y = 0; y < L; ++y) m2[x * L + y] = __ldg(C + (size_t)mem[x] * ldc + mem[y]);
+                pinv<L>(m2, minv);
+                p0_terms<L>(minv, ciS, p0, h00);
+                h_terms<L>(minv, ciS, p0, h00, cjS, cij, h01, denom);
+                d = decide_fast(h01, denom, A.th);
+                ++tests;
+                ++pinvs;
+            }
+            const unsigned hit = __ballot_sync(0xffffffffu, d != kDependent);
+            if (hit) {
+                const int first = __ffs(hit) - 1;
+                if (lane == first) {
+                    if (d == kNanError) nan = 1;
+                    else atomicMin(A.keys + e, dirbits | rank_of<L>(A.binom, w, pos));
+                }
+                break;
+            }
+        }
+    }
+    add_counter(&A.cnt->gpu_tests, tests);
+    add_counter(&A.cnt->gpu_pinv, pinvs);
+    if (nan) atomicOr(&A.cnt->err_nan, 1);
+}
+
+template <int L>
+static int launch_edge_L(const LevelArgs& A, int pass, long long e_begin, long long e_end, int num_sms,
+                         cudaStream_t s) {
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, level_edge_kernel<L>, 128, 0);
+    if (per_sm < 1) per_sm = 1;
+    level_edge_kernel<L><<<num_sms * per_sm, 128, 0, s>>>(A, pass, e_begin, e_end);
+    return 0;
+}
+
+int launch_level_edge(const LevelArgs& A, int pass, long long e_begin, long long e_end, int num_sms,
+                      cudaStream_t s) {
+    switch (A.ell) {
+        case 2: return launch_edge_L<2>(A, pass, e_begin, e_end, num_sms, s);
+        case 3: return launch_edge_L<3>(A, pass, e_begin, e_end, num_sms, s);
+        case 4: return launch_edge_L<4>(A, pass, e_begin, e_end, num_sms, s);
+        case 5: return launch_edge_L<5>(A, pass, e_begin, e_end, num_sms, s);
+        case 6: return launch_edge_L<6>(A, pass, e_begin, e_end, num_sms, s);
+        case 7: return launch_edge_L<7>(A, pass, e_begin, e_end, num_sms, s);
+        case 8: return launch_edge_L<8>(A, pass, e_begin, e_end, num_sms, s);
+        default: return -1;
+    }
+}
+
+// =========================================================== commit
+// One thread per undirected snapshot edge: decode the key (full-row rank in
+// the deciding row), clear the edge in the live bitmask, append the sepset
+// record (a, b, members...) and accumulate the serial strategy's ci_tests
+// (test_edge_over_sets counts, skeleton.hpp:140-158).
+__global__ void commit_kernel(LevelArgs A, uint32_t* adj, int W, long long e_und, int32_t* rec) {
+    const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    unsigned long long tests = 0, removed = 0;
+    const int ell = A.ell;
+    if (e < e_und) {
+        const int a = A.eu_a[e], qa = A.eu_qa[e], qb = A.eu_qb[e];
+        const int b = A.nbr[A.off[a] + qa];
+        const int wa = A.off[a + 1] - A.off[a], wb = A.off[b + 1] - A.off[b];
+        const unsigned long long T0 = wa >= ell + 1 ? A.binom(wa - 1, ell) : 0ull;
+        const unsigned long long T1 = wb >= ell + 1 ? A.binom(wb - 1, ell) : 0ull;
+        const unsigned long long key = A.keys[e];
+        if (key == (unsigned long long)kNoneKey) {
+            tests = T0 + T1;
+        } else {
+            const int dir = (int)(key >> kDirShift);
+            const unsigned long long t = key & kRankMask;
+            const int r = dir ? b : a, q = dir ? qb : qa, w = dir ? wb : wa;
+            int pos[kMaxKeyLevel];
+            unrank_rt(A.binom, w, ell, t, pos);
+            int red[kMaxKeyLevel];
+            for (int k = 0; k < ell; ++k) red[k] = pos[k] - (pos[k] > q);
+            const unsigned long long rr = rank_rt(A.binom, w - 1, ell, red);
+            tests = dir ? T0 + rr + 1ull : rr + 1ull;
+            removed = 1;
+            atomicAnd(adj + (size_t)a * W + (b >> 5), ~(1u << (b & 31)));
+            atomicAnd(adj + (size_t)b * W + (a >> 5), ~(1u << (a & 31)));
+            const unsigned long long slot = atomicAdd(&A.cnt->rec_count, 1ull);
+            int32_t* out = rec + slot * (size_t)(2 + ell);
+            out[0] = a;
+            out[1] = b;
+            const int orow = A.off[r];
+            for (int k = 0; k < ell; ++k) out[2 + k] = A.nbr[orow + pos[k]];
+        }
+    }
+    add_counter(&A.cnt->ci_serial, tests);
+    add_counter(&A.cnt->removed, removed);
+}
+
+void launch_commit(const LevelArgs& A, uint32_t* adj, int W, long long e_und, int32_t* rec, cudaStream_t s) {
+    if (e_und <= 0) return;
+    commit_kernel<<<(unsigned)((e_und + 255) / 256), 256, 0, s>>>(A, adj, W, e_und, rec);
+}
+
+// =========================================================== parity helpers
+template <int L>
+__global__ void ci_batch_kernel(const double* C, long long ldc, long long n, const int32_t* ij, const int32_t* sets,
+                                double tau, uint8_t* indep, double* zout, double* rhoout, uint8_t* degen, int* err) {
+    const long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= n) return;
+    const int i = ij[2 * k], j = ij[2 * k + 1];
+    double z, rho, h01 = 0.0, denom = 1.0;
+    int d;
+    if (L == 0) {
+        const double c = C[(size_t)i * ldc + j];
+        const double v = c < -kRhoClamp ? -kRhoClamp : (c > kRhoClamp ? kRhoClamp : c);
+        rho = v;
+        z = fabs(0.5 * log((1.0 + v) / (1.0 - v)));
+        d = z <= tau ? kIndependent : kDependent;
+        if (!(v > -1.0 && v < 1.0)) d = kNanError;
+    } else {
+        constexpr int LL = L > 0 ? L : 1;
+        int mem[LL];
+        double ciS[LL], cjS[LL], m2[LL * LL], minv[LL * LL], p0[LL], h00;
+#pragma unroll
+        for (int a = 0; a < LL; ++a) {
+            mem[a] = sets[k * LL + a];
+            ciS[a] = C[(size_t)i * ldc + mem[a]];
+            cjS[a] = C[(size_t)j * ldc + mem[a]];
+        }
+#pragma unroll
+        for (int a = 0; a < LL; ++a)
+#pragma unroll
+            for (int b = 0; b < LL; ++b) m2[a * LL + b] = C[(size_t)mem[a] * ldc + mem[b]];
+        pinv<LL>(m2, minv);
+        p0_terms<LL>(minv, ciS, p0, h00);
+        h_terms<LL>(minv, ciS, p0, h00, cjS, C[(size_t)i * ldc + j], h01, denom);
+        d = decide_exact(h01, denom, tau, &z, &rho);
+    }
+    if (d == kNanError) atomicOr(err, 1);
+    indep[k] = d == kIndependent;
+    zout[k] = z;
+    rhoout[k] = rho;
+    degen[k] = (L > 0) && !(denom > 0.0);
+}
+
+int launch_ci_batch(const double* C, long long ldc, int p, int ell, long long n, const int32_t* ij,
+                    const int32_t* sets, double tau, uint8_t* indep, double* z, double* rho, uint8_t* degen,
+                    int* err, cudaStream_t s) {
+    if (n <= 0) return 0;
+    const unsigned blocks = (unsigned)((n + 127) / 128);
+#define PCS_CI_CASE(LV) \
+    case LV: ci_batch_kernel<LV><<<blocks, 128, 0, s>>>(C, ldc, n, ij, sets, tau, indep, z, rho, degen, err); return 0;
+    switch (ell) {
+        PCS_CI_CASE(0) PCS_CI_CASE(1) PCS_CI_CASE(2) PCS_CI_CASE(3) PCS_CI_CASE(4)
+        PCS_CI_CASE(5) PCS_CI_CASE(6) PCS_CI_CASE(7) PCS_CI_CASE(8)
+        default: return -1;
+    }
+#undef PCS_CI_CASE
+}
+
+template <int L>
+__global__ void pinv_batch_kernel(const double* a, long long n, double* out) {
+    const long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= n) return;
+    double m[L * L], r[L * L];
+#pragma unroll
+    for (int q = 0; q < L * L; ++q) m[q] = a[k * L * L + q];
+    pinv<L>(m, r);
+#pragma unroll
+    for (int q = 0; q < L * L; ++q) out[k * L * L + q] = r[q];
+}
+
+int launch_pinv_batch(const double* a, int ell, long long n, double* out, cudaStream_t s) {
+    if (n <= 0) return 0;
+    const unsigned blocks = (unsigned)((n + 127) / 128);
+#define PCS_PINV_CASE(LV) \
+    case LV: pinv_batch_kernel<LV><<<blocks, 128, 0, s>>>(a, n, out); return 0;
+    switch (ell) {
+        PCS_PINV_CASE(1) PCS_PINV_CASE(2) PCS_PINV_CASE(3) PCS_PINV_CASE(4)
+        PCS_PINV_CASE(5) PCS_PINV_CASE(6) PCS_PINV_CASE(7) PCS_PINV_CASE(8)
+        default: return -1;
+    }
+#undef PCS_PINV_CASE
+}
+
+}  // namespace pcs

@@ -1,0 +1,320 @@
+// pcs_device.cuh -- device-side building blocks of the B200 PC-stable path.
+//
+// Every floating-point expression here follows the operation order of the
+// reference (/root/reference/proj/include/pcstable/stats.hpp) and of the CPU
+// oracle (oracle/pcs_oracle.c); the translation units that include this file
+// are compiled with -fmad=false so no a*b+c is contracted into one rounding.
+// Together with correctly rounded IEEE sqrt/div this makes every CI decision
+// bit-identical to the oracle (only log() may differ by an ulp, and log is
+// evaluated only inside the +-1e-9 band around the threshold; see
+// decide_fast()).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace pcs {
+
+constexpr int64_t kNoneKey = INT64_MAX;              // "no separating set found"
+constexpr int kDirShift = 62;                         // key = dir << 62 | full-row rank
+constexpr uint64_t kRankMask = (1ull << 62) - 1;
+constexpr double kRhoClamp = 1.0 - 1e-12;             // stats.hpp:284
+
+// Per-level decision constants (host computes them in long double).
+struct Thresholds {
+    double tau;      // threshold_tau(alpha, m, ell)          (stats.hpp:120-129)
+    double lo;       // |rho| <= lo  => z <= tau for certain (level 0)
+    double hi;       // |rho| >= hi  => z >  tau for certain (level 0)
+    double lo2;      // rho^2 <= lo2 => independent for certain
+    double hi2;      // rho^2 >= hi2 => dependent for certain
+};
+
+// ---------------------------------------------------------------- binomials
+// Table T[k * stride + n] = C(n, k) for 0 <= k <= ell, 0 <= n < stride,
+// saturated at UINT64_MAX (host-built per level, comb.hpp:35-46).
+struct BinomTable {
+    const unsigned long long* t;
+    int stride;
+    __device__ __forceinline__ unsigned long long operator()(int n, int k) const {
+        if (k < 0 || n < k) return 0ull;
+        return __ldg(t + (size_t)k * stride + n);
+    }
+};
+
+// Lexicographic unrank of rank t among the ell-subsets of {0..w-1}
+// (same map as comb.hpp:50-67, computed by binary search over the table).
+template <int L>
+__device__ __forceinline__ void unrank(const BinomTable& C, int w, unsigned long long t, int (&pos)[L]) {
+    int start = 0;
+#pragma unroll
+    for (int c = 0; c < L; ++c) {
+        const int k = L - c;
+        const unsigned long long total = C(w - start, k);
+        const unsigned long long need = total - t;  // largest v with C(w-v,k) >= need
+        int lo = start, hi = w - k;
+        while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if (C(w - mid, k) >= need) lo = mid; else hi = mid - 1;
+        }
+        pos[c] = lo;
+        t -= total - C(w - lo, k);
+        start = lo + 1;
+    }
+}
+
+// Inverse map: lexicographic rank of ascending positions in width w.
+template <int L>
+__device__ __forceinline__ unsigned long long rank_of(const BinomTable& C, int w, const int (&pos)[L]) {
+    unsigned long long s = 0;
+#pragma unroll
+    for (int a = 0; a < L; ++a) s += C(w - 1 - pos[a], L - a);
+    return C(w, L) - 1ull - s;
+}
+
+// ------------------------------------------------------- pseudo-inverse
+// pseudo_inverse_into (stats.hpp:172-208) for an L x L row-major block.
+// Kept Cholesky columns stay at their static index k (flag kept[k]) instead of
+// being compacted, so every loop bound is a compile-time constant and the
+// arrays live in registers; the sums visit exactly the same terms in the same
+// order as the compacted form (a sum starts from its first term, never 0.0).
+template <int L>
+__device__ __forceinline__ void pinv(const double (&a)[L * L], double (&out)[L * L]) {
+    double G[L * L];
+#pragma unroll
+    for (int i = 0; i < L; ++i)
+#pragma unroll
+        for (int j = 0; j < L; ++j) {
+            double s = a[0 * L + i] * a[0 * L + j];
+#pragma unroll
+            for (int q = 1; q < L; ++q) s = s + a[q * L + i] * a[q * L + j];
+            G[i * L + j] = s;
+        }
+    double mx = G[0];
+#pragma unroll
+    for (int i = 1; i < L; ++i) mx = G[i * L + i] > mx ? G[i * L + i] : mx;
+    const double tol = 1e-10 * mx;
+#pragma unroll
+    for (int q = 0; q < L * L; ++q) out[q] = 0.0;
+    if (!(tol > 0.0)) return;
+
+    double Lm[L * L];  // Lm[i*L + k]: column stored at static index k
+    bool kept[L];
+#pragma unroll
+    for (int k = 0; k < L; ++k) {
+#pragma unroll
+        for (int i = 0; i < L; ++i) {
+            if (i < k) { Lm[i * L + k] = 0.0; continue; }
+            double v = G[i * L + k];
+            bool have = false;
+            double s = 0.0;
+#pragma unroll
+            for (int c = 0; c < k; ++c)
+                if (kept[c]) { const double pr = Lm[i * L + c] * Lm[k * L + c]; s = have ? s + pr : pr; have = true; }
+            if (have) v = v - s;
+            Lm[i * L + k] = v;
+        }
+        const double pivot = Lm[k * L + k];
+        kept[k] = pivot > tol;
+        if (kept[k]) {
+            const double root = sqrt(pivot);
+            Lm[k * L + k] = root;
+#pragma unroll
+            for (int i = k + 1; i < L; ++i) Lm[i * L + k] = Lm[i * L + k] / root;
+        }
+    }
+    bool any = false;
+#pragma unroll
+    for (int k = 0; k < L; ++k) any |= kept[k];
+    if (!any) return;
+
+    // K = L'L over kept columns (stats.hpp:204)
+    double K[L * L];
+#pragma unroll
+    for (int x = 0; x < L; ++x)
+#pragma unroll
+        for (int y = 0; y < L; ++y) {
+            double s = Lm[0 * L + x] * Lm[0 * L + y];
+#pragma unroll
+            for (int i = 1; i < L; ++i) s = s + Lm[i * L + x] * Lm[i * L + y];
+            K[x * L + y] = s;
+        }
+    // in-place lower LLT over the kept index set (stats.hpp:205, Eigen unblocked LLT)
+    bool failed = false;
+#pragma unroll
+    for (int k = 0; k < L; ++k) {
+        if (!kept[k] || failed) continue;
+        double x = K[k * L + k];
+        {
+            bool have = false;
+            double s = 0.0;
+#pragma unroll
+            for (int c = 0; c < k; ++c)
+                if (kept[c]) { const double pr = K[k * L + c] * K[k * L + c]; s = have ? s + pr : pr; have = true; }
+            if (have) x = x - s;
+        }
+        if (x <= 0.0) { failed = true; continue; }
+        x = sqrt(x);
+        K[k * L + k] = x;
+#pragma unroll
+        for (int i = k + 1; i < L; ++i) {
+            if (!kept[i]) continue;
+            bool have = false;
+            double s = 0.0;
+#pragma unroll
+            for (int c = 0; c < k; ++c)
+                if (kept[c]) { const double pr = K[i * L + c] * K[k * L + c]; s = have ? s + pr : pr; have = true; }
+            if (have) K[i * L + k] = K[i * L + k] - s;
+        }
+#pragma unroll
+        for (int i = k + 1; i < L; ++i)
+            if (kept[i]) K[i * L + k] = K[i * L + k] / x;
+    }
+    // R = (L'L)^-1 by forward/backward substitution on lower(K)
+    double R[L * L];
+#pragma unroll
+    for (int col = 0; col < L; ++col) {
+        if (!kept[col]) continue;
+#pragma unroll
+        for (int k = 0; k < L; ++k) {
+            if (!kept[k]) continue;
+            double y = (k == col) ? 1.0 : 0.0;
+#pragma unroll
+            for (int c = 0; c < k; ++c)
+                if (kept[c]) y = y - K[k * L + c] * R[c * L + col];
+            R[k * L + col] = y / K[k * L + k];
+        }
+#pragma unroll
+        for (int k = L - 1; k >= 0; --k) {
+            if (!kept[k]) continue;
+            double y = R[k * L + col];
+#pragma unroll
+            for (int c = k + 1; c < L; ++c)
+                if (kept[c]) y = y - K[c * L + k] * R[c * L + col];
+            R[k * L + col] = y / K[k * L + k];
+        }
+    }
+    // LR = L R  (n x r)
+    double LR[L * L];
+#pragma unroll
+    for (int i = 0; i < L; ++i)
+#pragma unroll
+        for (int y = 0; y < L; ++y) {
+            if (!kept[y]) continue;
+            bool have = false;
+            double s = 0.0;
+#pragma unroll
+            for (int x = 0; x < L; ++x)
+                if (kept[x]) { const double pr = Lm[i * L + x] * R[x * L + y]; s = have ? s + pr : pr; have = true; }
+            LR[i * L + y] = s;
+        }
+    // T = LR LR'; out = T a'  (stats.hpp:207)
+    double T[L * L];
+#pragma unroll
+    for (int i = 0; i < L; ++i)
+#pragma unroll
+        for (int j = 0; j < L; ++j) {
+            bool have = false;
+            double s = 0.0;
+#pragma unroll
+            for (int y = 0; y < L; ++y)
+                if (kept[y]) { const double pr = LR[i * L + y] * LR[j * L + y]; s = have ? s + pr : pr; have = true; }
+            T[i * L + j] = s;
+        }
+#pragma unroll
+    for (int i = 0; i < L; ++i)
+#pragma unroll
+        for (int j = 0; j < L; ++j) {
+            double s = T[i * L + 0] * a[j * L + 0];
+#pragma unroll
+            for (int q = 1; q < L; ++q) s = s + T[i * L + q] * a[j * L + q];
+            out[i * L + j] = s;
+        }
+}
+
+// --------------------------------------------------------- decision
+// Outcome codes of one CI test.
+enum : int { kDependent = 0, kIndependent = 1, kNanError = 2 };
+
+// Exact reference decision from (h01, denom) (stats.hpp:301-306 + 345-351).
+__device__ __forceinline__ int decide_exact(double h01, double denom, double tau, double* z_out = nullptr,
+                                            double* rho_out = nullptr) {
+    if (!(denom > 0.0)) {  // degenerate -> dependent, z = +inf
+        if (z_out) *z_out = __longlong_as_double(0x7ff0000000000000ll);
+        if (rho_out) *rho_out = 0.0;
+        return kDependent;
+    }
+    double v = h01 / sqrt(denom);
+    v = v < -kRhoClamp ? -kRhoClamp : (v > kRhoClamp ? kRhoClamp : v);
+    if (rho_out) *rho_out = v;
+    if (!(v > -1.0 && v < 1.0)) return kNanError;  // fisher_z throws (stats.hpp:112)
+    const double z = fabs(0.5 * log((1.0 + v) / (1.0 - v)));
+    if (z_out) *z_out = z;
+    return z <= tau ? kIndependent : kDependent;
+}
+
+// Same decision; the log is skipped when rho^2 is provably outside the
+// +-1e-9 band around tanh(tau)^2 (host-computed lo2 / hi2 in long double).
+__device__ __forceinline__ int decide_fast(double h01, double denom, const Thresholds& th) {
+    if (!(denom > 0.0)) return kDependent;
+    const double A = h01 * h01;
+    if (denom >= 1e-250 && A >= 1e-250) {
+        if (A <= denom * th.lo2) return kIndependent;
+        if (A >= denom * th.hi2) return kDependent;
+    }
+    return decide_exact(h01, denom, th.tau);
+}
+
+// Level-0 decision on rho = clamp(c_ij) (stats.hpp:309-312).
+__device__ __forceinline__ int decide0(double c, const Thresholds& th) {
+    const double ac = fabs(c);
+    if (ac <= th.lo) return kIndependent;
+    if (ac >= th.hi) return kDependent;
+    double v = c < -kRhoClamp ? -kRhoClamp : (c > kRhoClamp ? kRhoClamp : c);
+    if (!(v > -1.0 && v < 1.0)) return kNanError;
+    const double z = fabs(0.5 * log((1.0 + v) / (1.0 - v)));
+    return z <= th.tau ? kIndependent : kDependent;
+}
+
+// Partial-correlation pieces with a shared inverse (stats.hpp:292-307):
+// given ciS (M1 row 0), P0 = ciS * Minv, h00 = 1 - P0.ciS (all per set)
+// and the target's cjS (M1 row 1) and c_ij, return (h01, denom).
+template <int L>
+__device__ __forceinline__ void h_terms(const double* Minv, const double* ciS, const double* P0, double h00,
+                                        const double (&cjS)[L], double cij, double& h01, double& denom) {
+    double P1[L];
+#pragma unroll
+    for (int col = 0; col < L; ++col) {
+        double s = cjS[0] * Minv[0 * L + col];
+#pragma unroll
+        for (int k = 1; k < L; ++k) s = s + cjS[k] * Minv[k * L + col];
+        P1[col] = s;
+    }
+    double d11 = P1[0] * cjS[0], d01 = P0[0] * cjS[0], d10 = P1[0] * ciS[0];
+#pragma unroll
+    for (int k = 1; k < L; ++k) {
+        d11 = d11 + P1[k] * cjS[k];
+        d01 = d01 + P0[k] * cjS[k];
+        d10 = d10 + P1[k] * ciS[k];
+    }
+    const double h11 = 1.0 - d11;
+    h01 = cij - 0.5 * (d01 + d10);
+    denom = h00 * h11;
+}
+
+// P0 = ciS * Minv and h00 = 1 - P0.ciS (row 0 of stats.hpp:296-297).
+template <int L>
+__device__ __forceinline__ void p0_terms(const double (&Minv)[L * L], const double (&ciS)[L], double (&P0)[L],
+                                         double& h00) {
+#pragma unroll
+    for (int col = 0; col < L; ++col) {
+        double s = ciS[0] * Minv[0 * L + col];
+#pragma unroll
+        for (int k = 1; k < L; ++k) s = s + ciS[k] * Minv[k * L + col];
+        P0[col] = s;
+    }
+    double d00 = P0[0] * ciS[0];
+#pragma unroll
+    for (int k = 1; k < L; ++k) d00 = d00 + P0[k] * ciS[k];
+    h00 = 1.0 - d00;
+}
+
+}  // namespace pcs

@@ -1,0 +1,85 @@
+// pcs_internal.h -- shared declarations between the host driver (host.cu) and
+// the kernel translation units (level.cu, corr.cu).  Not part of the ABI.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "pcs_device.cuh"
+
+namespace pcs {
+
+constexpr int kMaxTemplLevel = 8;  // ell handled by register-resident templates
+
+// Device-side counters of one level (zeroed by the host before each level).
+struct Counters {
+    unsigned long long ci_serial;   // serial-equivalent ci_tests (Appendix B of SURVEY.md)
+    unsigned long long removed;     // edges removed
+    unsigned long long gpu_tests;   // CI tests executed on the device
+    unsigned long long gpu_pinv;    // pseudo-inverses executed on the device
+    unsigned long long rec_count;   // sepset records written
+    unsigned long long units[2];    // persistent-grid work cursors (pass A / B)
+    int err_nan;                    // fisher_z would throw (NaN statistic)
+    int err_other;
+};
+
+// Summary of a fresh snapshot (compact(), core.hpp:227-239).
+struct SnapInfo {
+    long long e_dir;      // directed entries (2E)
+    long long e_und;      // undirected edges (E)
+    int max_width;
+    int pad;
+};
+
+// Everything a level kernel reads.
+struct LevelArgs {
+    const double* C;
+    long long ldc;
+    int p;
+    int ell;
+    const int32_t* off;      // p+1
+    const int32_t* nbr;      // 2E, ascending rows
+    const int32_t* lowcnt;   // p: neighbours < i
+    const int32_t* upoff;    // p+1: prefix of (deg - lowcnt)
+    const int32_t* eid;      // 2E: undirected id of each directed entry
+    const int32_t* eu_a;     // E: row a (a < b)
+    const int32_t* eu_qa;    // E: position of b in row a
+    const int32_t* eu_qb;    // E: position of a in row b
+    unsigned long long* keys;  // E
+    BinomTable binom;
+    Thresholds th;
+    Counters* cnt;
+};
+
+// ---- corr.cu
+void launch_normalize_corr(double* C, long long ldc, int p, int* err, cudaStream_t s);
+void launch_correlation(const double* X, int m, int p, double* Xc, double* G, long long ldg, double* mean,
+                        double* C, long long ldc, int* err_flags, cudaStream_t s);
+
+// ---- level.cu
+void launch_level0(const double* C, long long ldc, int p, int W, uint32_t* adj, Thresholds th, Counters* cnt,
+                   cudaStream_t s);
+void launch_snapshot_degrees(const uint32_t* adj, int p, int W, int32_t* deg, int32_t* lowcnt, cudaStream_t s);
+void launch_snapshot_scan(const int32_t* deg, const int32_t* lowcnt, int p, int32_t* off, int32_t* upoff,
+                          SnapInfo* info, cudaStream_t s);
+void launch_snapshot_fill(const uint32_t* adj, int p, int W, const int32_t* off, int32_t* nbr, cudaStream_t s);
+void launch_edge_index(const LevelArgs& A, int32_t* eid, int32_t* eu_a, int32_t* eu_qa, int32_t* eu_qb,
+                       cudaStream_t s);
+void launch_fill_keys(unsigned long long* keys, long long n, cudaStream_t s);
+// per-row work prefix for a pass (units of work: target tiles for ell=1, set bands for ell>=2,
+// restricted to [row_begin,row_end) for sharding); returns nothing, writes prefix[p+1]
+void launch_row_work(const LevelArgs& A, int pass, int variant, int row_begin, int row_end,
+                     unsigned long long* prefix, cudaStream_t s);
+void launch_level1(const LevelArgs& A, int pass, const unsigned long long* prefix, unsigned long long u_begin,
+                   unsigned long long u_end, cudaStream_t s);
+int launch_level_set(const LevelArgs& A, int pass, const unsigned long long* prefix, unsigned long long u_begin,
+                     unsigned long long u_end, int num_sms, cudaStream_t s);
+int launch_level_edge(const LevelArgs& A, int pass, long long e_begin, long long e_end, int num_sms,
+                      cudaStream_t s);
+void launch_commit(const LevelArgs& A, uint32_t* adj, int W, long long e_und, int32_t* rec, cudaStream_t s);
+// parity helpers (stats::ci_test / pseudo_inverse on the device, one test per thread)
+int launch_ci_batch(const double* C, long long ldc, int p, int ell, long long n, const int32_t* ij,
+                    const int32_t* sets, double tau, uint8_t* indep, double* z, double* rho, uint8_t* degen,
+                    int* err, cudaStream_t s);
+int launch_pinv_batch(const double* a, int ell, long long n, double* out, cudaStream_t s);
+
+}  // namespace pcs
