@@ -1,0 +1,361 @@
+#!/usr/bin/env python3
+"""bench.py -- PC-stable skeleton discovery (cuPC) on B200: serial-equivalent CI tests/s.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--workload C2]
+
+Metric (BASELINE.json): skeleton wall time and CI tests/sec.  A "step" is one
+compute_correlation + run_pc_stable pass (stats.hpp:132 + skeleton.hpp:341, the
+pair bench.hpp:107-113 times) over the workload's data.  `value` counts the
+serial-equivalent CI tests -- exactly LevelStats::ci_tests of the reference's
+Strategy::Serial on the same correlation matrix, a deterministic property of the
+input -- divided by the device time of the step with the data resident in HBM.
+
+Default workload = BASELINE configs[1] ("C2"): p=1000 variables, m=10000
+samples, random-DAG density 0.1, alpha=0.01, reference generator seeds
+7919/7920 (bench.hpp:94-96, case index 1), capped at level 3 through the
+reference's own SkeletonConfig::max_level: with the reference generator the
+uncapped run does not terminate in practice (level 4 alone is 2.3e13 and level 5
+about 1e15 serial-equivalent CI tests).
+
+N > 1 (torchrun): every rank holds the data, builds the correlation matrix and
+the per-level snapshot; each level's passes are sharded by work units and the
+key arrays are MIN-all-reduced over NCCL (paper_1812_08491_b200/multigpu.py);
+`value` is the same whole-job test count over the max-over-ranks device time
+("scaling": "strong").
+
+--impl reference times the reference algorithm on the host cores (the CPU
+oracle restatement of proj/include/pcstable; the reference itself cannot be
+built here) on a bounded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+WORKLOADS = {
+    "C1": dict(p=100, m=1000, d=2.0 / 99.0, alpha=0.01, case=0, max_level=None),
+    "C2": dict(p=1000, m=10000, d=0.1, alpha=0.01, case=1, max_level=3),
+    "C3": dict(p=1643, m=850, d=0.01, alpha=0.01, case=2, max_level=None),
+    "C4": dict(p=5361, m=63, d=0.002, alpha=0.01, case=3, max_level=None),
+}
+SNAPSHOT_FIXTURE = os.path.join(ROOT, "tests", "golden", "c2_level3_snapshot.npz")
+
+
+def describe(name: str, wl: dict) -> str:
+    cap = f", max_level={wl['max_level']}" if wl["max_level"] is not None else ""
+    return (f"{name}: p={wl['p']}, m={wl['m']} (BASELINE n), density={wl['d']:.6g}, alpha={wl['alpha']}"
+            f"{cap}, seed={7919 * wl['case']}")
+
+
+def flops_per_level(ell: int, tests: int, pinvs: int) -> float:
+    """4l^2+8l+13 flop per CI test and 38l^3/3 per pseudo-inverse (level 0: 6)."""
+    if ell == 0:
+        return 6.0 * tests
+    return tests * (4 * ell * ell + 8 * ell + 13) + pinvs * 38.0 * ell ** 3 / 3.0
+
+
+# ---------------------------------------------------------------- clocks
+class ClockSampler:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                                          "-lms", "200", "-i", str(self.device)], stdout=subprocess.PIPE,
+                                         stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                out, _ = self.proc.communicate(timeout=5)
+            except Exception:
+                out = ""
+            self.lines = [ln for ln in out.splitlines() if ln.strip()]
+        else:
+            self.lines = []
+
+    def summary(self) -> dict:
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                smax.append(float(f[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(smax), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ---------------------------------------------------------------- CPU side (reference arm / cpu_baseline)
+def cpu_sample(name: str, wl: dict, target_s: float, threads: int):
+    """Times the reference's fastest strategy (SetShared, all host threads) on a bounded sample of the
+    workload with the CPU oracle; returns (tests_per_s, description)."""
+    from oracle import pyoracle as O  # test infrastructure: the reference restated on the CPU
+
+    seed = 7919 * wl["case"]
+    w = O.random_dag(wl["p"], wl["d"], seed)
+    x = O.sample_linear_gaussian(w, wl["m"], seed + 1)
+    c = O.compute_correlation(x, threads=threads)
+    cfg = O.config(alpha=wl["alpha"], strategy=O.SET, workers=threads, set_groups=max(2, threads))
+    if name == "C2" and os.path.exists(SNAPSHOT_FIXTURE):
+        z = np.load(SNAPSHOT_FIXTURE)
+        off, idx = z["offsets"], z["indices"]
+        ell = int(z["level"])
+        tau = O.threshold_tau(wl["alpha"], wl["m"], ell)
+        widths = np.diff(off)
+        cost = np.array([math.comb(int(wd), ell) * max(int(wd) - ell, 0) for wd in widths], dtype=float)
+        order = np.argsort(cost)
+        # calibrate on the cheapest non-empty rows, then size the sample to ~target_s
+        nz = [r for r in order if cost[r] > 0]
+        cal_rows = nz[: max(threads, 4)]
+        t0 = time.time()
+        st = run_rows(O, c, off, idx, ell, tau, cfg, cal_rows)
+        rate = st.ci_tests / max(time.time() - t0, 1e-9)
+        budget = rate * target_s
+        rows, acc = [], 0.0
+        # evenly spaced rows across the cost distribution
+        for r in nz[:: max(1, len(nz) // 64)]:
+            if acc + cost[r] > budget and rows:
+                continue
+            rows.append(r)
+            acc += cost[r]
+        t0 = time.time()
+        st = run_rows(O, c, off, idx, ell, tau, cfg, rows)
+        dt = time.time() - t0
+        desc = (f"level {ell} of {name} (reference SetShared strategy, {threads} threads, set_groups={cfg.set_groups})"
+                f" on {len(rows)} of {int((widths > ell).sum())} rows of the level-{ell} snapshot "
+                f"(tests/golden/c2_level3_snapshot.npz): {st.ci_tests:.3e} CI tests in {dt:.2f} s")
+        return st.ci_tests / dt, desc
+    # whole workload on the CPU (small configs)
+    t0 = time.time()
+    r = O.run_pc_stable(c, wl["m"], cfg)
+    dt = time.time() - t0
+    tests = sum(l.ci_tests for l in r.levels)
+    return tests / dt, (f"full {name} run (reference SetShared strategy, {threads} threads): {tests:.3e} CI tests "
+                        f"in {dt:.2f} s")
+
+
+def run_rows(O, c, off, idx, ell, tau, cfg, rows):
+    """The reference's level on a snapshot restricted to `rows` (rows are independent units)."""
+    keep = np.zeros(len(off) - 1, bool)
+    keep[np.asarray(rows, int)] = True
+    off2 = [0]
+    idx2 = []
+    for i in range(len(off) - 1):
+        if keep[i]:
+            idx2.extend(idx[off[i]:off[i + 1]].tolist())
+        off2.append(len(idx2))
+    return O.run_level(c, np.asarray(off2, np.int32), np.asarray(idx2, np.int32), ell, tau, cfg)
+
+
+def reference_arm(args, name, wl):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    threads = os.cpu_count() or 1
+    rates, desc = [], ""
+    for k in range(args.warmup + args.steps):
+        rate, desc = cpu_sample(name, wl, args.cpu_seconds, threads)
+        if k >= args.warmup:
+            rates.append(rate)
+    value = statistics.mean(rates)
+    line = {
+        "metric": "CI tests/sec (serial-equivalent)", "value": value, "unit": "tests/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": None, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "impl": "reference",
+        "data": "synthetic (reference generator random_dag + sample_linear_gaussian)",
+        "config": {"workload": describe(name, wl), "variant": "reference SetShared (CPU)"},
+        "cpu_baseline": {"value": value, "unit": "tests/s", "cores": threads, "kind": "port", "sample": desc},
+        "e2e": {"value": value, "unit": "tests/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ---------------------------------------------------------------- GPU arm
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="C2", choices=sorted(WORKLOADS))
+    ap.add_argument("--variant", default="set", choices=["set", "edge"])
+    ap.add_argument("--max-level", type=int, default=-2, help="-2: workload default, -1: uncapped")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--verbose", action="store_true")
+    args = ap.parse_args()
+    name = args.workload
+    wl = dict(WORKLOADS[name])
+    if args.max_level != -2:
+        wl["max_level"] = None if args.max_level < 0 else args.max_level
+    if args.impl == "reference":
+        return reference_arm(args, name, wl)
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_1812_08491_b200 as pcs
+    from paper_1812_08491_b200.multigpu import run_pc_stable_sharded
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.cuda.current_device()
+    p, m = wl["p"], wl["m"]
+    seed = 7919 * wl["case"]
+    w = pcs.random_dag(p, wl["d"], seed)
+    x = pcs.sample_linear_gaussian(w, m, seed + 1)  # (m, p), column-major like Eigen
+    x_host = np.ascontiguousarray(x.T)               # row j = variable j
+    x_dev = torch.from_numpy(x_host).to(f"cuda:{dev}")
+    ldc = (p + 3) // 4 * 4
+    c_dev = torch.empty((p, ldc), dtype=torch.float64, device=f"cuda:{dev}")
+    stream = torch.cuda.Stream()
+    cfg = pcs.SkeletonConfig(alpha=wl["alpha"], max_level=wl["max_level"], strategy=pcs.Strategy(
+        "edge" if args.variant == "edge" else "set"), device=dev, stream=stream.cuda_stream)
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=f"cuda:{dev}")  # > 126 MB L2
+
+    def step():
+        if world == 1:
+            return pcs.run_pc_stable_data_device(x_dev.data_ptr(), m, p, cfg)
+        pcs.correlation_device(x_dev.data_ptr(), m, p, c_dev.data_ptr(), ldc, stream.cuda_stream)
+        return run_pc_stable_sharded(c_dev.data_ptr(), ldc, p, m, cfg, with_sepsets=False)
+
+    with torch.cuda.stream(stream):
+        for _ in range(args.warmup):
+            res = step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    launches0 = pcs.kernel_launches()
+    times = []
+    with ClockSampler(dev) as clk:
+        for _ in range(args.steps):
+            with torch.cuda.stream(stream):
+                flush.zero_()  # L2 flush between timed steps (outside the events)
+                e0 = torch.cuda.Event(enable_timing=True)
+                e1 = torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+                res = step()
+                e1.record(stream)
+            stream.synchronize()
+            times.append(e0.elapsed_time(e1))
+    torch.cuda.synchronize()
+    launches = pcs.kernel_launches() - launches0
+    total_ms = sum(times)
+    if world > 1:
+        t = torch.tensor([total_ms], dtype=torch.float64, device=f"cuda:{dev}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+        dist.barrier()
+    ms_per_step = total_ms / args.steps
+    serial_tests = sum(l.ci_tests for l in res.levels)
+    value = serial_tests / (ms_per_step * 1e-3)
+
+    # roofline of the dominant kernel (the CI-test kernels of the heaviest level)
+    dom = max(res.levels, key=lambda l: l.kernel_ms)
+    fl = flops_per_level(dom.level, dom.device_ci_tests, dom.device_pseudo_inverses)
+    achieved = fl / (dom.kernel_ms * 1e-3) / 1e12
+    peak = pcs.probe_fp64_tflops()
+    roofline = {"bound": "fp64", "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
+                "traffic": None,
+                "kernel": f"level-{dom.level} CI-test kernels ({'level1_kernel' if dom.level == 1 else 'level_set_kernel' if args.variant == 'set' else 'level_edge_kernel'}), 2 passes",
+                "kernel_ms": dom.kernel_ms, "algorithmic_flop": fl,
+                "peak_source": "pcs_probe_fp64_tflops (DFMA probe, this box; MEASURED_PEAKS.json has no FP64 figure)"}
+    prof = os.path.join(ROOT, "profiles", "r01_ncu_summary.json")
+    if os.path.exists(prof):
+        try:
+            roofline["traffic"] = json.load(open(prof)).get("traffic_bytes_per_launch")
+        except Exception:
+            pass
+
+    # end to end through the public API with host buffers (H2D of X and D2H of the result inside)
+    e2e = None
+    if not args.no_e2e and world == 1:
+        cfg_e = pcs.SkeletonConfig(alpha=wl["alpha"], max_level=wl["max_level"], strategy=cfg.strategy, device=dev)
+        x_pinned = torch.from_numpy(x_host).pin_memory().numpy().T  # (m, p) view, column-major
+        et = []
+        for _ in range(max(1, args.steps)):
+            flush.zero_()
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            r = pcs.run_pc_stable_data(x_pinned, cfg_e)
+            sep_n = r.sepsets.stored_count()
+            et.append(time.perf_counter() - t0)
+        rec_ints = sum((3 + l.level) * l.edges_removed for l in r.levels if l.level >= 1)
+        e2e = {"value": serial_tests / statistics.mean(et), "unit": "tests/s", "h2d_bytes_per_step": 8 * m * p,
+               "d2h_bytes_per_step": 4 * p * ((p + 31) // 32) + 4 * rec_ints + 72 * len(r.levels),
+               "s_per_step": statistics.mean(et), "removed_pairs": sep_n}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        threads = os.cpu_count() or 1
+        try:
+            rate, desc = cpu_sample(name, wl, args.cpu_seconds, threads)
+            cpu = {"value": rate, "unit": "tests/s", "cores": threads, "kind": "port", "sample": desc}
+        except Exception as exc:  # the oracle is a checker; never let it sink the GPU line
+            cpu = {"value": None, "unit": "tests/s", "cores": threads, "kind": "port", "sample": f"failed: {exc}"}
+
+    if rank == 0:
+        line = {
+            "metric": "CI tests/sec (serial-equivalent)", "value": value, "unit": "tests/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": f"synthetic (reference generator random_dag + sample_linear_gaussian, seeds {seed}/{seed + 1})",
+            "config": {
+                "workload": describe(name, wl), "variant": "cuPC-S" if args.variant == "set" else "cuPC-E",
+                "skeleton_wall_s": ms_per_step * 1e-3, "serial_ci_tests": serial_tests,
+                "levels_run": res.levels_run(), "stop_reason": res.stop_reason.value,
+                "edges_left": res.skeleton.edge_count(),
+                "per_level": [{"level": l.level, "ci_tests": l.ci_tests, "device_ci_tests": l.device_ci_tests,
+                               "device_pinv": l.device_pseudo_inverses, "removed": l.edges_removed,
+                               "kernel_ms": round(l.kernel_ms, 3)} for l in res.levels],
+                "l2": "flushed between timed steps (256 MiB write outside the events)",
+                "timing": "CUDA events on the library's stream per step, max over ranks",
+            },
+            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
+            "clocks": clk.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

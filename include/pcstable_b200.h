@@ -59,7 +59,9 @@ typedef struct {
     int32_t device;            /* CUDA device ordinal */
     int32_t shard_index;       /* multi-GPU session: this rank (0 for single GPU) */
     int32_t shard_count;       /* multi-GPU session: world size (1 for single GPU) */
-    int32_t reserved[5];
+    int32_t reserved0;
+    uint64_t stream;           /* cudaStream_t to run on (0: the library creates its own) */
+    int32_t reserved[4];
 } pcs_config;
 
 /* LevelStats (core.hpp:387-393) + device counters */
@@ -80,6 +82,9 @@ typedef struct pcs_session pcs_session;
 
 const char* pcs_version(void);
 const char* pcs_last_error(void); /* thread-local message of the last failure */
+unsigned long long pcs_kernel_launches(void); /* kernels launched by this library so far */
+/* measured FP64 FMA peak of the current device in TFLOP/s (roofline denominator of the CI kernels) */
+int pcs_probe_fp64_tflops(double* tflops);
 void pcs_config_default(pcs_config* cfg);
 
 /* stats::threshold_tau (stats.hpp:120-129); PCS_EINVAL for bad alpha/ell, PCS_ELEVEL for m - ell - 3 < 1 */
@@ -91,9 +96,16 @@ pcs_status pcs_correlation(const double* x, int32_t m, int32_t p, double* c_out,
 /* run_pc_stable (skeleton.hpp:341-391).  c: p x p host correlation matrix, validated and normalised
    exactly like the CorrelationMatrix constructor (core.hpp:73-95). */
 pcs_status pcs_run_pc_stable(const double* c, int32_t p, int32_t m, const pcs_config* cfg, pcs_result** out);
+/* compute_correlation from device-resident m x p column-major data into a device p x ldc buffer,
+   enqueued on `stream` (0 = legacy default stream); synchronous */
+pcs_status pcs_correlation_device(const double* d_x, int32_t m, int32_t p, double* d_c, int64_t ldc, uint64_t stream,
+                                  int32_t* zero_var_col);
 /* compute_correlation + run_pc_stable from m x p column-major host data (one device pipeline) */
 pcs_status pcs_run_pc_stable_data(const double* x, int32_t m, int32_t p, const pcs_config* cfg, pcs_result** out,
                                   int32_t* zero_var_col);
+/* same, with the m x p column-major data already in device memory */
+pcs_status pcs_run_pc_stable_data_device(const double* d_x, int32_t m, int32_t p, const pcs_config* cfg,
+                                         pcs_result** out, int32_t* zero_var_col);
 /* same as pcs_run_pc_stable with the correlation matrix already in device memory (row stride ldc) */
 pcs_status pcs_run_pc_stable_device(const double* d_c, int64_t ldc, int32_t p, int32_t m, const pcs_config* cfg,
                                     pcs_result** out);
@@ -109,6 +121,11 @@ int64_t pcs_result_member_total(const pcs_result* r);
 /* per unordered pair, triangular slot index of core.hpp:329-335: level (-1 = kept), offset into members */
 void pcs_result_sepsets(const pcs_result* r, int32_t* level, int64_t* offset, int32_t* members);
 double pcs_result_device_seconds(const pcs_result* r); /* CUDA-event time of the whole device pipeline */
+/* compact forms: live bitmask p x ceil(p/32) uint32 (bit j of word i*W + j/32), and the removal records
+   of levels >= 1 as consecutive (a, b, ell, members[ell]) int32 tuples (level-0 removals are implied) */
+void pcs_result_bitmask(const pcs_result* r, uint32_t* out);
+int64_t pcs_result_record_ints(const pcs_result* r);
+void pcs_result_records(const pcs_result* r, int32_t* out);
 void pcs_result_free(pcs_result* r);
 
 /* stats::ci_test for n tests of one level ell on the device (parity helper).
@@ -118,6 +135,12 @@ pcs_status pcs_ci_test_batch(const double* c, int32_t p, int32_t ell, int64_t n,
                              uint8_t* degenerate);
 /* stats::pseudo_inverse for n row-major ell x ell blocks on the device (parity helper) */
 pcs_status pcs_pseudo_inverse_batch(const double* a, int32_t ell, int64_t n, double* out);
+
+/* Benchmark-input generation, bit-identical to the reference generator (host, sequential by
+   construction): random_dag (datagen.hpp:42-56) -> weights n x n row-major (weights[i*n+j] != 0:
+   j causes i, j < i); sample_linear_gaussian (datagen.hpp:62-82) -> x m x n column-major. */
+pcs_status pcs_random_dag(int32_t n, double density, uint64_t seed, double* weights);
+pcs_status pcs_sample_linear_gaussian(const double* weights, int32_t n, int32_t m, uint64_t seed, double* x);
 
 /* Level-stepped session: the building block of multi-GPU runs (one process per GPU, the caller
    all-reduces the per-level key array with MIN between passes).  pcs_run_pc_stable is a session
@@ -132,6 +155,10 @@ pcs_status pcs_session_level_pass(pcs_session* s, int32_t pass);
 /* device pointer to the level's int64 key array (num_keys entries; MIN-reduce across ranks) */
 pcs_status pcs_session_keys(pcs_session* s, void** device_ptr, int64_t* count);
 pcs_status pcs_session_level_end(pcs_session* s);
+/* re-shard subsequent passes (multi-GPU rebalancing, profiling of a slice) */
+pcs_status pcs_session_set_shard(pcs_session* s, int32_t shard_index, int32_t shard_count);
+/* CSR snapshot of the current level (compact(), core.hpp:227-239): offsets[p+1], indices[offsets[p]] */
+pcs_status pcs_session_snapshot(pcs_session* s, int32_t* offsets, int32_t* indices);
 pcs_status pcs_session_finish(pcs_session* s, pcs_result** out);
 void pcs_session_free(pcs_session* s);
 

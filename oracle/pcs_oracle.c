@@ -29,6 +29,7 @@ static void set_err(const char* msg) {
 const char* orc_last_error(void) { return g_err; }
 
 #define NONE_KEY INT64_MAX
+static double now_s(void);
 
 /* ===================================================== rng.hpp:10-81 ===== */
 static uint64_t splitmix_next(uint64_t* st) { /* rng.hpp:14-19 */
@@ -1190,6 +1191,64 @@ static int run_level_keys(level_ctx* X, orc_level_stats* st) {
     st->pseudo_inverses = tests;
     st->edges_removed = removed;
     return ORC_OK;
+}
+
+/* One level (ell >= 1) of a strategy on a given snapshot, restricted to rows
+ * [row_begin, row_end) -- the bounded CPU sample bench.py times.  The live graph
+ * starts as the snapshot (run_level_* of skeleton.hpp:292-333). */
+int orc_run_level(const double* c, int p, const int32_t* offsets, const int32_t* indices, int ell, double tau,
+                  const orc_config* cfg, int row_begin, int row_end, orc_level_stats* out) {
+    if (ell < 1) { set_err("run_level: need ell >= 1"); return ORC_EINVAL; }
+    orc_result* R = (orc_result*)calloc(1, sizeof(orc_result));
+    if (!R) return ORC_ENOMEM;
+    R->p = p;
+    R->adj = (atomic_uchar*)malloc(sizeof(atomic_uchar) * (size_t)p * p);
+    const size_t ns = (size_t)p * (p - 1) / 2;
+    R->slots = (_Atomic(sepset_t*)*)malloc(sizeof(*R->slots) * (ns ? ns : 1));
+    if (!R->adj || !R->slots) { orc_result_free(R); return ORC_ENOMEM; }
+    for (size_t q = 0; q < ns; ++q) atomic_init(&R->slots[q], NULL);
+    for (size_t q = 0; q < (size_t)p * p; ++q) atomic_init(&R->adj[q], 0);
+    snapshot_t S;
+    S.p = p;
+    S.off = (int32_t*)malloc(sizeof(int32_t) * (size_t)(p + 1));
+    S.idx = (int32_t*)malloc(sizeof(int32_t) * (size_t)(offsets[p] + 1));
+    S.max_width = 0;
+    if (row_begin < 0) row_begin = 0;
+    if (row_end > p) row_end = p;
+    /* restrict the snapshot rows outside the range to empty (their units skip) */
+    int32_t n = 0;
+    for (int i = 0; i < p; ++i) {
+        S.off[i] = n;
+        for (int q = offsets[i]; q < offsets[i + 1]; ++q) {
+            const int j = indices[q];
+            atomic_store(&R->adj[(size_t)i * p + j], 1);
+            if (i >= row_begin && i < row_end) S.idx[n++] = j;
+        }
+        if ((int)(n - S.off[i]) > S.max_width) S.max_width = (int)(n - S.off[i]);
+    }
+    S.off[p] = n;
+    orc_config cfg2 = *cfg;
+    level_ctx X = {c, p, &S, R, tau, ell, &cfg2};
+    orc_level_stats st;
+    memset(&st, 0, sizeof st);
+    const double t0 = now_s();
+    int rc;
+    switch (cfg->strategy) {
+        case ORC_SERIAL: rc = run_level_serial(&X, &st); break;
+        case ORC_EDGE: {
+            const int chunks = (S.max_width + cfg->edges_per_unit - 1) / cfg->edges_per_unit;
+            rc = run_level_units(&X, chunks, ORC_EDGE, &st);
+            break;
+        }
+        case ORC_SET: rc = run_level_units(&X, cfg->set_groups, ORC_SET, &st); break;
+        default: rc = run_level_keys(&X, &st); break;
+    }
+    st.elapsed_s = now_s() - t0;
+    st.level = ell;
+    snap_free(&S);
+    orc_result_free(R);
+    if (!rc) *out = st;
+    return rc;
 }
 
 void orc_config_default(orc_config* cfg) { /* core.hpp:357-368 */

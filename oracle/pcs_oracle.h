@@ -125,6 +125,10 @@ void orc_result_free(orc_result* r);
 int orc_level_keys(const double* c, int p, const int32_t* offsets, const int32_t* indices, int ell,
                    double tau, int64_t e_begin, int64_t e_end, int64_t* keys, int threads);
 
+/* one level on a given snapshot, rows [row_begin, row_end) only (bounded CPU sample) */
+int orc_run_level(const double* c, int p, const int32_t* offsets, const int32_t* indices, int ell, double tau,
+                  const orc_config* cfg, int row_begin, int row_end, orc_level_stats* out);
+
 #ifdef __cplusplus
 }
 #endif

@@ -328,3 +328,19 @@ def level_keys(c: np.ndarray, offsets: np.ndarray, indices: np.ndarray, ell: int
     _check(lib().orc_level_keys(_dp(c), p, _ip(off), _ip(idx), ell, tau, e_begin, e_end,
                                 keys.ctypes.data_as(ct.POINTER(ct.c_int64)), threads))
     return keys[:max(e_end - e_begin, 0)]
+
+
+def run_level(c: np.ndarray, offsets: np.ndarray, indices: np.ndarray, ell: int, tau: float,
+              cfg: OrcConfig, row_begin: int = 0, row_end: int | None = None) -> LevelStats:
+    """One level of a reference strategy on a given snapshot, rows [row_begin, row_end) only."""
+    c = np.ascontiguousarray(c, np.float64)
+    p = c.shape[0]
+    off = np.ascontiguousarray(offsets, np.int32)
+    idx = np.ascontiguousarray(indices if len(indices) else np.zeros(1, np.int32), np.int32)
+    st = OrcLevel()
+    lib().orc_run_level.argtypes = [ct.POINTER(ct.c_double), ct.c_int, ct.POINTER(ct.c_int32),
+                                    ct.POINTER(ct.c_int32), ct.c_int, ct.c_double, ct.POINTER(OrcConfig),
+                                    ct.c_int, ct.c_int, ct.POINTER(OrcLevel)]
+    _check(lib().orc_run_level(_dp(c), p, _ip(off), _ip(idx), ell, tau, ct.byref(cfg), row_begin,
+                               p if row_end is None else row_end, ct.byref(st)))
+    return LevelStats(st.level, st.ci_tests, st.pseudo_inverses, st.edges_removed, st.elapsed_s)

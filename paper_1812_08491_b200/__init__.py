@@ -27,7 +27,8 @@ __all__ = [
     "Strategy", "StopReason", "SkeletonConfig", "LevelStats", "SkeletonResult", "AdjacencyMatrix",
     "SeparationSets", "ZeroVarianceError", "LevelUnreachableError", "PcsError", "compute_correlation",
     "threshold_tau", "run_pc_stable", "run_pc_stable_data", "ci_test_batch", "pseudo_inverse_batch",
-    "Session", "library", "LIB_PATH",
+    "Session", "library", "LIB_PATH", "random_dag", "sample_linear_gaussian", "run_pc_stable_data_device",
+    "run_pc_stable_device", "correlation_device", "kernel_launches",
 ]
 
 PKG_DIR = os.path.dirname(os.path.abspath(__file__))
@@ -76,7 +77,8 @@ class _Config(ct.Structure):
         ("alpha", ct.c_double), ("max_level", ct.c_int32), ("variant", ct.c_int32),
         ("edges_per_unit", ct.c_int32), ("workers_per_edge", ct.c_int32), ("set_groups", ct.c_int32),
         ("unit_width", ct.c_int32), ("device", ct.c_int32), ("shard_index", ct.c_int32),
-        ("shard_count", ct.c_int32), ("reserved", ct.c_int32 * 5),
+        ("shard_count", ct.c_int32), ("reserved0", ct.c_int32), ("stream", ct.c_uint64),
+        ("reserved", ct.c_int32 * 4),
     ]
 
 
@@ -108,6 +110,9 @@ def library():
     L.pcs_correlation.argtypes = [dp, ct.c_int32, ct.c_int32, dp, ip]
     L.pcs_run_pc_stable.argtypes = [dp, ct.c_int32, ct.c_int32, ct.POINTER(_Config), ct.POINTER(vp)]
     L.pcs_run_pc_stable_data.argtypes = [dp, ct.c_int32, ct.c_int32, ct.POINTER(_Config), ct.POINTER(vp), ip]
+    L.pcs_run_pc_stable_data_device.argtypes = [vp, ct.c_int32, ct.c_int32, ct.POINTER(_Config), ct.POINTER(vp), ip]
+    L.pcs_random_dag.argtypes = [ct.c_int32, ct.c_double, ct.c_uint64, dp]
+    L.pcs_sample_linear_gaussian.argtypes = [dp, ct.c_int32, ct.c_int32, ct.c_uint64, dp]
     L.pcs_run_pc_stable_device.argtypes = [vp, ct.c_int64, ct.c_int32, ct.c_int32, ct.POINTER(_Config),
                                            ct.POINTER(vp)]
     L.pcs_result_p.argtypes = [vp]
@@ -122,6 +127,15 @@ def library():
     L.pcs_result_sepsets.argtypes = [vp, ip, ct.POINTER(ct.c_int64), ip]
     L.pcs_result_device_seconds.argtypes = [vp]
     L.pcs_result_device_seconds.restype = ct.c_double
+    L.pcs_result_bitmask.argtypes = [vp, ct.POINTER(ct.c_uint32)]
+    L.pcs_result_record_ints.argtypes = [vp]
+    L.pcs_result_record_ints.restype = ct.c_int64
+    L.pcs_result_records.argtypes = [vp, ip]
+    L.pcs_correlation_device.argtypes = [vp, ct.c_int32, ct.c_int32, vp, ct.c_int64, ct.c_uint64, ip]
+    L.pcs_kernel_launches.restype = ct.c_ulonglong
+    L.pcs_probe_fp64_tflops.argtypes = [dp]
+    L.pcs_session_snapshot.argtypes = [vp, ip, ip]
+    L.pcs_session_set_shard.argtypes = [vp, ct.c_int32, ct.c_int32]
     L.pcs_result_free.argtypes = [vp]
     L.pcs_ci_test_batch.argtypes = [dp, ct.c_int32, ct.c_int32, ct.c_int64, ip, ip, ct.c_double, u8p, dp, dp, u8p]
     L.pcs_pseudo_inverse_batch.argtypes = [dp, ct.c_int32, ct.c_int64, dp]
@@ -172,6 +186,7 @@ class SkeletonConfig:  # core.hpp:357-384
     worker_count: int = 1           # CPU knob of the reference; inert on the device
     schedule_seed: Optional[int] = None  # inert: device results never depend on schedule
     device: int = 0
+    stream: int = 0                 # cudaStream_t handle to run on (0: library-owned stream)
 
     def validate(self):  # core.hpp:370-383
         if not (0.0 < self.alpha < 1.0):
@@ -192,6 +207,7 @@ class SkeletonConfig:  # core.hpp:357-384
         c.edges_per_unit, c.workers_per_edge = self.edges_per_unit, self.workers_per_edge
         c.set_groups, c.unit_width = self.set_groups, self.unit_width
         c.device, c.shard_index, c.shard_count = self.device, shard_index, shard_count
+        c.stream = int(self.stream)
         return c
 
 
@@ -208,30 +224,52 @@ class LevelStats:  # core.hpp:387-393 (+ device counters)
 
 
 class AdjacencyMatrix:
-    """Read-only view with the reference's accessors (core.hpp:109-194)."""
+    """Read-only skeleton with the reference's accessors (core.hpp:109-194), backed by the
+    device's live bitmask (bit j of word i*W + j/32)."""
 
-    def __init__(self, cells: np.ndarray):
-        self.cells = cells
+    def __init__(self, bits: np.ndarray, n: int):
+        self.bits = bits
+        self.n = n
+        self._cells = None
+
+    @property
+    def cells(self) -> np.ndarray:
+        if self._cells is None:
+            b = np.unpackbits(self.bits.view(np.uint8).reshape(self.n, -1), axis=1, bitorder="little")
+            self._cells = np.ascontiguousarray(b[:, : self.n])
+        return self._cells
 
     def size(self) -> int:
-        return self.cells.shape[0]
+        return self.n
 
     def at(self, i: int, j: int) -> bool:
-        return bool(self.cells[i, j])
+        return bool((int(self.bits[i, j >> 5]) >> (j & 31)) & 1)
 
     def edge_count(self) -> int:
         return int(np.triu(self.cells, 1).sum())
+
+    def edges(self) -> np.ndarray:
+        """(E, 2) array of surviving edges (i < j), ascending."""
+        return np.argwhere(np.triu(self.cells, 1))
 
     def __eq__(self, other) -> bool:
         return isinstance(other, AdjacencyMatrix) and np.array_equal(self.cells, other.cells)
 
 
 class SeparationSets:
-    """Sepsets keyed by unordered pair (core.hpp:267-339)."""
+    """Sepsets keyed by unordered pair (core.hpp:267-339).  Level-0 removals carry the empty set;
+    removals at level >= 1 come from the device's (a, b, ell, members...) records."""
 
-    def __init__(self, n: int, sets: dict):
+    def __init__(self, n: int, skeleton: AdjacencyMatrix, records: np.ndarray):
         self.n = n
-        self._sets = sets
+        self._skel = skeleton
+        self._rec = {}
+        k = 0
+        while k < len(records):
+            a, b, ell = int(records[k]), int(records[k + 1]), int(records[k + 2])
+            self._rec[(min(a, b), max(a, b))] = tuple(int(v) for v in records[k + 3:k + 3 + ell])
+            k += 3 + ell
+        self._dict = None
 
     def size(self) -> int:
         return self.n
@@ -239,17 +277,27 @@ class SeparationSets:
     def find(self, i: int, j: int):
         if i == j or not (0 <= i < self.n and 0 <= j < self.n):
             raise ValueError("SeparationSets: invalid vertex pair")
-        return self._sets.get((min(i, j), max(i, j)))
-
-    def stored_count(self) -> int:
-        return len(self._sets)
-
-    def for_each(self) -> Iterator:
-        for k in sorted(self._sets):
-            yield k[0], k[1], self._sets[k]
+        key = (min(i, j), max(i, j))
+        if self._skel.at(*key):
+            return None
+        return self._rec.get(key, ())
 
     def as_dict(self) -> dict:
-        return dict(self._sets)
+        if self._dict is None:
+            iu, ju = np.nonzero(np.triu(1 - self._skel.cells, 1))
+            d = {(int(a), int(b)): () for a, b in zip(iu, ju)}
+            d.update(self._rec)
+            self._dict = d
+        return self._dict
+
+    def stored_count(self) -> int:
+        n = self.n
+        return n * (n - 1) // 2 - self._skel.edge_count()
+
+    def for_each(self) -> Iterator:
+        d = self.as_dict()
+        for k in sorted(d):
+            yield k[0], k[1], d[k]
 
 
 @dataclass
@@ -264,8 +312,7 @@ class SkeletonResult:  # skeleton.hpp:33-40
         return len(self.levels)
 
     def edge_set(self):
-        iu = np.argwhere(np.triu(self.skeleton.cells, 1))
-        return [tuple(map(int, e)) for e in iu]
+        return [tuple(map(int, e)) for e in self.skeleton.edges()]
 
 
 def _dp(a):
@@ -277,27 +324,23 @@ def _ip(a):
 
 
 def _collect(h, with_sepsets: bool = True) -> SkeletonResult:
+    """Copies a pcs_result into Python objects (bitmask + records; sepsets decoded lazily)."""
     L = library()
     p = L.pcs_result_p(h)
     lv = (_Level * 256)()
     n = L.pcs_result_levels(h, lv, 256)
     levels = [LevelStats(lv[k].level, lv[k].ci_tests, lv[k].pseudo_inverses, lv[k].edges_removed, lv[k].elapsed_s,
                          lv[k].device_ci_tests, lv[k].device_pseudo_inverses, lv[k].kernel_ms) for k in range(n)]
-    adj = np.empty((p, p), np.uint8)
-    L.pcs_result_adjacency(h, adj.ctypes.data_as(ct.POINTER(ct.c_uint8)))
-    sets = {}
-    if with_sepsets:
-        ns = p * (p - 1) // 2
-        tot = L.pcs_result_member_total(h)
-        lvl = np.empty(ns, np.int32)
-        off = np.empty(ns, np.int64)
-        mem = np.empty(max(tot, 1), np.int32)
-        L.pcs_result_sepsets(h, _ip(lvl), off.ctypes.data_as(ct.POINTER(ct.c_int64)), _ip(mem))
-        iu, ju = np.triu_indices(p, 1)
-        for s in np.nonzero(lvl >= 0)[0]:
-            sets[(int(iu[s]), int(ju[s]))] = tuple(int(v) for v in mem[off[s]:off[s] + lvl[s]])
-    return SkeletonResult(AdjacencyMatrix(adj), SeparationSets(p, sets), levels, _STOP[L.pcs_result_stop_reason(h)],
-                          L.pcs_result_device_seconds(h))
+    W = (p + 31) // 32
+    bits = np.empty((p, W), np.uint32)
+    L.pcs_result_bitmask(h, bits.ctypes.data_as(ct.POINTER(ct.c_uint32)))
+    nrec = L.pcs_result_record_ints(h)
+    rec = np.empty(max(nrec, 1), np.int32)
+    if nrec:
+        L.pcs_result_records(h, _ip(rec))
+    adj = AdjacencyMatrix(bits, p)
+    sep = SeparationSets(p, adj, rec[:nrec] if with_sepsets else np.empty(0, np.int32))
+    return SkeletonResult(adj, sep, levels, _STOP[L.pcs_result_stop_reason(h)], L.pcs_result_device_seconds(h))
 
 
 # ----------------------------------------------------------------- API
@@ -361,6 +404,66 @@ def run_pc_stable_data(data, cfg: Optional[SkeletonConfig] = None, with_sepsets:
         return _collect(h, with_sepsets)
     finally:
         library().pcs_result_free(h)
+
+
+def run_pc_stable_data_device(x_ptr: int, m: int, p: int, cfg: Optional[SkeletonConfig] = None,
+                              with_sepsets: bool = False) -> SkeletonResult:
+    """compute_correlation + run_pc_stable on m x p column-major data already in device memory."""
+    cfg = cfg or SkeletonConfig()
+    abi = cfg._abi()
+    h = ct.c_void_p()
+    col = ct.c_int32(-1)
+    rc = library().pcs_run_pc_stable_data_device(ct.c_void_p(x_ptr), m, p, ct.byref(abi), ct.byref(h),
+                                                 ct.byref(col))
+    if rc:
+        _raise(rc, col.value)
+    try:
+        return _collect(h, with_sepsets)
+    finally:
+        library().pcs_result_free(h)
+
+
+def correlation_device(x_ptr: int, m: int, p: int, c_ptr: int, ldc: int, stream: int = 0):
+    """compute_correlation from device-resident column-major data into a device p x ldc buffer."""
+    col = ct.c_int32(-1)
+    rc = library().pcs_correlation_device(ct.c_void_p(x_ptr), m, p, ct.c_void_p(c_ptr), ldc, stream, ct.byref(col))
+    if rc:
+        _raise(rc, col.value)
+
+
+def probe_fp64_tflops() -> float:
+    """Measured FP64 FMA peak (TFLOP/s) of the current device."""
+    out = ct.c_double()
+    rc = library().pcs_probe_fp64_tflops(ct.byref(out))
+    if rc:
+        _raise(rc)
+    return out.value
+
+
+def kernel_launches() -> int:
+    """Kernels launched by the library so far in this process."""
+    return int(library().pcs_kernel_launches())
+
+
+def random_dag(n: int, density: float, seed: int) -> np.ndarray:
+    """random_dag (datagen.hpp:42-56): n x n weights, weights[i, j] != 0 means j causes i (j < i)."""
+    w = np.empty((n, n), np.float64)
+    rc = library().pcs_random_dag(n, density, seed, _dp(w))
+    if rc:
+        raise ValueError("random_dag: need n >= 2 and density in (0, 1)")
+    return w
+
+
+def sample_linear_gaussian(weights: np.ndarray, m: int, seed: int) -> np.ndarray:
+    """sample_linear_gaussian (datagen.hpp:62-82): returns the (m, n) data matrix (samples x variables),
+    stored column-major like Eigen (x.T is C-contiguous)."""
+    w = np.ascontiguousarray(weights, np.float64)
+    n = w.shape[0]
+    xt = np.empty((n, m), np.float64)  # row j = variable j == column-major m x n
+    rc = library().pcs_sample_linear_gaussian(_dp(w), n, m, seed, _dp(xt))
+    if rc:
+        raise ValueError("sample_linear_gaussian: need m >= 4 and strictly lower-triangular weights")
+    return xt.T
 
 
 def run_pc_stable_device(c_ptr: int, ldc: int, p: int, sample_count: int, cfg: Optional[SkeletonConfig] = None,
@@ -451,6 +554,23 @@ class Session:
         if rc:
             _raise(rc)
         return ptr.value or 0, n.value
+
+    def set_shard(self, shard_index: int, shard_count: int):
+        rc = library().pcs_session_set_shard(self._h, shard_index, shard_count)
+        if rc:
+            _raise(rc)
+
+    def snapshot(self, p: int, e_dir: Optional[int] = None):
+        """CSR snapshot (offsets, indices) of the current level (compact(), core.hpp:227-239)."""
+        off = np.empty(p + 1, np.int32)
+        rc = library().pcs_session_snapshot(self._h, _ip(off), None)
+        if rc:
+            _raise(rc)
+        idx = np.empty(max(int(off[-1]), 1), np.int32)
+        rc = library().pcs_session_snapshot(self._h, _ip(off), _ip(idx))
+        if rc:
+            _raise(rc)
+        return off, idx[: int(off[-1])]
 
     def level_end(self):
         rc = library().pcs_session_level_end(self._h)

@@ -24,6 +24,7 @@ UNITS = {
     "level.cu": ["-fmad=false"],
     "corr.cu": [],
     "host.cu": [],
+    "probe.cu": [],
 }
 
 
@@ -61,6 +62,16 @@ def build(verbose: bool = False, force: bool = False) -> str:
                 raise RuntimeError(f"nvcc failed for {unit}")
             if verbose:
                 sys.stderr.write(res.stderr)
+    # host-only datagen: plain g++, no FMA contraction (reference Release build has none)
+    dsrc = os.path.join(CSRC, "datagen.cpp")
+    dobj = os.path.join(BUILD, "datagen.o")
+    objs.append(dobj)
+    if force or _stale(dobj, [dsrc, *headers, __file__]):
+        cmd = ["g++", "-O2", "-std=c++17", "-fPIC", "-ffp-contract=off", "-c", dsrc, "-o", dobj]
+        res = subprocess.run(cmd, capture_output=True, text=True)
+        if res.returncode != 0:
+            sys.stderr.write(res.stderr)
+            raise RuntimeError("g++ failed for datagen.cpp")
     if force or _stale(LIB, objs):
         cmd = [nvcc(), *ARCH, "-shared", "-o", LIB, *objs, "-lcudart_static", "-lrt", "-ldl", "-lpthread"]
         res = subprocess.run(cmd, capture_output=True, text=True)

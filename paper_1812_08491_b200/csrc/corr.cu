@@ -46,7 +46,9 @@ void launch_normalize_corr(double* C, long long ldc, int p, int* err, cudaStream
     long long n = (long long)p * p;
     long long blocks = (n + 255) / 256;
     if (blocks > 148 * 16) blocks = 148 * 16;
+    ++g_kernel_launches;
     normalize_kernel<<<(int)blocks, 256, 0, s>>>(C, ldc, p, err);
+    ++g_kernel_launches;
     set_diag_kernel<<<(p + 255) / 256, 256, 0, s>>>(C, ldc, p);
 }
 
@@ -175,18 +177,23 @@ __global__ void corr_finalize_kernel(const double* __restrict__ G, long long ldg
 void launch_correlation(const double* X, int m, int p, double* Xc, double* G, long long ldg, double* mean, double* C,
                         long long ldc, int* err_flags, cudaStream_t s) {
     const int ldk = (m + kGK - 1) / kGK * kGK;
+    ++g_kernel_launches;
     colmean_kernel<<<p, 256, 0, s>>>(X, m, p, mean, err_flags);
     long long n = (long long)p * ldk;
     long long blocks = (n + 255) / 256;
     if (blocks > 148 * 32) blocks = 148 * 32;
+    ++g_kernel_launches;
     center_kernel<<<(int)blocks, 256, 0, s>>>(X, m, p, mean, Xc, ldk);
     const int nb = (p + kGT - 1) / kGT;
+    ++g_kernel_launches;
     gram_dmma_kernel<<<dim3(nb, nb), 128, 0, s>>>(Xc, p, ldk, G, ldg);
     double* sd = mean;  // mean is dead after centring
+    ++g_kernel_launches;
     corr_sd_kernel<<<(p + 255) / 256, 256, 0, s>>>(G, ldg, p, sd, err_flags + 1);
     n = (long long)p * p;
     blocks = (n + 255) / 256;
     if (blocks > 148 * 32) blocks = 148 * 32;
+    ++g_kernel_launches;
     corr_finalize_kernel<<<(int)blocks, 256, 0, s>>>(G, ldg, p, sd, C, ldc);
 }
 

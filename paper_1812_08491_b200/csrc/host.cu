@@ -158,7 +158,7 @@ struct pcs_session {
     int device = 0, num_sms = 148;
     cudaStream_t st = nullptr;
     cudaEvent_t ev_begin = nullptr, ev_end = nullptr, ev_k0 = nullptr, ev_k1 = nullptr;
-    bool own_c = true;
+    bool own_c = true, own_stream = true;
     double* dC = nullptr;
     uint32_t* dAdj = nullptr;
     int32_t *dDeg = nullptr, *dLow = nullptr, *dOff = nullptr, *dUp = nullptr;
@@ -174,6 +174,8 @@ struct pcs_session {
     long long capRec = 0;
     unsigned long long* dBinom = nullptr;
     size_t capBinom = 0;
+    unsigned char* dScratch = nullptr;  // generic-ell per-lane scratch
+    long long capScratch = 0;
     // level state
     int ell = -1;
     bool stopped = false, in_level = false;
@@ -199,11 +201,12 @@ void free_session(pcs_session* s) {
     cudaFree(s->dInfo); cudaFree(s->dCnt); cudaFree(s->dPrefix); cudaFree(s->dNbr); cudaFree(s->dEid);
     cudaFree(s->dEuA); cudaFree(s->dEuQa); cudaFree(s->dEuQb); cudaFree(s->dKeys); cudaFree(s->dRec);
     cudaFree(s->dBinom);
+    cudaFree(s->dScratch);
     if (s->ev_begin) cudaEventDestroy(s->ev_begin);
     if (s->ev_end) cudaEventDestroy(s->ev_end);
     if (s->ev_k0) cudaEventDestroy(s->ev_k0);
     if (s->ev_k1) cudaEventDestroy(s->ev_k1);
-    if (s->st) cudaStreamDestroy(s->st);
+    if (s->st && s->own_stream) cudaStreamDestroy(s->st);
     delete s;
 }
 
@@ -233,7 +236,12 @@ pcs_status realloc_dev(T** ptr, long long n) {
 pcs_status session_alloc(pcs_session* s) {
     const int p = s->p;
     s->W = (p + 31) / 32;
-    CUDA_TRY(cudaStreamCreateWithFlags(&s->st, cudaStreamNonBlocking));
+    if (s->cfg.stream) {
+        s->st = reinterpret_cast<cudaStream_t>(s->cfg.stream);
+        s->own_stream = false;
+    } else {
+        CUDA_TRY(cudaStreamCreateWithFlags(&s->st, cudaStreamNonBlocking));
+    }
     CUDA_TRY(cudaEventCreate(&s->ev_begin));
     CUDA_TRY(cudaEventCreate(&s->ev_end));
     CUDA_TRY(cudaEventCreate(&s->ev_k0));
@@ -439,9 +447,16 @@ pcs_status pcs_session_level_begin(pcs_session* s, int32_t* running, int32_t* el
     if (!binomial_exact(maxw, ell, &tmp) || tmp >= (1ull << 62))
         return fail(PCS_EUNSUPPORTED, "level " + std::to_string(ell) + ": C(" + std::to_string(maxw) + ", " +
                                           std::to_string(ell) + ") conditioning sets per row exceed 2^62");
-    if (ell > kMaxTemplLevel)
+    if (ell > kMaxRtLevel)
         return fail(PCS_EUNSUPPORTED, "conditioning level " + std::to_string(ell) + " > " +
-                                          std::to_string(kMaxTemplLevel) + " not yet supported on the device");
+                                          std::to_string(kMaxRtLevel) + " not supported on the device");
+    if (ell > kMaxTemplLevel) {
+        const long long need = level_rt_scratch_bytes(ell, s->num_sms, nullptr);
+        if (need > s->capScratch) {
+            if ((st = realloc_dev(&s->dScratch, need))) return st;
+            s->capScratch = need;
+        }
+    }
     if (s->info.e_dir > s->capDir) {
         if ((st = realloc_dev(&s->dNbr, s->info.e_dir))) return st;
         if ((st = realloc_dev(&s->dEid, s->info.e_dir))) return st;
@@ -478,7 +493,7 @@ pcs_status pcs_session_level_pass(pcs_session* s, int32_t pass) {
     LevelArgs A = level_args(s);
     const int shard = s->cfg.shard_index, nsh = s->cfg.shard_count;
     if (!s->kernel_timing) { CUDA_TRY(cudaEventRecord(s->ev_k0, s->st)); }
-    if (s->cfg.variant == PCS_VARIANT_SET || s->ell == 1) {
+    if (s->cfg.variant == PCS_VARIANT_SET || s->ell == 1 || s->ell > kMaxTemplLevel) {
         launch_row_work(A, pass, s->cfg.variant, 0, s->p, s->dPrefix, s->st);
         unsigned long long total = 0;
         CUDA_TRY(cudaMemcpyAsync(&total, s->dPrefix + s->p, sizeof(total), cudaMemcpyDeviceToHost, s->st));
@@ -488,6 +503,10 @@ pcs_status pcs_session_level_pass(pcs_session* s, int32_t pass) {
         if (u1 > u0) {
             if (s->ell == 1) {
                 launch_level1(A, pass, s->dPrefix, u0, u1, s->st);
+            } else if (s->ell > kMaxTemplLevel) {
+                CUDA_TRY(cudaMemsetAsync(&s->dCnt->units[pass], 0, sizeof(unsigned long long), s->st));
+                if (launch_level_set_rt(A, pass, s->dPrefix, u0, u1, s->num_sms, s->dScratch, s->st))
+                    return fail(PCS_EUNSUPPORTED, "level not supported by the generic set kernel");
             } else {
                 if (launch_level_set(A, pass, s->dPrefix, u0, u1, s->num_sms, s->st))
                     return fail(PCS_EUNSUPPORTED, "level not supported by the set kernel");
@@ -502,6 +521,27 @@ pcs_status pcs_session_level_pass(pcs_session* s, int32_t pass) {
     CUDA_TRY(cudaGetLastError());
     CUDA_TRY(cudaEventRecord(s->ev_k1, s->st));
     s->kernel_timing = true;
+    return PCS_OK;
+}
+
+pcs_status pcs_session_snapshot(pcs_session* s, int32_t* offsets, int32_t* indices) {
+    if (!s || !s->in_level || s->ell < 1) return fail(PCS_EINVAL, "no level >= 1 in progress");
+    CUDA_TRY(cudaSetDevice(s->device));
+    CUDA_TRY(cudaMemcpyAsync(offsets, s->dOff, sizeof(int32_t) * (size_t)(s->p + 1), cudaMemcpyDeviceToHost, s->st));
+    if (indices && s->info.e_dir > 0)
+        CUDA_TRY(cudaMemcpyAsync(indices, s->dNbr, sizeof(int32_t) * (size_t)s->info.e_dir, cudaMemcpyDeviceToHost,
+                                 s->st));
+    CUDA_TRY(cudaStreamSynchronize(s->st));
+    return PCS_OK;
+}
+
+unsigned long long pcs_kernel_launches(void) { return g_kernel_launches; }
+
+pcs_status pcs_session_set_shard(pcs_session* s, int32_t shard_index, int32_t shard_count) {
+    if (!s || shard_count < 1 || shard_index < 0 || shard_index >= shard_count)
+        return fail(PCS_EINVAL, "bad shard index/count");
+    s->cfg.shard_index = shard_index;
+    s->cfg.shard_count = shard_count;
     return PCS_OK;
 }
 
@@ -618,7 +658,7 @@ pcs_status pcs_run_pc_stable_device(const double* d_c, int64_t ldc, int32_t p, i
 }
 
 static pcs_status correlation_device(cudaStream_t stream, const double* x, int m, int p, double* dC, long long ldc,
-                                     int32_t* zero_var_col) {
+                                     int32_t* zero_var_col, bool x_on_device = false) {
     if (m < 4) return fail(PCS_EINVAL, "DataMatrix: need at least 4 samples, got " + std::to_string(m));
     if (p < 2) return fail(PCS_EINVAL, "DataMatrix: need at least 2 variables, got " + std::to_string(p));
     const int ldk = (m + 31) / 32 * 32;
@@ -627,16 +667,17 @@ static pcs_status correlation_device(cudaStream_t stream, const double* x, int m
     int* dErr = nullptr;
     pcs_status st = PCS_OK;
     auto cleanup = [&]() { cudaFree(dX); cudaFree(dXc); cudaFree(dG); cudaFree(dMean); cudaFree(dErr); };
-    if (cudaMalloc(&dX, sizeof(double) * (size_t)m * p) || cudaMalloc(&dXc, sizeof(double) * (size_t)p * ldk) ||
+    if ((!x_on_device && cudaMalloc(&dX, sizeof(double) * (size_t)m * p)) ||
+        cudaMalloc(&dXc, sizeof(double) * (size_t)p * ldk) ||
         cudaMalloc(&dG, sizeof(double) * (size_t)p * ldg) || cudaMalloc(&dMean, sizeof(double) * (size_t)p) ||
         cudaMalloc(&dErr, sizeof(int) * 2)) {
         cleanup();
         return fail(PCS_ENOMEM, "cudaMalloc failed in compute_correlation");
     }
     int init[2] = {0, INT32_MAX};
-    cudaMemcpyAsync(dX, x, sizeof(double) * (size_t)m * p, cudaMemcpyHostToDevice, stream);
+    if (!x_on_device) cudaMemcpyAsync(dX, x, sizeof(double) * (size_t)m * p, cudaMemcpyHostToDevice, stream);
     cudaMemcpyAsync(dErr, init, sizeof(init), cudaMemcpyHostToDevice, stream);
-    launch_correlation(dX, m, p, dXc, dG, ldg, dMean, dC, ldc, dErr, stream);
+    launch_correlation(x_on_device ? x : dX, m, p, dXc, dG, ldg, dMean, dC, ldc, dErr, stream);
     int err[2];
     cudaMemcpyAsync(err, dErr, sizeof(err), cudaMemcpyDeviceToHost, stream);
     cudaError_t ce = cudaStreamSynchronize(stream);
@@ -670,8 +711,8 @@ pcs_status pcs_correlation(const double* x, int32_t m, int32_t p, double* c_out,
     return st;
 }
 
-pcs_status pcs_run_pc_stable_data(const double* x, int32_t m, int32_t p, const pcs_config* cfg, pcs_result** out,
-                                  int32_t* zero_var_col) {
+static pcs_status run_data(const double* x, bool on_device, int32_t m, int32_t p, const pcs_config* cfg,
+                           pcs_result** out, int32_t* zero_var_col) {
     *out = nullptr;
     pcs_session* s = nullptr;
     pcs_status st = session_new(p, m, cfg, &s);
@@ -682,10 +723,27 @@ pcs_status pcs_run_pc_stable_data(const double* x, int32_t m, int32_t p, const p
         return fail(PCS_ENOMEM, "cudaMalloc failed");
     }
     cudaEventRecord(s->ev_begin, s->st);
-    st = correlation_device(s->st, x, m, p, s->dC, s->ldc, zero_var_col);
+    st = correlation_device(s->st, x, m, p, s->dC, s->ldc, zero_var_col, on_device);
     if (!st) st = run_session(s, out);
     free_session(s);
     return st;
+}
+
+pcs_status pcs_correlation_device(const double* d_x, int32_t m, int32_t p, double* d_c, int64_t ldc, uint64_t stream,
+                                  int32_t* zero_var_col) {
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) return fail(PCS_ECUDA, "no CUDA device available");
+    return correlation_device(reinterpret_cast<cudaStream_t>(stream), d_x, m, p, d_c, ldc, zero_var_col, true);
+}
+
+pcs_status pcs_run_pc_stable_data(const double* x, int32_t m, int32_t p, const pcs_config* cfg, pcs_result** out,
+                                  int32_t* zero_var_col) {
+    return run_data(x, false, m, p, cfg, out, zero_var_col);
+}
+
+pcs_status pcs_run_pc_stable_data_device(const double* d_x, int32_t m, int32_t p, const pcs_config* cfg,
+                                         pcs_result** out, int32_t* zero_var_col) {
+    return run_data(d_x, true, m, p, cfg, out, zero_var_col);
 }
 
 int32_t pcs_result_p(const pcs_result* r) { return r->p; }
@@ -714,6 +772,14 @@ void pcs_result_edge_list(const pcs_result* r, int32_t* out) {
         for (int j = i + 1; j < r->p; ++j)
             if (res_at(r, i, j)) { out[2 * k] = i; out[2 * k + 1] = j; ++k; }
 }
+int64_t pcs_result_record_ints(const pcs_result* r) { return (int64_t)r->recs.size(); }
+void pcs_result_records(const pcs_result* r, int32_t* out) {
+    if (!r->recs.empty()) std::memcpy(out, r->recs.data(), sizeof(int32_t) * r->recs.size());
+}
+void pcs_result_bitmask(const pcs_result* r, uint32_t* out) {
+    if (!r->adj.empty()) std::memcpy(out, r->adj.data(), sizeof(uint32_t) * r->adj.size());
+}
+
 int64_t pcs_result_member_total(const pcs_result* r) {
     int64_t tot = 0;
     for (size_t k = 0; k < r->recs.size();) {
@@ -755,7 +821,7 @@ void pcs_result_free(pcs_result* r) { delete r; }
 pcs_status pcs_ci_test_batch(const double* c, int32_t p, int32_t ell, int64_t n, const int32_t* ij,
                              const int32_t* sets, double tau, uint8_t* independent, double* z, double* rho,
                              uint8_t* degenerate) {
-    if (ell < 0 || ell > kMaxTemplLevel) return fail(PCS_EUNSUPPORTED, "ci_test_batch: ell out of range");
+    if (ell < 0 || ell > kMaxRtLevel) return fail(PCS_EUNSUPPORTED, "ci_test_batch: ell out of range");
     pcs_config cfg;
     pcs_config_default(&cfg);
     pcs_session* s = nullptr;
@@ -776,7 +842,13 @@ pcs_status pcs_ci_test_batch(const double* c, int32_t p, int32_t ell, int64_t n,
     cudaMemcpy(dIJ, ij, sizeof(int32_t) * 2 * n, cudaMemcpyHostToDevice);
     if (ell > 0) cudaMemcpy(dS, sets, sizeof(int32_t) * n * ell, cudaMemcpyHostToDevice);
     cudaMemset(dErr, 0, sizeof(int));
-    launch_ci_batch(s->dC, s->ldc, p, ell, n, dIJ, dS, tau, dInd, dZ, dR, dDeg, dErr, s->st);
+    double* dW = nullptr;
+    if (ell > kMaxTemplLevel) {
+        cudaMalloc(&dW, sizeof(double) * nn * (7ull * ell * ell + 4ull * ell + 1));
+        launch_ci_batch_rt(s->dC, s->ldc, ell, n, dIJ, dS, tau, dInd, dZ, dR, dDeg, dErr, dW, s->st);
+    } else {
+        launch_ci_batch(s->dC, s->ldc, p, ell, n, dIJ, dS, tau, dInd, dZ, dR, dDeg, dErr, s->st);
+    }
     cudaStreamSynchronize(s->st);
     int err = 0;
     cudaMemcpy(independent, dInd, n, cudaMemcpyDeviceToHost);
@@ -786,6 +858,7 @@ pcs_status pcs_ci_test_batch(const double* c, int32_t p, int32_t ell, int64_t n,
     cudaMemcpy(&err, dErr, sizeof(int), cudaMemcpyDeviceToHost);
     cudaError_t ce = cudaGetLastError();
     cudaFree(dIJ); cudaFree(dS); cudaFree(dInd); cudaFree(dDeg); cudaFree(dZ); cudaFree(dR); cudaFree(dErr);
+    cudaFree(dW);
     free_session(s);
     if (ce != cudaSuccess) return fail(PCS_ECUDA, cudaGetErrorString(ce));
     if (err) return fail(PCS_ENAN, "fisher_z: rho must lie in (-1, 1)");
@@ -793,7 +866,7 @@ pcs_status pcs_ci_test_batch(const double* c, int32_t p, int32_t ell, int64_t n,
 }
 
 pcs_status pcs_pseudo_inverse_batch(const double* a, int32_t ell, int64_t n, double* out) {
-    if (ell < 1 || ell > kMaxTemplLevel) return fail(PCS_EUNSUPPORTED, "pseudo_inverse_batch: ell out of range");
+    if (ell < 1 || ell > kMaxRtLevel) return fail(PCS_EUNSUPPORTED, "pseudo_inverse_batch: ell out of range");
     int ndev = 0;
     if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) return fail(PCS_ECUDA, "no CUDA device available");
     for (int64_t q = 0; q < n * ell * ell; ++q)
@@ -803,10 +876,17 @@ pcs_status pcs_pseudo_inverse_batch(const double* a, int32_t ell, int64_t n, dou
     CUDA_TRY(cudaMalloc(&dA, bytes));
     CUDA_TRY(cudaMalloc(&dO, bytes));
     cudaMemcpy(dA, a, sizeof(double) * n * ell * ell, cudaMemcpyHostToDevice);
-    launch_pinv_batch(dA, ell, n, dO, 0);
+    double* dW = nullptr;
+    if (ell > kMaxTemplLevel) {
+        CUDA_TRY(cudaMalloc(&dW, sizeof(double) * 5ull * ell * ell * (size_t)std::max<int64_t>(n, 1)));
+        launch_pinv_batch_rt(dA, ell, n, dO, dW, 0);
+    } else {
+        launch_pinv_batch(dA, ell, n, dO, 0);
+    }
     cudaError_t ce = cudaMemcpy(out, dO, sizeof(double) * n * ell * ell, cudaMemcpyDeviceToHost);
     cudaFree(dA);
     cudaFree(dO);
+    cudaFree(dW);
     if (ce != cudaSuccess) return fail(PCS_ECUDA, cudaGetErrorString(ce));
     return PCS_OK;
 }

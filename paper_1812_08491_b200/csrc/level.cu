@@ -21,6 +21,8 @@
 
 namespace pcs {
 
+unsigned long long g_kernel_launches = 0;
+
 namespace {
 
 __device__ __forceinline__ unsigned long long warp_sum(unsigned long long v) {
@@ -100,6 +102,7 @@ void launch_level0(const double* C, long long ldc, int p, int W, uint32_t* adj, 
     const long long items = (long long)p * W;
     long long blocks = (items * 32 + 255) / 256;
     if (blocks > 148 * 16) blocks = 148 * 16;
+    ++g_kernel_launches;
     level0_kernel<<<(int)blocks, 256, 0, s>>>(C, ldc, p, W, adj, th, cnt);
 }
 
@@ -126,6 +129,7 @@ __global__ void snapshot_degree_kernel(const uint32_t* __restrict__ adj, int p, 
 }
 
 void launch_snapshot_degrees(const uint32_t* adj, int p, int W, int32_t* deg, int32_t* lowcnt, cudaStream_t s) {
+    ++g_kernel_launches;
     snapshot_degree_kernel<<<(p * 32 + 255) / 256, 256, 0, s>>>(adj, p, W, deg, lowcnt);
 }
 
@@ -172,6 +176,7 @@ __global__ void snapshot_scan_kernel(const int32_t* __restrict__ deg, const int3
 
 void launch_snapshot_scan(const int32_t* deg, const int32_t* lowcnt, int p, int32_t* off, int32_t* upoff,
                           SnapInfo* info, cudaStream_t s) {
+    ++g_kernel_launches;
     snapshot_scan_kernel<<<1, 1024, 0, s>>>(deg, lowcnt, p, off, upoff, info);
 }
 
@@ -202,6 +207,7 @@ __global__ void snapshot_fill_kernel(const uint32_t* __restrict__ adj, int p, in
 }
 
 void launch_snapshot_fill(const uint32_t* adj, int p, int W, const int32_t* off, int32_t* nbr, cudaStream_t s) {
+    ++g_kernel_launches;
     snapshot_fill_kernel<<<(p * 32 + 255) / 256, 256, 0, s>>>(adj, p, W, off, nbr);
 }
 
@@ -233,6 +239,7 @@ __global__ void edge_index_kernel(LevelArgs A, int32_t* eid, int32_t* eu_a, int3
 
 void launch_edge_index(const LevelArgs& A, int32_t* eid, int32_t* eu_a, int32_t* eu_qa, int32_t* eu_qb,
                        cudaStream_t s) {
+    ++g_kernel_launches;
     edge_index_kernel<<<(A.p * 32 + 255) / 256, 256, 0, s>>>(A, eid, eu_a, eu_qa, eu_qb);
 }
 
@@ -244,6 +251,7 @@ void launch_fill_keys(unsigned long long* keys, long long n, cudaStream_t s) {
     if (n <= 0) return;
     long long blocks = (n + 255) / 256;
     if (blocks > 148 * 8) blocks = 148 * 8;
+    ++g_kernel_launches;
     fill_keys_kernel<<<(int)blocks, 256, 0, s>>>(keys, n);
 }
 
@@ -293,7 +301,9 @@ __global__ void scan_u64_kernel(unsigned long long* a, int n) {
 
 void launch_row_work(const LevelArgs& A, int pass, int variant, int row_begin, int row_end,
                      unsigned long long* prefix, cudaStream_t s) {
+    ++g_kernel_launches;
     row_work_kernel<<<(A.p + 255) / 256, 256, 0, s>>>(A, pass, variant, row_begin, row_end, prefix);
+    ++g_kernel_launches;
     scan_u64_kernel<<<1, 1024, 0, s>>>(prefix, A.p);
 }
 
@@ -377,6 +387,7 @@ void launch_level1(const LevelArgs& A, int pass, const unsigned long long* prefi
     const unsigned long long kMaxGrid = 1ull << 30;
     for (unsigned long long base = u_begin; base < u_end; base += kMaxGrid) {
         const unsigned long long n = u_end - base < kMaxGrid ? u_end - base : kMaxGrid;
+        ++g_kernel_launches;
         level1_kernel<<<(unsigned)n, kL1Threads, 0, s>>>(A, pass, prefix, base);
     }
 }
@@ -510,6 +521,7 @@ static int launch_set_L(const LevelArgs& A, int pass, const unsigned long long* 
     int per_sm = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, level_set_kernel<L>, kSetWarps * 32, smem);
     if (per_sm < 1) per_sm = 1;
+    ++g_kernel_launches;
     level_set_kernel<L><<<num_sms * per_sm, kSetWarps * 32, smem, s>>>(A, pass, prefix, u_begin, u_end);
     return 0;
 }
@@ -603,6 +615,7 @@ static int launch_edge_L(const LevelArgs& A, int pass, long long e_begin, long l
     int per_sm = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, level_edge_kernel<L>, 128, 0);
     if (per_sm < 1) per_sm = 1;
+    ++g_kernel_launches;
     level_edge_kernel<L><<<num_sms * per_sm, 128, 0, s>>>(A, pass, e_begin, e_end);
     return 0;
 }
@@ -619,6 +632,192 @@ int launch_level_edge(const LevelArgs& A, int pass, long long e_begin, long long
         case 8: return launch_edge_L<8>(A, pass, e_begin, e_end, num_sms, s);
         default: return -1;
     }
+}
+
+// =========================================================== ell > 8 (generic)
+// cuPC-S with runtime ell: lane-parallel pseudo-inverses as in level_set_kernel,
+// all per-set matrices in a per-lane slice of global scratch (L1/L2 resident).
+// Serves both device variants above kMaxTemplLevel (results are identical).
+__host__ __device__ inline long long rt_lane_doubles(int n) { return 7ll * n * n + 4ll * n + 1; }
+
+__global__ void __launch_bounds__(128) level_set_rt_kernel(LevelArgs A, int pass, const unsigned long long* prefix,
+                                                           unsigned long long u_begin, unsigned long long u_end,
+                                                           double* scratch, int* iscratch) {
+    const int n = A.ell;
+    const int lane = threadIdx.x & 31;
+    const long long gwarp = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const long long SD = rt_lane_doubles(n);
+    double* wbase = scratch + gwarp * 32 * SD;
+    int* ibase = iscratch + gwarp * 32 * 2 * n;
+    // per-lane regions
+    double* m2 = wbase + lane * SD;
+    double* minv = m2 + n * n;
+    double* ws = minv + n * n;
+    double* ciS = ws + 5 * n * n;
+    double* p0 = ciS + n;
+    double* h00p = p0 + n;
+    double* P1 = h00p + 1;
+    double* cjS = P1 + n;
+    int* pos = ibase + lane * 2 * n;
+    int* mem = pos + n;
+    const double* __restrict__ C = A.C;
+    const long long ldc = A.ldc;
+    const unsigned long long dirbits = (unsigned long long)pass << kDirShift;
+    unsigned long long tests = 0, pinvs = 0;
+    int nan = 0;
+    unsigned long long* cursor = &A.cnt->units[pass];
+    for (;;) {
+        unsigned long long u = 0;
+        if (lane == 0) u = u_begin + atomicAdd(cursor, 1ull);
+        u = __shfl_sync(0xffffffffu, u, 0);
+        if (u >= u_end) break;
+        const int i = find_row(prefix, A.p, u);
+        const unsigned long long t0 = (u - prefix[i]) * kSetBand;
+        const int oi = A.off[i], w = A.off[i + 1] - oi, lc = A.lowcnt[i];
+        const int qbeg = pass == 0 ? lc : 0, qend = pass == 0 ? w : lc;
+        const unsigned long long K0 = dirbits | t0;
+        bool open = false;
+        for (int q = qbeg + lane; q < qend; q += 32) open |= A.keys[A.eid[oi + q]] > K0;
+        if (!__any_sync(0xffffffffu, open)) continue;
+        const unsigned long long total = A.binom(w, n);
+        const unsigned long long t = t0 + lane;
+        const bool valid = t < total;
+        if (valid) {
+            unrank_rt(A.binom, w, n, t, pos);
+            for (int a = 0; a < n; ++a) {
+                mem[a] = A.nbr[oi + pos[a]];
+                ciS[a] = __ldg(C + (size_t)i * ldc + mem[a]);
+            }
+            for (int a = 0; a < n; ++a)
+                for (int b = 0; b < n; ++b) m2[a * n + b] = __ldg(C + (size_t)mem[a] * ldc + mem[b]);
+            pinv_rt(m2, n, minv, ws);
+            double h00;
+            p0_terms_rt(minv, ciS, n, p0, h00);
+            *h00p = h00;
+        }
+        const int nvalid = __popc(__ballot_sync(0xffffffffu, valid));
+        if (lane == 0) pinvs += nvalid;
+        __syncwarp();
+        __threadfence_block();
+        for (int qc = qbeg; qc < qend; qc += 32) {
+            const int q = qc + lane;
+            bool live = q < qend;
+            int j = 0, e = 0;
+            unsigned long long key = 0;
+            double cij = 0.0;
+            if (live) {
+                j = A.nbr[oi + q];
+                e = A.eid[oi + q];
+                key = A.keys[e];
+                live = key > K0;
+                if (live) cij = __ldg(C + (size_t)i * ldc + j);
+            }
+            if (!__any_sync(0xffffffffu, live)) continue;
+            for (int sg = 0; sg < nvalid; ++sg) {
+                if (!live) break;
+                const double* S = wbase + sg * SD;
+                const int* Spos = ibase + sg * 2 * n;
+                const unsigned long long Kc = dirbits | (t0 + sg);
+                if (key <= Kc) { live = false; break; }
+                bool member = false;
+                for (int a = 0; a < n; ++a) member |= Spos[a] == q;
+                if (member) continue;
+                for (int a = 0; a < n; ++a) cjS[a] = __ldg(C + (size_t)Spos[n + a] * ldc + j);
+                double h01, denom;
+                const double* Sminv = S + n * n;
+                const double* SciS = S + 7 * n * n;
+                h_terms_rt(Sminv, SciS, SciS + n, SciS[2 * n], cjS, n, cij, P1, h01, denom);
+                const int d = decide_fast(h01, denom, A.th);
+                ++tests;
+                if (d != kDependent) {
+                    live = false;
+                    if (d == kNanError) nan = 1;
+                    else atomicMin(A.keys + e, Kc);
+                }
+            }
+        }
+        __syncwarp();
+    }
+    add_counter(&A.cnt->gpu_tests, tests);
+    if (lane == 0 && pinvs) atomicAdd(&A.cnt->gpu_pinv, pinvs);
+    if (nan) atomicOr(&A.cnt->err_nan, 1);
+}
+
+long long level_rt_scratch_bytes(int ell, int num_sms, int* blocks_out) {
+    const long long per_lane = rt_lane_doubles(ell) * 8 + 2ll * ell * 4;
+    long long blocks = (long long)num_sms * 8;
+    const long long budget = 2ll << 30;
+    while (blocks > num_sms && blocks * 128 * per_lane > budget) blocks -= num_sms;
+    if (blocks_out) *blocks_out = (int)blocks;
+    return blocks * 128 * per_lane;
+}
+
+int launch_level_set_rt(const LevelArgs& A, int pass, const unsigned long long* prefix, unsigned long long u_begin,
+                        unsigned long long u_end, int num_sms, void* scratch, cudaStream_t s) {
+    if (A.ell > kMaxRtLevel) return -1;
+    int blocks = 0;
+    level_rt_scratch_bytes(A.ell, num_sms, &blocks);
+    const long long lanes = (long long)blocks * 128;
+    double* sd = static_cast<double*>(scratch);
+    int* si = reinterpret_cast<int*>(sd + lanes * rt_lane_doubles(A.ell));
+    ++g_kernel_launches;
+    level_set_rt_kernel<<<blocks, 128, 0, s>>>(A, pass, prefix, u_begin, u_end, sd, si);
+    return 0;
+}
+
+// generic-ell parity helpers (one test / block per thread, global scratch)
+__global__ void ci_batch_rt_kernel(const double* C, long long ldc, int n, long long cnt, const int32_t* ij,
+                                   const int32_t* sets, double tau, uint8_t* indep, double* zout, double* rhoout,
+                                   uint8_t* degen, int* err, double* scratch) {
+    const long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= cnt) return;
+    double* m2 = scratch + k * rt_lane_doubles(n);
+    double* minv = m2 + n * n;
+    double* ws = minv + n * n;
+    double* ciS = ws + 5 * n * n;
+    double* p0 = ciS + n;
+    double* P1 = p0 + n + 1;
+    double* cjS = P1 + n;
+    const int i = ij[2 * k], j = ij[2 * k + 1];
+    const int32_t* mem = sets + k * n;
+    for (int a = 0; a < n; ++a) {
+        ciS[a] = C[(size_t)i * ldc + mem[a]];
+        cjS[a] = C[(size_t)j * ldc + mem[a]];
+        for (int b = 0; b < n; ++b) m2[a * n + b] = C[(size_t)mem[a] * ldc + mem[b]];
+    }
+    pinv_rt(m2, n, minv, ws);
+    double h00, h01, denom, z, rho;
+    p0_terms_rt(minv, ciS, n, p0, h00);
+    h_terms_rt(minv, ciS, p0, h00, cjS, n, C[(size_t)i * ldc + j], P1, h01, denom);
+    const int d = decide_exact(h01, denom, tau, &z, &rho);
+    if (d == kNanError) atomicOr(err, 1);
+    indep[k] = d == kIndependent;
+    zout[k] = z;
+    rhoout[k] = rho;
+    degen[k] = !(denom > 0.0);
+}
+
+__global__ void pinv_batch_rt_kernel(const double* a, int n, long long cnt, double* out, double* scratch) {
+    const long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= cnt) return;
+    pinv_rt(a + k * n * n, n, out + k * n * n, scratch + k * 5ll * n * n);
+}
+
+int launch_ci_batch_rt(const double* C, long long ldc, int ell, long long n, const int32_t* ij, const int32_t* sets,
+                       double tau, uint8_t* indep, double* z, double* rho, uint8_t* degen, int* err, double* scratch,
+                       cudaStream_t s) {
+    if (n <= 0) return 0;
+    ++g_kernel_launches;
+    ci_batch_rt_kernel<<<(unsigned)((n + 127) / 128), 128, 0, s>>>(C, ldc, ell, n, ij, sets, tau, indep, z, rho,
+                                                                   degen, err, scratch);
+    return 0;
+}
+
+int launch_pinv_batch_rt(const double* a, int ell, long long n, double* out, double* scratch, cudaStream_t s) {
+    if (n <= 0) return 0;
+    ++g_kernel_launches;
+    pinv_batch_rt_kernel<<<(unsigned)((n + 127) / 128), 128, 0, s>>>(a, ell, n, out, scratch);
+    return 0;
 }
 
 // =========================================================== commit
@@ -666,6 +865,7 @@ __global__ void commit_kernel(LevelArgs A, uint32_t* adj, int W, long long e_und
 
 void launch_commit(const LevelArgs& A, uint32_t* adj, int W, long long e_und, int32_t* rec, cudaStream_t s) {
     if (e_und <= 0) return;
+    ++g_kernel_launches;
     commit_kernel<<<(unsigned)((e_und + 255) / 256), 256, 0, s>>>(A, adj, W, e_und, rec);
 }
 

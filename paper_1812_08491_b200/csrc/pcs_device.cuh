@@ -317,4 +317,155 @@ __device__ __forceinline__ void p0_terms(const double (&Minv)[L * L], const doub
     h00 = 1.0 - d00;
 }
 
+// ------------------------------------------------------- runtime-ell variants
+// Same operation order as pinv<L> / p0_terms<L> / h_terms<L>; matrices live in
+// caller-provided (global) scratch.  Used for ell > kMaxTemplLevel.
+constexpr int kMaxRtLevel = 64;
+
+// ws: 5*n*n doubles
+__device__ inline void pinv_rt(const double* a, int n, double* out, double* ws) {
+    double* G = ws;
+    double* Lm = ws + n * n;
+    double* K = ws + 2 * n * n;
+    double* R = ws + 3 * n * n;
+    double* LR = ws + 4 * n * n;
+    double* T = G;  // G is dead once the Cholesky is done
+    bool kept[kMaxRtLevel];
+    for (int i = 0; i < n; ++i)
+        for (int j = 0; j < n; ++j) {
+            double s = a[0 * n + i] * a[0 * n + j];
+            for (int q = 1; q < n; ++q) s = s + a[q * n + i] * a[q * n + j];
+            G[i * n + j] = s;
+        }
+    double mx = G[0];
+    for (int i = 1; i < n; ++i) mx = G[i * n + i] > mx ? G[i * n + i] : mx;
+    const double tol = 1e-10 * mx;
+    for (int q = 0; q < n * n; ++q) out[q] = 0.0;
+    if (!(tol > 0.0)) return;
+    for (int k = 0; k < n; ++k) {
+        for (int i = 0; i < n; ++i) {
+            if (i < k) { Lm[i * n + k] = 0.0; continue; }
+            double v = G[i * n + k];
+            bool have = false;
+            double s = 0.0;
+            for (int c = 0; c < k; ++c)
+                if (kept[c]) { const double pr = Lm[i * n + c] * Lm[k * n + c]; s = have ? s + pr : pr; have = true; }
+            if (have) v = v - s;
+            Lm[i * n + k] = v;
+        }
+        const double pivot = Lm[k * n + k];
+        kept[k] = pivot > tol;
+        if (kept[k]) {
+            const double root = sqrt(pivot);
+            Lm[k * n + k] = root;
+            for (int i = k + 1; i < n; ++i) Lm[i * n + k] = Lm[i * n + k] / root;
+        }
+    }
+    bool any = false;
+    for (int k = 0; k < n; ++k) any |= kept[k];
+    if (!any) return;
+    for (int x = 0; x < n; ++x)
+        for (int y = 0; y < n; ++y) {
+            if (!kept[x] || !kept[y]) continue;
+            double s = Lm[0 * n + x] * Lm[0 * n + y];
+            for (int i = 1; i < n; ++i) s = s + Lm[i * n + x] * Lm[i * n + y];
+            K[x * n + y] = s;
+        }
+    bool failed = false;
+    for (int k = 0; k < n; ++k) {
+        if (!kept[k] || failed) continue;
+        double x = K[k * n + k];
+        {
+            bool have = false;
+            double s = 0.0;
+            for (int c = 0; c < k; ++c)
+                if (kept[c]) { const double pr = K[k * n + c] * K[k * n + c]; s = have ? s + pr : pr; have = true; }
+            if (have) x = x - s;
+        }
+        if (x <= 0.0) { failed = true; continue; }
+        x = sqrt(x);
+        K[k * n + k] = x;
+        for (int i = k + 1; i < n; ++i) {
+            if (!kept[i]) continue;
+            bool have = false;
+            double s = 0.0;
+            for (int c = 0; c < k; ++c)
+                if (kept[c]) { const double pr = K[i * n + c] * K[k * n + c]; s = have ? s + pr : pr; have = true; }
+            if (have) K[i * n + k] = K[i * n + k] - s;
+        }
+        for (int i = k + 1; i < n; ++i)
+            if (kept[i]) K[i * n + k] = K[i * n + k] / x;
+    }
+    for (int col = 0; col < n; ++col) {
+        if (!kept[col]) continue;
+        for (int k = 0; k < n; ++k) {
+            if (!kept[k]) continue;
+            double y = (k == col) ? 1.0 : 0.0;
+            for (int c = 0; c < k; ++c)
+                if (kept[c]) y = y - K[k * n + c] * R[c * n + col];
+            R[k * n + col] = y / K[k * n + k];
+        }
+        for (int k = n - 1; k >= 0; --k) {
+            if (!kept[k]) continue;
+            double y = R[k * n + col];
+            for (int c = k + 1; c < n; ++c)
+                if (kept[c]) y = y - K[c * n + k] * R[c * n + col];
+            R[k * n + col] = y / K[k * n + k];
+        }
+    }
+    for (int i = 0; i < n; ++i)
+        for (int y = 0; y < n; ++y) {
+            if (!kept[y]) continue;
+            bool have = false;
+            double s = 0.0;
+            for (int x = 0; x < n; ++x)
+                if (kept[x]) { const double pr = Lm[i * n + x] * R[x * n + y]; s = have ? s + pr : pr; have = true; }
+            LR[i * n + y] = s;
+        }
+    for (int i = 0; i < n; ++i)
+        for (int j = 0; j < n; ++j) {
+            bool have = false;
+            double s = 0.0;
+            for (int y = 0; y < n; ++y)
+                if (kept[y]) { const double pr = LR[i * n + y] * LR[j * n + y]; s = have ? s + pr : pr; have = true; }
+            T[i * n + j] = s;
+        }
+    for (int i = 0; i < n; ++i)
+        for (int j = 0; j < n; ++j) {
+            double s = T[i * n + 0] * a[j * n + 0];
+            for (int q = 1; q < n; ++q) s = s + T[i * n + q] * a[j * n + q];
+            out[i * n + j] = s;
+        }
+}
+
+__device__ inline void p0_terms_rt(const double* Minv, const double* ciS, int n, double* P0, double& h00) {
+    for (int col = 0; col < n; ++col) {
+        double s = ciS[0] * Minv[0 * n + col];
+        for (int k = 1; k < n; ++k) s = s + ciS[k] * Minv[k * n + col];
+        P0[col] = s;
+    }
+    double d00 = P0[0] * ciS[0];
+    for (int k = 1; k < n; ++k) d00 = d00 + P0[k] * ciS[k];
+    h00 = 1.0 - d00;
+}
+
+// P1 scratch of n doubles
+__device__ inline void h_terms_rt(const double* Minv, const double* ciS, const double* P0, double h00,
+                                  const double* cjS, int n, double cij, double* P1, double& h01, double& denom) {
+    for (int col = 0; col < n; ++col) {
+        double s = cjS[0] * Minv[0 * n + col];
+        for (int k = 1; k < n; ++k) s = s + cjS[k] * Minv[k * n + col];
+        P1[col] = s;
+    }
+    double d11 = P1[0] * cjS[0], d01 = P0[0] * cjS[0], d10 = P1[0] * ciS[0];
+    for (int k = 1; k < n; ++k) {
+        d11 = d11 + P1[k] * cjS[k];
+        d01 = d01 + P0[k] * cjS[k];
+        d10 = d10 + P1[k] * ciS[k];
+    }
+    const double h11 = 1.0 - d11;
+    h01 = cij - 0.5 * (d01 + d10);
+    denom = h00 * h11;
+}
+
 }  // namespace pcs

@@ -8,6 +8,9 @@
 
 namespace pcs {
 
+// number of kernels this library has launched (diagnostics: bench.py's gpu_launches)
+extern unsigned long long g_kernel_launches;
+
 constexpr int kMaxTemplLevel = 8;  // ell handled by register-resident templates
 
 // Device-side counters of one level (zeroed by the host before each level).
@@ -75,6 +78,14 @@ int launch_level_set(const LevelArgs& A, int pass, const unsigned long long* pre
                      unsigned long long u_end, int num_sms, cudaStream_t s);
 int launch_level_edge(const LevelArgs& A, int pass, long long e_begin, long long e_end, int num_sms,
                       cudaStream_t s);
+// generic ell (> kMaxTemplLevel, <= kMaxRtLevel): cuPC-S with global per-lane scratch
+long long level_rt_scratch_bytes(int ell, int num_sms, int* blocks_out);
+int launch_level_set_rt(const LevelArgs& A, int pass, const unsigned long long* prefix, unsigned long long u_begin,
+                        unsigned long long u_end, int num_sms, void* scratch, cudaStream_t s);
+int launch_ci_batch_rt(const double* C, long long ldc, int ell, long long n, const int32_t* ij, const int32_t* sets,
+                       double tau, uint8_t* indep, double* z, double* rho, uint8_t* degen, int* err, double* scratch,
+                       cudaStream_t s);
+int launch_pinv_batch_rt(const double* a, int ell, long long n, double* out, double* scratch, cudaStream_t s);
 void launch_commit(const LevelArgs& A, uint32_t* adj, int W, long long e_und, int32_t* rec, cudaStream_t s);
 // parity helpers (stats::ci_test / pseudo_inverse on the device, one test per thread)
 int launch_ci_batch(const double* C, long long ldc, int p, int ell, long long n, const int32_t* ij,

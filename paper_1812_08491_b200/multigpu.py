@@ -1,0 +1,72 @@
+"""Multi-GPU PC-stable: one process per GPU, per-level sharding, one MIN all-reduce
+of the level's key array after each pass.
+
+Every rank holds the replicated correlation matrix and builds the identical
+snapshot; pass p of a level is split into contiguous work-unit ranges (rank r
+of N takes units [r*U/N, (r+1)*U/N)).  A key is (dir << 62 | rank of the first
+separating set) per undirected edge, so MIN over ranks is exactly the serial
+strategy's choice and subsumes the "bitwise AND of the live mask" merge (NCCL
+has no AND).  The commit that follows is replicated and deterministic.
+
+The level loop is written against a small protocol (level_begin / level_pass /
+keys / level_end / finish) so the same orchestration is exercised on CPU with
+gloo and an oracle-backed session in tests/test_multigpu_gloo.py.
+"""
+from __future__ import annotations
+
+from typing import Callable, Optional
+
+
+def level_loop(session, allreduce_min: Optional[Callable[[object, int], None]], world: int):
+    """Runs the PC-stable level loop on `session`; `allreduce_min(ptr_or_array, n)` merges keys."""
+    while True:
+        running, ell, nkeys = session.level_begin()
+        if not running:
+            break
+        for pass_index in (0, 1):
+            session.level_pass(pass_index)
+            if world > 1 and nkeys > 0 and allreduce_min is not None:
+                keys, n = session.keys()
+                allreduce_min(keys, n)
+        session.level_end()
+    return session
+
+
+class _CudaArray:
+    """__cuda_array_interface__ view of library-owned device memory (int64 keys)."""
+
+    def __init__(self, ptr: int, n: int):
+        self.__cuda_array_interface__ = {"shape": (n,), "typestr": "<i8", "data": (ptr, False), "version": 3,
+                                         "strides": None}
+
+
+def torch_allreduce_min(group=None):
+    """MIN all-reduce of a device key array through torch.distributed (NCCL over NVLink)."""
+    import torch
+    import torch.distributed as dist
+
+    def _reduce(ptr: int, n: int):
+        t = torch.as_tensor(_CudaArray(ptr, n), device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MIN, group=group)
+        torch.cuda.current_stream().synchronize()
+
+    return _reduce
+
+
+def run_pc_stable_sharded(c_ptr: int, ldc: int, p: int, sample_count: int, cfg=None, group=None,
+                          with_sepsets: bool = True):
+    """run_pc_stable over all ranks of `group` (torch.distributed initialised, one GPU per rank)."""
+    import torch.distributed as dist
+
+    from . import Session, SkeletonConfig
+
+    cfg = cfg or SkeletonConfig()
+    rank = dist.get_rank(group) if dist.is_initialized() else 0
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    s = Session(sample_count=sample_count, cfg=cfg, shard_index=rank, shard_count=world, device_ptr=c_ptr, ldc=ldc,
+                p=p)
+    try:
+        level_loop(s, torch_allreduce_min(group) if world > 1 else None, world)
+        return s.finish(with_sepsets)
+    finally:
+        s.close()
