@@ -1222,6 +1222,7 @@ int orc_run_level(const double* c, int p, const int32_t* offsets, const int32_t*
         for (int q = offsets[i]; q < offsets[i + 1]; ++q) {
             const int j = indices[q];
             atomic_store(&R->adj[(size_t)i * p + j], 1);
+            atomic_store(&R->adj[(size_t)j * p + i], 1);
             if (i >= row_begin && i < row_end) S.idx[n++] = j;
         }
         if ((int)(n - S.off[i]) > S.max_width) S.max_width = (int)(n - S.off[i]);

@@ -258,17 +258,25 @@ class AdjacencyMatrix:
 
 class SeparationSets:
     """Sepsets keyed by unordered pair (core.hpp:267-339).  Level-0 removals carry the empty set;
-    removals at level >= 1 come from the device's (a, b, ell, members...) records."""
+    removals at level >= 1 come from the device's records, grouped by level and looked up by
+    binary search (no per-record Python work until as_dict() is asked for)."""
 
-    def __init__(self, n: int, skeleton: AdjacencyMatrix, records: np.ndarray):
+    def __init__(self, n: int, skeleton: AdjacencyMatrix, records: np.ndarray, levels: list):
         self.n = n
         self._skel = skeleton
-        self._rec = {}
-        k = 0
-        while k < len(records):
-            a, b, ell = int(records[k]), int(records[k + 1]), int(records[k + 2])
-            self._rec[(min(a, b), max(a, b))] = tuple(int(v) for v in records[k + 3:k + 3 + ell])
-            k += 3 + ell
+        self._blocks = []
+        at = 0
+        for lv in levels:
+            if lv.level < 1 or lv.edges_removed == 0 or at >= len(records):
+                continue
+            ell, cnt = lv.level, lv.edges_removed
+            blk = np.asarray(records[at:at + cnt * (3 + ell)]).reshape(cnt, 3 + ell)
+            at += cnt * (3 + ell)
+            a = np.minimum(blk[:, 0], blk[:, 1]).astype(np.int64)
+            b = np.maximum(blk[:, 0], blk[:, 1]).astype(np.int64)
+            key = a * n + b
+            order = np.argsort(key, kind="stable")
+            self._blocks.append((ell, key[order], np.ascontiguousarray(blk[order, 3:])))
         self._dict = None
 
     def size(self) -> int:
@@ -277,16 +285,23 @@ class SeparationSets:
     def find(self, i: int, j: int):
         if i == j or not (0 <= i < self.n and 0 <= j < self.n):
             raise ValueError("SeparationSets: invalid vertex pair")
-        key = (min(i, j), max(i, j))
-        if self._skel.at(*key):
+        a, b = min(i, j), max(i, j)
+        if self._skel.at(a, b):
             return None
-        return self._rec.get(key, ())
+        k = a * self.n + b
+        for _, keys, mem in self._blocks:
+            x = int(np.searchsorted(keys, k))
+            if x < len(keys) and keys[x] == k:
+                return tuple(int(v) for v in mem[x])
+        return ()
 
     def as_dict(self) -> dict:
         if self._dict is None:
             iu, ju = np.nonzero(np.triu(1 - self._skel.cells, 1))
             d = {(int(a), int(b)): () for a, b in zip(iu, ju)}
-            d.update(self._rec)
+            for _, keys, mem in self._blocks:
+                for k, row in zip(keys.tolist(), mem.tolist()):
+                    d[(k // self.n, k % self.n)] = tuple(row)
             self._dict = d
         return self._dict
 
@@ -339,7 +354,7 @@ def _collect(h, with_sepsets: bool = True) -> SkeletonResult:
     if nrec:
         L.pcs_result_records(h, _ip(rec))
     adj = AdjacencyMatrix(bits, p)
-    sep = SeparationSets(p, adj, rec[:nrec] if with_sepsets else np.empty(0, np.int32))
+    sep = SeparationSets(p, adj, rec[:nrec] if with_sepsets else np.empty(0, np.int32), levels)
     return SkeletonResult(adj, sep, levels, _STOP[L.pcs_result_stop_reason(h)], L.pcs_result_device_seconds(h))
 
 

@@ -170,8 +170,10 @@ struct pcs_session {
     int32_t *dEuA = nullptr, *dEuQa = nullptr, *dEuQb = nullptr;
     unsigned long long* dKeys = nullptr;
     long long capUnd = 0;
-    int32_t* dRec = nullptr;
-    long long capRec = 0;
+    int32_t* dRec = nullptr;       // record pool: per level, count x (2 + ell) ints
+    long long capRec = 0, recUsed = 0;
+    struct LevelRecs { int ell; long long offset, count; };
+    std::vector<LevelRecs> recLevels;
     unsigned long long* dBinom = nullptr;
     size_t capBinom = 0;
     unsigned char* dScratch = nullptr;  // generic-ell per-lane scratch
@@ -187,7 +189,6 @@ struct pcs_session {
     float kernel_ms = 0.f;
     bool kernel_timing = false;
     std::vector<pcs_level_stats> levels;
-    std::vector<int32_t> recs;
 };
 
 namespace {
@@ -469,9 +470,20 @@ pcs_status pcs_session_level_begin(pcs_session* s, int32_t* running, int32_t* el
         if ((st = realloc_dev(&s->dKeys, s->info.e_und))) return st;
         s->capUnd = s->info.e_und;
     }
-    if (s->info.e_und * (2 + ell) > s->capRec) {
-        if ((st = realloc_dev(&s->dRec, s->info.e_und * (2 + ell)))) return st;
-        s->capRec = s->info.e_und * (2 + ell);
+    {
+        const long long need = s->recUsed + s->info.e_und * (2 + ell);
+        if (need > s->capRec) {  // grow the record pool, keeping earlier levels' records
+            const long long cap = std::max(need, s->capRec * 3 / 2);
+            int32_t* np = nullptr;
+            CUDA_TRY(cudaMalloc(&np, sizeof(int32_t) * (size_t)cap));
+            if (s->recUsed)
+                CUDA_TRY(cudaMemcpyAsync(np, s->dRec, sizeof(int32_t) * (size_t)s->recUsed, cudaMemcpyDeviceToDevice,
+                                         s->st));
+            CUDA_TRY(cudaStreamSynchronize(s->st));
+            cudaFree(s->dRec);
+            s->dRec = np;
+            s->capRec = cap;
+        }
     }
     if ((st = build_binomials(s, ell, maxw))) return st;
     launch_snapshot_fill(s->dAdj, s->p, s->W, s->dOff, s->dNbr, s->st);
@@ -557,7 +569,7 @@ pcs_status pcs_session_level_end(pcs_session* s) {
     if (!s || !s->in_level) return fail(PCS_EINVAL, "no level in progress");
     CUDA_TRY(cudaSetDevice(s->device));
     LevelArgs A = level_args(s);
-    if (s->ell >= 1) launch_commit(A, s->dAdj, s->W, s->info.e_und, s->dRec, s->st);
+    if (s->ell >= 1) launch_commit(A, s->dAdj, s->W, s->info.e_und, s->dRec + s->recUsed, s->st);
     Counters c{};
     CUDA_TRY(cudaMemcpyAsync(&c, s->dCnt, sizeof(Counters), cudaMemcpyDeviceToHost, s->st));
     CUDA_TRY(cudaStreamSynchronize(s->st));
@@ -577,15 +589,8 @@ pcs_status pcs_session_level_end(pcs_session* s) {
         L.device_ci_tests = c.gpu_tests;
         L.device_pseudo_inverses = c.gpu_pinv;
         if (c.rec_count) {
-            const size_t w = (size_t)(2 + s->ell);
-            std::vector<int32_t> r(c.rec_count * w);
-            CUDA_TRY(cudaMemcpy(r.data(), s->dRec, sizeof(int32_t) * r.size(), cudaMemcpyDeviceToHost));
-            for (unsigned long long k = 0; k < c.rec_count; ++k) {
-                s->recs.push_back(r[k * w]);
-                s->recs.push_back(r[k * w + 1]);
-                s->recs.push_back(s->ell);
-                for (int q = 0; q < s->ell; ++q) s->recs.push_back(r[k * w + 2 + q]);
-            }
+            s->recLevels.push_back({s->ell, s->recUsed, (long long)c.rec_count});
+            s->recUsed += (long long)c.rec_count * (2 + s->ell);
         }
     }
     L.edges_removed = c.removed;
@@ -608,7 +613,24 @@ pcs_status pcs_session_finish(pcs_session* s, pcs_result** out) {
     r->W = s->W;
     r->stop_reason = s->stop_reason;
     r->levels = s->levels;
-    r->recs = s->recs;
+    if (s->recUsed) {  // one copy of the record pool, re-laid out as (a, b, ell, members...)
+        std::vector<int32_t> pool((size_t)s->recUsed);
+        CUDA_TRY(cudaMemcpyAsync(pool.data(), s->dRec, sizeof(int32_t) * pool.size(), cudaMemcpyDeviceToHost, s->st));
+        CUDA_TRY(cudaStreamSynchronize(s->st));
+        size_t total = 0;
+        for (const auto& L : s->recLevels) total += (size_t)L.count * (3 + L.ell);
+        r->recs.resize(total);
+        size_t at = 0;
+        for (const auto& L : s->recLevels) {
+            const int32_t* src = pool.data() + L.offset;
+            for (long long k = 0; k < L.count; ++k, src += 2 + L.ell) {
+                r->recs[at++] = src[0];
+                r->recs[at++] = src[1];
+                r->recs[at++] = L.ell;
+                for (int q = 0; q < L.ell; ++q) r->recs[at++] = src[2 + q];
+            }
+        }
+    }
     r->adj.resize((size_t)s->p * s->W);
     CUDA_TRY(cudaMemcpyAsync(r->adj.data(), s->dAdj, sizeof(uint32_t) * r->adj.size(), cudaMemcpyDeviceToHost, s->st));
     CUDA_TRY(cudaEventRecord(s->ev_end, s->st));

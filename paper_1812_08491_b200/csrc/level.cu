@@ -404,18 +404,36 @@ struct SetSlot {
 };
 
 constexpr int kSetWarps = 4;
+constexpr int kTgtStage = 256;  // live targets staged per warp at a time
 
+// Per-warp shared memory: 32 set slots + a compacted list of the row's live targets.
 template <int L>
-__global__ void __launch_bounds__(kSetWarps * 32) level_set_kernel(LevelArgs A, int pass,
-                                                                  const unsigned long long* prefix,
-                                                                  unsigned long long u_begin,
-                                                                  unsigned long long u_end) {
+struct SetWarpSmem {
+    SetSlot<L> slot[32];
+    unsigned long long tkey[kTgtStage];  // current key of the target's edge (updated on a hit)
+    double tcij[kTgtStage];
+    int tq[kTgtStage];                    // position in the row
+    int tj[kTgtStage];                    // vertex id
+    int te[kTgtStage];                    // undirected edge id
+};
+
+// Unit = (row i, band of 32 consecutive conditioning-set ranks).  Phase 1: each lane
+// unranks one set, gathers M2 and computes its pseudo-inverse, P0 and h00 (the parts
+// shared by every target, stats.hpp:292-300) into its slot.  Phase 2: for each set in
+// rank order, with that set's data in registers, the lanes sweep the row's live targets
+// (compacted in shared memory); a target stops at its first separating set.
+template <int L>
+__global__ void __launch_bounds__(kSetWarps * 32, 4) level_set_kernel(LevelArgs A, int pass,
+                                                                     const unsigned long long* prefix,
+                                                                     unsigned long long u_begin,
+                                                                     unsigned long long u_end) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-    SetSlot<L>* slots = reinterpret_cast<SetSlot<L>*>(smem_raw) + wib * 32;
+    SetWarpSmem<L>& S = reinterpret_cast<SetWarpSmem<L>*>(smem_raw)[wib];
     const double* __restrict__ C = A.C;
     const long long ldc = A.ldc;
     const unsigned long long dirbits = (unsigned long long)pass << kDirShift;
+    const unsigned lt_mask = (1u << lane) - 1u;
     unsigned long long tests = 0, pinvs = 0;
     int nan = 0;
     unsigned long long* cursor = &A.cnt->units[pass];
@@ -429,80 +447,111 @@ __global__ void __launch_bounds__(kSetWarps * 32) level_set_kernel(LevelArgs A, 
         const int oi = A.off[i], w = A.off[i + 1] - oi, lc = A.lowcnt[i];
         const int qbeg = pass == 0 ? lc : 0, qend = pass == 0 ? w : lc;
         const unsigned long long K0 = dirbits | t0;
-        // any target of this row still open at rank t0?
-        bool open = false;
-        for (int q = qbeg + lane; q < qend; q += 32) open |= A.keys[A.eid[oi + q]] > K0;
-        if (!__any_sync(0xffffffffu, open)) continue;
-        // lane-parallel pseudo-inverses of the band's 32 sets
         const unsigned long long total = A.binom(w, L);
-        const unsigned long long t = t0 + lane;
-        const bool valid = t < total;
-        if (valid) {
-            int pos[L];
-            unrank<L>(A.binom, w, t, pos);
-            double m2[L * L], minv[L * L], ciS[L], p0[L], h00;
-#pragma unroll
-            for (int a = 0; a < L; ++a) {
-                slots[lane].pos[a] = pos[a];
-                const int ma = A.nbr[oi + pos[a]];
-                slots[lane].mem[a] = ma;
-                ciS[a] = __ldg(C + (size_t)i * ldc + ma);
+        const int nvalid = (int)min(32ull, total - t0);
+        bool have_sets = false;
+        for (int tb = qbeg; tb < qend; tb += kTgtStage) {
+            const int tend = min(tb + kTgtStage, qend);
+            // ---- stage the live targets of [tb, tend), compacted
+            int nlive = 0;
+            for (int q0 = tb; q0 < tend; q0 += 32) {
+                const int q = q0 + lane;
+                bool live = false;
+                int e = 0;
+                unsigned long long key = 0;
+                if (q < tend) {
+                    e = A.eid[oi + q];
+                    key = A.keys[e];
+                    live = key > K0;
+                }
+                const unsigned bal = __ballot_sync(0xffffffffu, live);
+                if (live) {
+                    const int at = nlive + __popc(bal & lt_mask);
+                    const int j = A.nbr[oi + q];
+                    S.tkey[at] = key;
+                    S.tq[at] = q;
+                    S.tj[at] = j;
+                    S.te[at] = e;
+                    S.tcij[at] = __ldg(C + (size_t)i * ldc + j);
+                }
+                nlive += __popc(bal);
             }
+            if (nlive == 0) continue;
+            // ---- phase 1 (once per unit): lane-parallel pseudo-inverses of the band's sets
+            if (!have_sets) {
+                have_sets = true;
+                if (lane < nvalid) {
+                    int pos[L];
+                    unrank<L>(A.binom, w, t0 + lane, pos);
+                    int mem[L];
+                    double m2[L * L], minv[L * L], ciS[L], p0[L], h00;
 #pragma unroll
-            for (int a = 0; a < L; ++a)
+                    for (int a = 0; a < L; ++a) {
+                        mem[a] = A.nbr[oi + pos[a]];
+                        ciS[a] = __ldg(C + (size_t)i * ldc + mem[a]);
+                    }
 #pragma unroll
-                for (int b = 0; b < L; ++b)
-                    m2[a * L + b] = __ldg(C + (size_t)slots[lane].mem[a] * ldc + slots[lane].mem[b]);
-            pinv<L>(m2, minv);
-            p0_terms<L>(minv, ciS, p0, h00);
+                    for (int a = 0; a < L; ++a)
 #pragma unroll
-            for (int q = 0; q < L * L; ++q) slots[lane].minv[q] = minv[q];
+                        for (int b = 0; b < L; ++b) m2[a * L + b] = __ldg(C + (size_t)mem[a] * ldc + mem[b]);
+                    pinv<L>(m2, minv);
+                    p0_terms<L>(minv, ciS, p0, h00);
+                    SetSlot<L>& sl = S.slot[lane];
 #pragma unroll
-            for (int a = 0; a < L; ++a) { slots[lane].ciS[a] = ciS[a]; slots[lane].p0[a] = p0[a]; }
-            slots[lane].h00 = h00;
-        }
-        const int nvalid = __popc(__ballot_sync(0xffffffffu, valid));
-        if (lane == 0) pinvs += nvalid;
-        __syncwarp();
-        // every open target of the row against the band's sets, in rank order
-        for (int qc = qbeg; qc < qend; qc += 32) {
-            const int q = qc + lane;
-            bool live = q < qend;
-            int j = 0, e = 0;
-            unsigned long long key = 0;
-            double cij = 0.0;
-            if (live) {
-                j = A.nbr[oi + q];
-                e = A.eid[oi + q];
-                key = A.keys[e];
-                live = key > K0;
-                if (live) cij = __ldg(C + (size_t)i * ldc + j);
+                    for (int q = 0; q < L * L; ++q) sl.minv[q] = minv[q];
+#pragma unroll
+                    for (int a = 0; a < L; ++a) {
+                        sl.ciS[a] = ciS[a];
+                        sl.p0[a] = p0[a];
+                        sl.pos[a] = pos[a];
+                        sl.mem[a] = mem[a];
+                    }
+                    sl.h00 = h00;
+                }
+                if (lane == 0) pinvs += nvalid;
             }
-            if (!__any_sync(0xffffffffu, live)) continue;
+            __syncwarp();
+            // ---- phase 2: sets in rank order, lanes over the live targets
             for (int sg = 0; sg < nvalid; ++sg) {
-                if (!live) break;
-                const SetSlot<L>& S = slots[sg];
+                const SetSlot<L>& sl = S.slot[sg];
+                double minv[L * L], ciS[L], p0[L];
+                int pos[L];
+                const double* cols[L];
+#pragma unroll
+                for (int q = 0; q < L * L; ++q) minv[q] = sl.minv[q];
+#pragma unroll
+                for (int a = 0; a < L; ++a) {
+                    ciS[a] = sl.ciS[a];
+                    p0[a] = sl.p0[a];
+                    pos[a] = sl.pos[a];
+                    cols[a] = C + (size_t)sl.mem[a] * ldc;
+                }
+                const double h00 = sl.h00;
                 const unsigned long long Kc = dirbits | (t0 + sg);
-                if (key <= Kc) { live = false; break; }
-                bool member = false;
+                for (int k = lane; k < nlive; k += 32) {
+                    if (S.tkey[k] <= Kc) continue;  // already separated at a lower rank
+                    const int q = S.tq[k];
+                    bool member = false;
 #pragma unroll
-                for (int a = 0; a < L; ++a) member |= S.pos[a] == q;
-                if (member) continue;
-                double cjS[L];
+                    for (int a = 0; a < L; ++a) member |= pos[a] == q;
+                    if (member) continue;
+                    const int j = S.tj[k];
+                    double cjS[L];
 #pragma unroll
-                for (int a = 0; a < L; ++a) cjS[a] = __ldg(C + (size_t)S.mem[a] * ldc + j);
-                double h01, denom;
-                h_terms<L>(S.minv, S.ciS, S.p0, S.h00, cjS, cij, h01, denom);
-                const int d = decide_fast(h01, denom, A.th);
-                ++tests;
-                if (d != kDependent) {
-                    live = false;
-                    if (d == kNanError) nan = 1;
-                    else atomicMin(A.keys + e, Kc);
+                    for (int a = 0; a < L; ++a) cjS[a] = __ldg(cols[a] + j);
+                    double h01, denom;
+                    h_terms<L>(minv, ciS, p0, h00, cjS, S.tcij[k], h01, denom);
+                    const int d = decide_fast(h01, denom, A.th);
+                    ++tests;
+                    if (d != kDependent) {
+                        if (d == kNanError) nan = 1;
+                        else atomicMin(A.keys + S.te[k], Kc);
+                        S.tkey[k] = Kc;
+                    }
                 }
             }
+            __syncwarp();
         }
-        __syncwarp();
     }
     add_counter(&A.cnt->gpu_tests, tests);
     if (lane == 0 && pinvs) atomicAdd(&A.cnt->gpu_pinv, pinvs);
@@ -512,7 +561,7 @@ __global__ void __launch_bounds__(kSetWarps * 32) level_set_kernel(LevelArgs A, 
 template <int L>
 static int launch_set_L(const LevelArgs& A, int pass, const unsigned long long* prefix, unsigned long long u_begin,
                         unsigned long long u_end, int num_sms, cudaStream_t s) {
-    const size_t smem = sizeof(SetSlot<L>) * 32 * kSetWarps;
+    const size_t smem = sizeof(SetWarpSmem<L>) * kSetWarps;
     static bool attr_set = false;
     if (!attr_set) {
         cudaFuncSetAttribute(level_set_kernel<L>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
