@@ -511,12 +511,11 @@ __global__ void __launch_bounds__(kSetWarps * 32, 4) level_set_kernel(LevelArgs 
                 if (lane == 0) pinvs += nvalid;
             }
             __syncwarp();
-            // ---- phase 2: sets in rank order, lanes over the live targets
+            // ---- phase 2: sets in rank order, lanes over the live targets (two per lane per step)
             for (int sg = 0; sg < nvalid; ++sg) {
                 const SetSlot<L>& sl = S.slot[sg];
                 double minv[L * L], ciS[L], p0[L];
-                int pos[L];
-                const double* cols[L];
+                int pos[L], roff[L];
 #pragma unroll
                 for (int q = 0; q < L * L; ++q) minv[q] = sl.minv[q];
 #pragma unroll
@@ -524,29 +523,52 @@ __global__ void __launch_bounds__(kSetWarps * 32, 4) level_set_kernel(LevelArgs 
                     ciS[a] = sl.ciS[a];
                     p0[a] = sl.p0[a];
                     pos[a] = sl.pos[a];
-                    cols[a] = C + (size_t)sl.mem[a] * ldc;
+                    roff[a] = sl.mem[a] * (int)ldc;  // p * ldc < 2^31 (p <= 46340)
                 }
                 const double h00 = sl.h00;
                 const unsigned long long Kc = dirbits | (t0 + sg);
-                for (int k = lane; k < nlive; k += 32) {
-                    if (S.tkey[k] <= Kc) continue;  // already separated at a lower rank
-                    const int q = S.tq[k];
-                    bool member = false;
+                for (int k0 = 0; k0 < nlive; k0 += 64) {
+                    const int ka = k0 + lane, kb = ka + 32;
+                    bool va = ka < nlive && S.tkey[ka] > Kc;
+                    bool vb = kb < nlive && S.tkey[kb] > Kc;
+                    int qa = -1, qb = -1;
+                    if (va) qa = S.tq[ka];
+                    if (vb) qb = S.tq[kb];
 #pragma unroll
-                    for (int a = 0; a < L; ++a) member |= pos[a] == q;
-                    if (member) continue;
-                    const int j = S.tj[k];
-                    double cjS[L];
+                    for (int a = 0; a < L; ++a) {
+                        va = va && pos[a] != qa;
+                        vb = vb && pos[a] != qb;
+                    }
+                    if (!(va || vb)) continue;
+                    const double* Ca = C + (va ? S.tj[ka] : 0);
+                    const double* Cb = C + (vb ? S.tj[kb] : 0);
+                    double cjA[L], cjB[L];
 #pragma unroll
-                    for (int a = 0; a < L; ++a) cjS[a] = __ldg(cols[a] + j);
-                    double h01, denom;
-                    h_terms<L>(minv, ciS, p0, h00, cjS, S.tcij[k], h01, denom);
-                    const int d = decide_fast(h01, denom, A.th);
-                    ++tests;
-                    if (d != kDependent) {
-                        if (d == kNanError) nan = 1;
-                        else atomicMin(A.keys + S.te[k], Kc);
-                        S.tkey[k] = Kc;
+                    for (int a = 0; a < L; ++a) {
+                        cjA[a] = __ldg(Ca + roff[a]);
+                        cjB[a] = __ldg(Cb + roff[a]);
+                    }
+                    const double cija = va ? S.tcij[ka] : 0.0, cijb = vb ? S.tcij[kb] : 0.0;
+                    double h01a, dena, h01b, denb;
+                    h_terms<L>(minv, ciS, p0, h00, cjA, cija, h01a, dena);
+                    h_terms<L>(minv, ciS, p0, h00, cjB, cijb, h01b, denb);
+                    if (va) {
+                        const int d = decide_fast(h01a, dena, A.th);
+                        ++tests;
+                        if (d != kDependent) {
+                            if (d == kNanError) nan = 1;
+                            else atomicMin(A.keys + S.te[ka], Kc);
+                            S.tkey[ka] = Kc;
+                        }
+                    }
+                    if (vb) {
+                        const int d = decide_fast(h01b, denb, A.th);
+                        ++tests;
+                        if (d != kDependent) {
+                            if (d == kNanError) nan = 1;
+                            else atomicMin(A.keys + S.te[kb], Kc);
+                            S.tkey[kb] = Kc;
+                        }
                     }
                 }
             }
