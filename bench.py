@@ -294,10 +294,13 @@ def main():
                 "kernel": f"level-{dom.level} CI-test kernels ({'level1_kernel' if dom.level == 1 else 'level_set_kernel' if args.variant == 'set' else 'level_edge_kernel'}), 2 passes",
                 "kernel_ms": dom.kernel_ms, "algorithmic_flop": fl,
                 "peak_source": "pcs_probe_fp64_tflops (DFMA probe, this box; MEASURED_PEAKS.json has no FP64 figure)"}
-    prof = os.path.join(ROOT, "profiles", "r01_ncu_summary.json")
+    prof = os.path.join(ROOT, "profiles", "ncu_traffic.json")  # written by tools/ncu_summary.py
     if os.path.exists(prof):
         try:
-            roofline["traffic"] = json.load(open(prof)).get("traffic_bytes_per_launch")
+            t = json.load(open(prof))
+            if t.get("kernel_tag") == f"level_set_kernel<{dom.level}>" and args.variant == "set":
+                roofline["traffic"] = t.get("traffic_bytes_per_launch")
+                roofline["traffic_note"] = t.get("note")
         except Exception:
             pass
 

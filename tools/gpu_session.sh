@@ -1,0 +1,33 @@
+#!/bin/bash
+# One gpurun session: GPU tests, smoke, per-level diagnostics, bench line, ncu launch list and one
+# --set full capture of the dominant kernel.  Usage (from this container):
+#   gpurun --timeout 2400 -- 'bash tools/gpu_session.sh [tests] [explore] [bench] [ncu]'
+set -u
+mkdir -p gpurun_out
+OUT=gpurun_out
+STEPS="${*:-tests explore bench ncu}"
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,memory.total --format=csv > $OUT/gpu.txt 2>&1
+nproc >> $OUT/gpu.txt
+python -c "import __graft_entry__ as g; g.build()" > $OUT/build.log 2>&1 || echo "build failed" >> $OUT/build.log
+for s in $STEPS; do
+  case $s in
+    tests)
+      timeout 1200 python -m pytest tests -m gpu -x -q > $OUT/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> $OUT/pytest_gpu.log
+      timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $OUT/smoke.log 2>&1; echo "smoke rc=$?" >> $OUT/smoke.log
+      ;;
+    explore)
+      timeout 600 python tools/explore.py C1,C3,C4 set,edge > $OUT/explore.log 2>&1
+      timeout 600 python tools/explore.py C2 set 3 >> $OUT/explore.log 2>&1
+      ;;
+    bench)
+      timeout 900 python bench.py > $OUT/bench.json 2> $OUT/bench.err
+      ;;
+    ncu)
+      timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/launches.csv \
+        python bench.py --steps 1 --warmup 0 --no-cpu-baseline --no-e2e > $OUT/ncu_bench.log 2>&1
+      timeout 900 ncu --set full --clock-control none --import-source on -k regex:level_set --launch-skip 2 -c 1 -f -o $OUT/top \
+        python tools/profile_target.py 3 32 set > $OUT/ncu_full.log 2>&1
+      ;;
+  esac
+done
+echo done > $OUT/session_done.txt
