@@ -393,6 +393,25 @@ void launch_level1(const LevelArgs& A, int pass, const unsigned long long* prefi
 }
 
 // =========================================================== ell >= 2, cuPC-S
+// Unit = (row i, band of 32 consecutive conditioning-set ranks t0 .. t0+31).
+//
+// Phase 1 (once per unit): lane k unranks set t0+k, gathers M2 and computes its
+// pseudo-inverse and the per-set parts of the test (P0 = C(i,S) M2^+, h00;
+// stats.hpp:292-300) into shared slot k.
+//
+// Phase 2: the row's live targets (edges whose key is still above the band's
+// first rank) are compacted into shared memory and dealt out NT per lane
+// (interleaved, so lanes hold neighbouring vertex ids).  The warp then walks the
+// 32 sets in rank order; per set every lane evaluates its NT targets as
+// independent straight-line chains (ILP NT).  Consecutive ranks share their first
+// L-1 members, so the gathers C(j, S) of those members stay in registers until the
+// prefix changes and only the last member is gathered per test -- one L2 load per
+// test instead of L -- and that load is issued one set ahead (software prefetch).
+// A target stops at its first separating set (its relative key drops to that set).
+//
+// A unit that finds no live target proves every later unit of the row dead
+// (keys only decrease, ranks only increase) and advances the work cursor past the
+// row.
 template <int L>
 struct SetSlot {
     double minv[L * L];
@@ -400,34 +419,144 @@ struct SetSlot {
     double p0[L];
     double h00;
     int pos[L];
-    int mem[L];
+    int roff[L];  // row offsets mem[a] * ldc of the set's members
 };
 
 constexpr int kSetWarps = 4;
-constexpr int kTgtStage = 256;  // live targets staged per warp at a time
 
-// Per-warp shared memory: 32 set slots + a compacted list of the row's live targets.
+template <int L>
+struct SetCfg {
+    static constexpr int NT = L <= 3 ? 4 : 2;  // targets per lane per set
+    static constexpr int kStage = 32 * NT;     // live targets staged per pass over the band
+};
+
 template <int L>
 struct SetWarpSmem {
     SetSlot<L> slot[32];
-    unsigned long long tkey[kTgtStage];  // current key of the target's edge (updated on a hit)
-    double tcij[kTgtStage];
-    int tq[kTgtStage];                    // position in the row
-    int tj[kTgtStage];                    // vertex id
-    int te[kTgtStage];                    // undirected edge id
+    unsigned long long tkey[SetCfg<L>::kStage];
+    double tcij[SetCfg<L>::kStage];
+    int tq[SetCfg<L>::kStage];
+    int tj[SetCfg<L>::kStage];
+    int te[SetCfg<L>::kStage];
 };
 
-// Unit = (row i, band of 32 consecutive conditioning-set ranks).  Phase 1: each lane
-// unranks one set, gathers M2 and computes its pseudo-inverse, P0 and h00 (the parts
-// shared by every target, stats.hpp:292-300) into its slot.  Phase 2: for each set in
-// rank order, with that set's data in registers, the lanes sweep the row's live targets
-// (compacted in shared memory); a target stops at its first separating set.
+// Phase 2 for one staged batch of targets, NT (<= SetCfg<L>::NT) per lane.
+// segmask: bit s set when set s starts a new run of equal leading L-1 members.
+template <int L, int NT>
+__device__ __forceinline__ void set_sweep(const LevelArgs& A, SetWarpSmem<L>& S, int lane, int nlive, int nvalid,
+                                          unsigned segmask, unsigned long long K0, unsigned long long& tests,
+                                          int& nan) {
+    const double* __restrict__ C = A.C;
+    const double hi2 = A.th.hi2;
+    int tq[NT], te[NT], rel[NT];
+    const double* Cj[NT];  // C + j: gathers C(mem, j) = Cj[t][mem * ldc] (one IMAD.WIDE each)
+    double cij[NT];
+#pragma unroll
+    for (int t = 0; t < NT; ++t) {
+        const int k = t * 32 + lane;
+        if (k < nlive) {
+            const unsigned long long d = S.tkey[k] - K0;  // > 0 (staged targets are live)
+            rel[t] = d > 0x3fffffffull ? 0x3fffffff : (int)d;
+            tq[t] = S.tq[k];
+            Cj[t] = C + S.tj[k];
+            te[t] = S.te[k];
+            cij[t] = S.tcij[k];
+        } else {
+            rel[t] = -1;
+            tq[t] = -1;
+            Cj[t] = C;  // valid address: loads stay unconditional
+            te[t] = 0;
+            cij[t] = 0.0;
+        }
+    }
+    constexpr int LP = L > 1 ? L - 1 : 1;
+    double cp[NT][LP];
+    double nxt[NT];
+    {
+        const int ro = S.slot[0].roff[L - 1];
+#pragma unroll
+        for (int t = 0; t < NT; ++t) nxt[t] = __ldg(Cj[t] + ro);
+    }
+    const unsigned valid_mask = nvalid >= 32 ? 0xffffffffu : ((1u << nvalid) - 1u);
+    segmask &= valid_mask;
+    int sg = 0;
+    while (sg < nvalid) {
+        // new run of sets sharing their first L-1 members: gather those once per target
+        {
+            const SetSlot<L>& sl = S.slot[sg];
+#pragma unroll
+            for (int a = 0; a < L - 1; ++a) {
+                const int ro = sl.roff[a];
+#pragma unroll
+                for (int t = 0; t < NT; ++t) cp[t][a] = __ldg(Cj[t] + ro);
+            }
+        }
+        const unsigned later = segmask & ~((2u << sg) - 1u);
+        const int seg_end = later ? __ffs(later) - 1 : nvalid;
+        for (; sg < seg_end; ++sg) {
+            const SetSlot<L>& sl = S.slot[sg];
+            double cur[NT];
+#pragma unroll
+            for (int t = 0; t < NT; ++t) cur[t] = nxt[t];
+            {  // prefetch the next set's last-member gathers (clamped: always a valid slot)
+                const int ro = S.slot[min(sg + 1, nvalid - 1)].roff[L - 1];
+#pragma unroll
+                for (int t = 0; t < NT; ++t) nxt[t] = __ldg(Cj[t] + ro);
+            }
+            double minv[L * L], ciS[L], p0[L];
+            int pos[L];
+#pragma unroll
+            for (int q = 0; q < L * L; ++q) minv[q] = sl.minv[q];
+#pragma unroll
+            for (int a = 0; a < L; ++a) {
+                ciS[a] = sl.ciS[a];
+                p0[a] = sl.p0[a];
+                pos[a] = sl.pos[a];
+            }
+            const double h00 = sl.h00;
+            double h01[NT], den[NT];
+#pragma unroll
+            for (int t = 0; t < NT; ++t) {
+                double cjS[L];
+#pragma unroll
+                for (int a = 0; a < L - 1; ++a) cjS[a] = cp[t][a];
+                cjS[L - 1] = cur[t];
+                h_terms<L>(minv, ciS, p0, h00, cjS, cij[t], h01[t], den[t]);
+            }
+            // branch-free common path: count the valid tests, flag the (rare) possible hits
+            unsigned cand = 0;
+#pragma unroll
+            for (int t = 0; t < NT; ++t) {
+                bool v = rel[t] > sg;
+#pragma unroll
+                for (int a = 0; a < L; ++a) v = v && pos[a] != tq[t];
+                tests += v;
+                cand |= (unsigned)(v && !surely_dependent(h01[t], den[t], hi2)) << t;
+            }
+            if (__any_sync(0xffffffffu, cand)) {
+#pragma unroll
+                for (int t = 0; t < NT; ++t) {
+                    if ((cand >> t) & 1u) {
+                        const int d = decide_fast(h01[t], den[t], A.th);
+                        if (d != kDependent) {
+                            if (d == kNanError) nan = 1;
+                            else atomicMin(A.keys + te[t], K0 + (unsigned long long)sg);
+                            rel[t] = sg;
+                        }
+                    }
+                }
+            }
+        }
+    }
+}
+
 template <int L>
-__global__ void __launch_bounds__(kSetWarps * 32, 4) level_set_kernel(LevelArgs A, int pass,
+__global__ void __launch_bounds__(kSetWarps * 32, 3) level_set_kernel(LevelArgs A, int pass,
                                                                      const unsigned long long* prefix,
                                                                      unsigned long long u_begin,
                                                                      unsigned long long u_end) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
+    constexpr int kStage = SetCfg<L>::kStage;
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     SetWarpSmem<L>& S = reinterpret_cast<SetWarpSmem<L>*>(smem_raw)[wib];
     const double* __restrict__ C = A.C;
@@ -450,8 +579,9 @@ __global__ void __launch_bounds__(kSetWarps * 32, 4) level_set_kernel(LevelArgs 
         const unsigned long long total = A.binom(w, L);
         const int nvalid = (int)min(32ull, total - t0);
         bool have_sets = false;
-        for (int tb = qbeg; tb < qend; tb += kTgtStage) {
-            const int tend = min(tb + kTgtStage, qend);
+        unsigned segmask = 1u;
+        for (int tb = qbeg; tb < qend; tb += kStage) {
+            const int tend = min(tb + kStage, qend);
             // ---- stage the live targets of [tb, tend), compacted
             int nlive = 0;
             for (int q0 = tb; q0 < tend; q0 += 32) {
@@ -504,75 +634,42 @@ __global__ void __launch_bounds__(kSetWarps * 32, 4) level_set_kernel(LevelArgs 
                         sl.ciS[a] = ciS[a];
                         sl.p0[a] = p0[a];
                         sl.pos[a] = pos[a];
-                        sl.mem[a] = mem[a];
+                        sl.roff[a] = mem[a] * (int)ldc;  // p * ldc < 2^31 (p <= 46340)
                     }
                     sl.h00 = h00;
                 }
                 if (lane == 0) pinvs += nvalid;
-            }
-            __syncwarp();
-            // ---- phase 2: sets in rank order, lanes over the live targets (two per lane per step)
-            for (int sg = 0; sg < nvalid; ++sg) {
-                const SetSlot<L>& sl = S.slot[sg];
-                double minv[L * L], ciS[L], p0[L];
-                int pos[L], roff[L];
+                // runs of consecutive sets with equal leading L-1 members (lexicographic order)
+                bool starts = lane == 0;
+                if (L > 1) {
+                    const int prev = lane > 0 ? lane - 1 : 0;
 #pragma unroll
-                for (int q = 0; q < L * L; ++q) minv[q] = sl.minv[q];
-#pragma unroll
-                for (int a = 0; a < L; ++a) {
-                    ciS[a] = sl.ciS[a];
-                    p0[a] = sl.p0[a];
-                    pos[a] = sl.pos[a];
-                    roff[a] = sl.mem[a] * (int)ldc;  // p * ldc < 2^31 (p <= 46340)
-                }
-                const double h00 = sl.h00;
-                const unsigned long long Kc = dirbits | (t0 + sg);
-                for (int k0 = 0; k0 < nlive; k0 += 64) {
-                    const int ka = k0 + lane, kb = ka + 32;
-                    bool va = ka < nlive && S.tkey[ka] > Kc;
-                    bool vb = kb < nlive && S.tkey[kb] > Kc;
-                    int qa = -1, qb = -1;
-                    if (va) qa = S.tq[ka];
-                    if (vb) qb = S.tq[kb];
-#pragma unroll
-                    for (int a = 0; a < L; ++a) {
-                        va = va && pos[a] != qa;
-                        vb = vb && pos[a] != qb;
-                    }
-                    if (!(va || vb)) continue;
-                    const double* Ca = C + (va ? S.tj[ka] : 0);
-                    const double* Cb = C + (vb ? S.tj[kb] : 0);
-                    double cjA[L], cjB[L];
-#pragma unroll
-                    for (int a = 0; a < L; ++a) {
-                        cjA[a] = __ldg(Ca + roff[a]);
-                        cjB[a] = __ldg(Cb + roff[a]);
-                    }
-                    const double cija = va ? S.tcij[ka] : 0.0, cijb = vb ? S.tcij[kb] : 0.0;
-                    double h01a, dena, h01b, denb;
-                    h_terms<L>(minv, ciS, p0, h00, cjA, cija, h01a, dena);
-                    h_terms<L>(minv, ciS, p0, h00, cjB, cijb, h01b, denb);
-                    if (va) {
-                        const int d = decide_fast(h01a, dena, A.th);
-                        ++tests;
-                        if (d != kDependent) {
-                            if (d == kNanError) nan = 1;
-                            else atomicMin(A.keys + S.te[ka], Kc);
-                            S.tkey[ka] = Kc;
-                        }
-                    }
-                    if (vb) {
-                        const int d = decide_fast(h01b, denb, A.th);
-                        ++tests;
-                        if (d != kDependent) {
-                            if (d == kNanError) nan = 1;
-                            else atomicMin(A.keys + S.te[kb], Kc);
-                            S.tkey[kb] = Kc;
-                        }
+                    for (int a = 0; a < L - 1; ++a) {
+                        const int mine = lane < nvalid ? S.slot[lane].pos[a] : -1;
+                        const int theirs = __shfl_sync(0xffffffffu, mine, prev);
+                        starts = starts || mine != theirs;
                     }
                 }
+                segmask = __ballot_sync(0xffffffffu, starts);
             }
             __syncwarp();
+            // ---- phase 2: sets in rank order, NT targets per lane
+            const int nt = (nlive + 31) >> 5;
+            if constexpr (SetCfg<L>::NT == 4) {
+                if (nt == 4) set_sweep<L, 4>(A, S, lane, nlive, nvalid, segmask, K0, tests, nan);
+                else if (nt == 3) set_sweep<L, 3>(A, S, lane, nlive, nvalid, segmask, K0, tests, nan);
+                else if (nt == 2) set_sweep<L, 2>(A, S, lane, nlive, nvalid, segmask, K0, tests, nan);
+                else set_sweep<L, 1>(A, S, lane, nlive, nvalid, segmask, K0, tests, nan);
+            } else {
+                if (nt == 2) set_sweep<L, 2>(A, S, lane, nlive, nvalid, segmask, K0, tests, nan);
+                else set_sweep<L, 1>(A, S, lane, nlive, nvalid, segmask, K0, tests, nan);
+            }
+            __syncwarp();
+        }
+        if (!have_sets && lane == 0) {
+            // no live target at rank t0: none at any later rank of this row either
+            const unsigned long long next_row = prefix[i + 1] - u_begin;
+            atomicMax(cursor, next_row);
         }
     }
     add_counter(&A.cnt->gpu_tests, tests);

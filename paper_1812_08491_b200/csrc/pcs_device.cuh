@@ -263,6 +263,15 @@ __device__ __forceinline__ int decide_fast(double h01, double denom, const Thres
     return decide_exact(h01, denom, th.tau);
 }
 
+// Branch-free common-case filter: true only when decide_exact() is certainly
+// kDependent (rho^2 provably above the upper band; NaN / degenerate / tiny
+// denominators fall through to decide_fast()).  With denom >= 1e-250 and
+// hi2 >= tanh(tau)^2 > 1e-4 the product is a normal number, so both sides carry
+// at most one rounding and the 1e-9 band dominates.
+__device__ __forceinline__ bool surely_dependent(double h01, double denom, double hi2) {
+    return (denom >= 1e-250) & (h01 * h01 >= denom * hi2);
+}
+
 // Level-0 decision on rho = clamp(c_ij) (stats.hpp:309-312).
 __device__ __forceinline__ int decide0(double c, const Thresholds& th) {
     const double ac = fabs(c);

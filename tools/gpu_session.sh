@@ -19,6 +19,13 @@ for s in $STEPS; do
       timeout 600 python tools/explore.py C1,C3,C4 set,edge > $OUT/explore.log 2>&1
       timeout 600 python tools/explore.py C2 set 3 >> $OUT/explore.log 2>&1
       ;;
+    c2)
+      timeout 600 python tools/explore.py C2 set 3 > $OUT/explore_c2.log 2>&1
+      ;;
+    ncufull)
+      timeout 900 ncu --set full --clock-control none --import-source on -k regex:level_set --launch-skip 2 -c 1 -f -o $OUT/top \
+        python tools/profile_target.py 3 32 set > $OUT/ncu_full.log 2>&1
+      ;;
     bench)
       timeout 900 python bench.py > $OUT/bench.json 2> $OUT/bench.err
       ;;
