@@ -75,6 +75,8 @@ typedef struct {
     uint64_t device_ci_tests;         /* CI tests the device actually executed */
     uint64_t device_pseudo_inverses;  /* pseudo-inverses the device actually executed */
     double kernel_ms;                 /* CUDA-event time of the level's CI-test kernels */
+    uint64_t device_exact_tests;      /* tests re-evaluated in the reference's operation order (not
+                                         certified dependent by the FMA filter) */
 } pcs_level_stats;
 
 typedef struct pcs_result pcs_result;
@@ -161,6 +163,30 @@ pcs_status pcs_session_set_shard(pcs_session* s, int32_t shard_index, int32_t sh
 pcs_status pcs_session_snapshot(pcs_session* s, int32_t* offsets, int32_t* indices);
 pcs_status pcs_session_finish(pcs_session* s, pcs_result** out);
 void pcs_session_free(pcs_session* s);
+
+/* ---- orientation (orient.hpp) ----
+ * MixedGraph (orient.hpp:15-32): directed (from, to) pairs and undirected (a < b) pairs, both ascending
+ * (the reference's std::set order).  stage 1 = find_v_structures (orient.hpp:40-89, device kernel),
+ * 2 = apply_meek_rules (orient.hpp:147-167, host fixed point in the reference's visiting order),
+ * 3 = orient_skeleton (orient.hpp:170-173).  PCS_EINVAL when a consulted nonadjacent pair has no
+ * separating set (the reference's std::invalid_argument, orient.hpp:60-63). */
+typedef struct pcs_mixed_graph pcs_mixed_graph;
+/* on a device result (its skeleton and sepsets; level-0 removals carry S = {}) */
+pcs_status pcs_orient_result(const pcs_result* r, int32_t stage, pcs_mixed_graph** out);
+/* on the compact result form: live bitmask p x ceil(p/32) and the (a, b, ell, members) records */
+pcs_status pcs_orient_records(int32_t p, const uint32_t* bitmask, const int32_t* records, int64_t record_ints,
+                              int32_t stage, pcs_mixed_graph** out);
+/* on caller data: skeleton p*p uint8 (symmetric) and sepsets in pcs_result_sepsets' triangular layout
+ * (level -1 = no separating set).  With stage 2 the input mixed graph is directed_in (pairs) plus every
+ * other skeleton edge undirected. */
+pcs_status pcs_orient_skeleton(int32_t p, const uint8_t* adj, const int32_t* sep_level, const int64_t* sep_offset,
+                               const int32_t* members, int32_t stage, const int32_t* directed_in,
+                               int64_t n_directed_in, pcs_mixed_graph** out);
+int64_t pcs_mixed_directed_count(const pcs_mixed_graph* g);
+int64_t pcs_mixed_undirected_count(const pcs_mixed_graph* g);
+void pcs_mixed_directed(const pcs_mixed_graph* g, int32_t* pairs /* 2 * count */);
+void pcs_mixed_undirected(const pcs_mixed_graph* g, int32_t* pairs /* 2 * count */);
+void pcs_mixed_free(pcs_mixed_graph* g);
 
 #ifdef __cplusplus
 }

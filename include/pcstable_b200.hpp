@@ -42,6 +42,7 @@
 #include <cstdint>
 #include <memory>
 #include <optional>
+#include <set>
 #include <stdexcept>
 #include <string>
 #include <utility>
@@ -337,6 +338,7 @@ struct LevelStats {
     std::uint64_t device_ci_tests = 0;
     std::uint64_t device_pseudo_inverses = 0;
     double kernel_ms = 0.0;
+    std::uint64_t device_exact_tests = 0;
 };
 
 enum class StopReason { MaxDegreeReached, LevelCapReached, SampleSizeExhausted };
@@ -425,6 +427,7 @@ inline SkeletonResult collect(pcs_result* raw) {
         x.device_ci_tests = L.device_ci_tests;
         x.device_pseudo_inverses = L.device_pseudo_inverses;
         x.kernel_ms = L.kernel_ms;
+        x.device_exact_tests = L.device_exact_tests;
         levels.push_back(x);
     }
     StopReason reason = StopReason::MaxDegreeReached;
@@ -458,6 +461,89 @@ inline SkeletonResult run_pc_stable(const DataMatrix& data, const SkeletonConfig
     detail::check(pcs_run_pc_stable_data(data.data(), data.sample_count(), data.variable_count(), &abi, &r, &col),
                   col);
     return detail::collect(r);
+}
+
+/// Partially directed graph produced by orientation (orient.hpp:15-32).
+struct MixedGraph {
+    Index n = 0;
+    std::set<std::pair<Index, Index>> directed;
+    std::set<std::pair<Index, Index>> undirected;
+
+    bool has_directed(Index from, Index to) const { return directed.count({from, to}) > 0; }
+    bool has_undirected(Index a, Index b) const {
+        if (a > b) std::swap(a, b);
+        return undirected.count({a, b}) > 0;
+    }
+    bool adjacent(Index a, Index b) const { return has_undirected(a, b) || has_directed(a, b) || has_directed(b, a); }
+    friend bool operator==(const MixedGraph& x, const MixedGraph& y) {
+        return x.n == y.n && x.directed == y.directed && x.undirected == y.undirected;
+    }
+};
+
+namespace detail {
+
+inline MixedGraph orient_call(const AdjacencyMatrix& skeleton, const SeparationSets* sepsets, int stage,
+                              const std::vector<int32_t>& directed_in) {
+    const Index n = skeleton.size();
+    if (sepsets && sepsets->size() != n)
+        throw std::invalid_argument("find_v_structures: skeleton and sepsets sizes differ");
+    const std::size_t slots = static_cast<std::size_t>(n) * (n - 1) / 2;
+    std::vector<int32_t> level(std::max<std::size_t>(slots, 1), -1), members;
+    std::vector<int64_t> offset(std::max<std::size_t>(slots, 1), 0);
+    std::vector<uint8_t> cells(static_cast<std::size_t>(n) * n);
+    for (Index i = 0; i < n; ++i)
+        for (Index j = 0; j < n; ++j) cells[static_cast<std::size_t>(i) * n + j] = i != j && skeleton.at(i, j);
+    if (sepsets) {
+        std::size_t s = 0;
+        for (Index i = 0; i < n; ++i)
+            for (Index j = i + 1; j < n; ++j, ++s)
+                if (const auto* set = sepsets->find(i, j)) {
+                    level[s] = static_cast<int32_t>(set->size());
+                    offset[s] = static_cast<int64_t>(members.size());
+                    members.insert(members.end(), set->begin(), set->end());
+                }
+    }
+    if (members.empty()) members.push_back(0);
+    pcs_mixed_graph* g = nullptr;
+    check(pcs_orient_skeleton(n, cells.data(), level.data(), offset.data(), members.data(), stage,
+                              directed_in.empty() ? nullptr : directed_in.data(),
+                              static_cast<int64_t>(directed_in.size() / 2), &g));
+    MixedGraph out;
+    out.n = n;
+    std::vector<int32_t> d(2 * static_cast<std::size_t>(pcs_mixed_directed_count(g)) + 2),
+        u(2 * static_cast<std::size_t>(pcs_mixed_undirected_count(g)) + 2);
+    pcs_mixed_directed(g, d.data());
+    pcs_mixed_undirected(g, u.data());
+    for (int64_t k = 0; k < pcs_mixed_directed_count(g); ++k) out.directed.insert({d[2 * k], d[2 * k + 1]});
+    for (int64_t k = 0; k < pcs_mixed_undirected_count(g); ++k) out.undirected.insert({u[2 * k], u[2 * k + 1]});
+    pcs_mixed_free(g);
+    return out;
+}
+
+}  // namespace detail
+
+/// find_v_structures (orient.hpp:40-89): unshielded-triple votes on the device.
+inline MixedGraph find_v_structures(const AdjacencyMatrix& skeleton, const SeparationSets& sepsets) {
+    return detail::orient_call(skeleton, &sepsets, 1, {});
+}
+
+/// apply_meek_rules (orient.hpp:147-167): the reference's visiting order, on the host.
+inline MixedGraph apply_meek_rules(MixedGraph g) {
+    if (g.n < 2) return g;
+    AdjacencyMatrix skel(g.n);
+    std::vector<int32_t> din;
+    for (const auto& [a, b] : g.directed) {
+        skel.set_edge(a, b);
+        din.push_back(a);
+        din.push_back(b);
+    }
+    for (const auto& [a, b] : g.undirected) skel.set_edge(a, b);
+    return detail::orient_call(skel, nullptr, 2, din);
+}
+
+/// orient_skeleton (orient.hpp:170-173).
+inline MixedGraph orient_skeleton(const AdjacencyMatrix& skeleton, const SeparationSets& sepsets) {
+    return detail::orient_call(skeleton, &sepsets, 3, {});
 }
 
 }  // namespace pcstable

@@ -129,6 +129,14 @@ int orc_level_keys(const double* c, int p, const int32_t* offsets, const int32_t
 int orc_run_level(const double* c, int p, const int32_t* offsets, const int32_t* indices, int ell, double tau,
                   const orc_config* cfg, int row_begin, int row_end, orc_level_stats* out);
 
+/* ---- orient.hpp (pcs_orient_oracle.c) ----
+ * stage bit 1: find_v_structures, bit 2: apply_meek_rules (3 = orient_skeleton).  With bit 1 clear
+ * the input mixed graph is directed_in + every other skeleton edge undirected.  Outputs ascending
+ * pairs; buffers hold n*(n-1)/2 pairs.  ORC_EINVAL: a consulted nonadjacent pair has no sepset. */
+int orc_orient(int n, const uint8_t* skeleton, const int32_t* sep_level, const int64_t* sep_offset,
+               const int32_t* members, int stage, const int32_t* directed_in, int64_t n_directed_in,
+               int32_t* dir_out, int64_t* n_dir, int32_t* und_out, int64_t* n_und);
+
 #ifdef __cplusplus
 }
 #endif

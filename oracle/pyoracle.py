@@ -99,6 +99,8 @@ def lib():
         L.orc_result_free.argtypes = [ct.c_void_p]
         L.orc_level_keys.argtypes = [dp, ct.c_int, ip, ip, ct.c_int, ct.c_double, ct.c_int64, ct.c_int64,
                                      ct.POINTER(ct.c_int64), ct.c_int]
+        L.orc_orient.argtypes = [ct.c_int, ct.POINTER(ct.c_uint8), ip, ct.POINTER(ct.c_int64), ip, ct.c_int, ip,
+                                 ct.c_int64, ip, ct.POINTER(ct.c_int64), ip, ct.POINTER(ct.c_int64)]
         _lib = L
     return _lib
 
@@ -344,3 +346,48 @@ def run_level(c: np.ndarray, offsets: np.ndarray, indices: np.ndarray, ell: int,
     _check(lib().orc_run_level(_dp(c), p, _ip(off), _ip(idx), ell, tau, ct.byref(cfg), row_begin,
                                p if row_end is None else row_end, ct.byref(st)))
     return LevelStats(st.level, st.ci_tests, st.pseudo_inverses, st.edges_removed, st.elapsed_s)
+
+
+# ---------------------------------------------------------------- orient.hpp
+class MixedGraph:
+    """orient.hpp:15-32: directed (from, to) pairs and undirected (a < b) pairs, ascending."""
+
+    def __init__(self, n: int, directed, undirected):
+        self.n = n
+        self.directed = sorted((int(a), int(b)) for a, b in directed)
+        self.undirected = sorted((min(int(a), int(b)), max(int(a), int(b))) for a, b in undirected)
+
+    def __eq__(self, other):
+        return (self.n, self.directed, self.undirected) == (other.n, other.directed, other.undirected)
+
+    def __repr__(self):
+        return f"MixedGraph(n={self.n}, directed={self.directed}, undirected={self.undirected})"
+
+
+def _sep_layout(n: int, sepsets: dict):
+    ns = n * (n - 1) // 2
+    lvl = np.full(max(ns, 1), -1, np.int32)
+    off = np.zeros(max(ns, 1), np.int64)
+    mem = []
+    for (i, j), s in sepsets.items():
+        a, b = min(i, j), max(i, j)
+        slot = a * (2 * n - a - 1) // 2 + (b - a - 1)
+        lvl[slot] = len(s)
+        off[slot] = len(mem)
+        mem.extend(int(v) for v in s)
+    return lvl, off, np.asarray(mem if mem else [0], np.int32)
+
+
+def orient(n: int, skeleton: np.ndarray, sepsets: dict, stage: int = 3, directed=()) -> MixedGraph:
+    """stage 1: find_v_structures, 2: apply_meek_rules (on skeleton + `directed`), 3: orient_skeleton."""
+    adj = np.ascontiguousarray(skeleton, np.uint8)
+    lvl, off, mem = _sep_layout(n, sepsets)
+    din = np.asarray(list(directed) if len(directed) else [(0, 0)], np.int32).reshape(-1, 2)
+    cap = max(n * (n - 1) // 2, 1)
+    dout = np.empty((cap, 2), np.int32)
+    uout = np.empty((cap, 2), np.int32)
+    nd, nu = ct.c_int64(), ct.c_int64()
+    _check(lib().orc_orient(n, adj.ctypes.data_as(ct.POINTER(ct.c_uint8)), _ip(lvl),
+                            off.ctypes.data_as(ct.POINTER(ct.c_int64)), _ip(mem), stage, _ip(din),
+                            len(directed), _ip(dout), ct.byref(nd), _ip(uout), ct.byref(nu)))
+    return MixedGraph(n, [tuple(r) for r in dout[:nd.value]], [tuple(r) for r in uout[:nu.value]])

@@ -28,7 +28,8 @@ __all__ = [
     "SeparationSets", "ZeroVarianceError", "LevelUnreachableError", "PcsError", "compute_correlation",
     "threshold_tau", "run_pc_stable", "run_pc_stable_data", "ci_test_batch", "pseudo_inverse_batch",
     "Session", "library", "LIB_PATH", "random_dag", "sample_linear_gaussian", "run_pc_stable_data_device",
-    "run_pc_stable_device", "correlation_device", "kernel_launches",
+    "run_pc_stable_device", "correlation_device", "kernel_launches", "MixedGraph", "find_v_structures",
+    "apply_meek_rules", "orient_skeleton",
 ]
 
 PKG_DIR = os.path.dirname(os.path.abspath(__file__))
@@ -86,7 +87,7 @@ class _Level(ct.Structure):
     _fields_ = [
         ("level", ct.c_int32), ("pad", ct.c_int32), ("ci_tests", ct.c_uint64), ("pseudo_inverses", ct.c_uint64),
         ("edges_removed", ct.c_uint64), ("elapsed_s", ct.c_double), ("device_ci_tests", ct.c_uint64),
-        ("device_pseudo_inverses", ct.c_uint64), ("kernel_ms", ct.c_double),
+        ("device_pseudo_inverses", ct.c_uint64), ("kernel_ms", ct.c_double), ("device_exact_tests", ct.c_uint64),
     ]
 
 
@@ -148,6 +149,16 @@ def library():
     L.pcs_session_level_end.argtypes = [vp]
     L.pcs_session_finish.argtypes = [vp, ct.POINTER(vp)]
     L.pcs_session_free.argtypes = [vp]
+    L.pcs_orient_records.argtypes = [ct.c_int32, ct.POINTER(ct.c_uint32), ip, ct.c_int64, ct.c_int32, ct.POINTER(vp)]
+    L.pcs_orient_skeleton.argtypes = [ct.c_int32, u8p, ip, ct.POINTER(ct.c_int64), ip, ct.c_int32, ip, ct.c_int64,
+                                      ct.POINTER(vp)]
+    L.pcs_mixed_directed_count.argtypes = [vp]
+    L.pcs_mixed_directed_count.restype = ct.c_int64
+    L.pcs_mixed_undirected_count.argtypes = [vp]
+    L.pcs_mixed_undirected_count.restype = ct.c_int64
+    L.pcs_mixed_directed.argtypes = [vp, ip]
+    L.pcs_mixed_undirected.argtypes = [vp, ip]
+    L.pcs_mixed_free.argtypes = [vp]
     _lib = L
     return L
 
@@ -221,6 +232,7 @@ class LevelStats:  # core.hpp:387-393 (+ device counters)
     device_ci_tests: int = 0
     device_pseudo_inverses: int = 0
     kernel_ms: float = 0.0
+    device_exact_tests: int = 0
 
 
 class AdjacencyMatrix:
@@ -264,6 +276,7 @@ class SeparationSets:
     def __init__(self, n: int, skeleton: AdjacencyMatrix, records: np.ndarray, levels: list):
         self.n = n
         self._skel = skeleton
+        self.records = np.ascontiguousarray(records, np.int32)  # (a, b, ell, members...) of levels >= 1
         self._blocks = []
         at = 0
         for lv in levels:
@@ -345,7 +358,8 @@ def _collect(h, with_sepsets: bool = True) -> SkeletonResult:
     lv = (_Level * 256)()
     n = L.pcs_result_levels(h, lv, 256)
     levels = [LevelStats(lv[k].level, lv[k].ci_tests, lv[k].pseudo_inverses, lv[k].edges_removed, lv[k].elapsed_s,
-                         lv[k].device_ci_tests, lv[k].device_pseudo_inverses, lv[k].kernel_ms) for k in range(n)]
+                         lv[k].device_ci_tests, lv[k].device_pseudo_inverses, lv[k].kernel_ms,
+                         lv[k].device_exact_tests) for k in range(n)]
     W = (p + 31) // 32
     bits = np.empty((p, W), np.uint32)
     L.pcs_result_bitmask(h, bits.ctypes.data_as(ct.POINTER(ct.c_uint32)))
@@ -612,3 +626,99 @@ class Session:
             self.close()
         except Exception:
             pass
+
+
+# ----------------------------------------------------------------- orientation (orient.hpp)
+class MixedGraph:
+    """orient.hpp:15-32: directed (from, to) and undirected (a < b) pairs."""
+
+    def __init__(self, n: int = 0, directed=(), undirected=()):
+        self.n = int(n)
+        self.directed = {(int(a), int(b)) for a, b in directed}
+        self.undirected = {(min(int(a), int(b)), max(int(a), int(b))) for a, b in undirected}
+
+    def has_directed(self, a: int, b: int) -> bool:
+        return (a, b) in self.directed
+
+    def has_undirected(self, a: int, b: int) -> bool:
+        return (min(a, b), max(a, b)) in self.undirected
+
+    def adjacent(self, a: int, b: int) -> bool:
+        return self.has_undirected(a, b) or self.has_directed(a, b) or self.has_directed(b, a)
+
+    def __eq__(self, other) -> bool:
+        return (isinstance(other, MixedGraph) and self.n == other.n and self.directed == other.directed
+                and self.undirected == other.undirected)
+
+    def __repr__(self) -> str:
+        return f"MixedGraph(n={self.n}, directed={sorted(self.directed)}, undirected={sorted(self.undirected)})"
+
+
+def _collect_mixed(h) -> MixedGraph:
+    L = library()
+    try:
+        nd, nu = L.pcs_mixed_directed_count(h), L.pcs_mixed_undirected_count(h)
+        d = np.empty((max(nd, 1), 2), np.int32)
+        u = np.empty((max(nu, 1), 2), np.int32)
+        L.pcs_mixed_directed(h, _ip(d))
+        L.pcs_mixed_undirected(h, _ip(u))
+    finally:
+        L.pcs_mixed_free(h)
+    return d[:nd], u[:nu]
+
+
+def _orient(skeleton, sepsets, stage: int, directed=()) -> MixedGraph:
+    L = library()
+    h = ct.c_void_p()
+    if isinstance(skeleton, AdjacencyMatrix) and isinstance(sepsets, SeparationSets) and stage != 2:
+        n = skeleton.n
+        if sepsets.n != n:
+            raise ValueError("find_v_structures: skeleton and sepsets sizes differ")
+        bits = np.ascontiguousarray(skeleton.bits, np.uint32)
+        rec = sepsets.records if len(sepsets.records) else np.zeros(1, np.int32)
+        rc = L.pcs_orient_records(n, bits.ctypes.data_as(ct.POINTER(ct.c_uint32)), _ip(rec), len(sepsets.records),
+                                  stage, ct.byref(h))
+    else:
+        cells = skeleton.cells if isinstance(skeleton, AdjacencyMatrix) else np.asarray(skeleton)
+        n = cells.shape[0]
+        adj = np.ascontiguousarray(cells != 0, np.uint8)
+        sep = sepsets.as_dict() if isinstance(sepsets, SeparationSets) else dict(sepsets or {})
+        if isinstance(sepsets, SeparationSets) and sepsets.n != n:
+            raise ValueError("find_v_structures: skeleton and sepsets sizes differ")
+        ns = max(n * (n - 1) // 2, 1)
+        lvl = np.full(ns, -1, np.int32)
+        off = np.zeros(ns, np.int64)
+        mem = []
+        for (i, j), st in sep.items():
+            a, b = min(i, j), max(i, j)
+            slot = a * (2 * n - a - 1) // 2 + (b - a - 1)
+            lvl[slot] = len(st)
+            off[slot] = len(mem)
+            mem.extend(int(v) for v in st)
+        mem = np.asarray(mem if mem else [0], np.int32)
+        din = np.asarray(list(directed) if len(directed) else [(0, 0)], np.int32).reshape(-1, 2)
+        rc = L.pcs_orient_skeleton(n, adj.ctypes.data_as(ct.POINTER(ct.c_uint8)), _ip(lvl),
+                                   off.ctypes.data_as(ct.POINTER(ct.c_int64)), _ip(mem), stage, _ip(din),
+                                   len(directed), ct.byref(h))
+    if rc:
+        _raise(rc)
+    d, u = _collect_mixed(h)
+    return MixedGraph(n, map(tuple, d.tolist()), map(tuple, u.tolist()))
+
+
+def find_v_structures(skeleton, sepsets) -> MixedGraph:
+    """orient.hpp:40-89 (unshielded-triple votes on the device)."""
+    return _orient(skeleton, sepsets, 1)
+
+
+def apply_meek_rules(g: MixedGraph) -> MixedGraph:
+    """orient.hpp:147-167 (the reference's visiting order, on the host)."""
+    adj = np.zeros((g.n, g.n), np.uint8)
+    for a, b in list(g.directed) + list(g.undirected):
+        adj[a, b] = adj[b, a] = 1
+    return _orient(adj, None, 2, directed=sorted(g.directed))
+
+
+def orient_skeleton(skeleton, sepsets) -> MixedGraph:
+    """orient.hpp:170-173: v-structures then the Meek rules."""
+    return _orient(skeleton, sepsets, 3)

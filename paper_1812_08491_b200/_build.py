@@ -25,6 +25,7 @@ UNITS = {
     "corr.cu": [],
     "host.cu": [],
     "probe.cu": [],
+    "orient.cu": [],
 }
 
 

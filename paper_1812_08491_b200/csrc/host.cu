@@ -12,6 +12,7 @@
 #include <chrono>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -326,6 +327,11 @@ LevelArgs level_args(pcs_session* s) {
     A.binom.stride = s->binom_stride;
     A.th = s->th;
     A.cnt = s->dCnt;
+    static const int filter = [] {
+        const char* e = std::getenv("PCS_FILTER");
+        return e ? std::atoi(e) : 1;
+    }();
+    A.filter = filter;
     return A;
 }
 
@@ -336,10 +342,14 @@ void stop(pcs_session* s, int reason) {
 
 }  // namespace
 
+namespace pcs {
+void set_last_error(const std::string& msg) { g_err = msg; }
+}  // namespace pcs
+
 // ================================================================ C ABI
 extern "C" {
 
-const char* pcs_version(void) { return "pcstable_b200 0.1 (sm_100a, abi 1)"; }
+const char* pcs_version(void) { return "pcstable_b200 0.2 (sm_100a, abi 2)"; }
 const char* pcs_last_error(void) { return g_err.c_str(); }
 
 void pcs_config_default(pcs_config* cfg) {  // core.hpp:357-368
@@ -588,6 +598,7 @@ pcs_status pcs_session_level_end(pcs_session* s) {
         L.pseudo_inverses = c.ci_serial;  // skeleton.hpp:151-152
         L.device_ci_tests = c.gpu_tests;
         L.device_pseudo_inverses = c.gpu_pinv;
+        L.device_exact_tests = c.gpu_exact;
         if (c.rec_count) {
             s->recLevels.push_back({s->ell, s->recUsed, (long long)c.rec_count});
             s->recUsed += (long long)c.rec_count * (2 + s->ell);

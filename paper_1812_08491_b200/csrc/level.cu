@@ -673,6 +673,7 @@ __global__ void __launch_bounds__(kSetWarps * 32, 3) level_set_kernel(LevelArgs 
         }
     }
     add_counter(&A.cnt->gpu_tests, tests);
+    add_counter(&A.cnt->gpu_exact, tests);  // every test is evaluated in the reference's operation order
     if (lane == 0 && pinvs) atomicAdd(&A.cnt->gpu_pinv, pinvs);
     if (nan) atomicOr(&A.cnt->err_nan, 1);
 }

@@ -2,6 +2,7 @@
 // the kernel translation units (level.cu, corr.cu).  Not part of the ABI.
 #pragma once
 #include <cstdint>
+#include <string>
 #include <cuda_runtime.h>
 
 #include "pcs_device.cuh"
@@ -10,6 +11,8 @@ namespace pcs {
 
 // number of kernels this library has launched (diagnostics: bench.py's gpu_launches)
 extern unsigned long long g_kernel_launches;
+// message returned by pcs_last_error() (host.cu)
+void set_last_error(const std::string& msg);
 
 constexpr int kMaxTemplLevel = 8;  // ell handled by register-resident templates
 
@@ -19,6 +22,7 @@ struct Counters {
     unsigned long long removed;     // edges removed
     unsigned long long gpu_tests;   // CI tests executed on the device
     unsigned long long gpu_pinv;    // pseudo-inverses executed on the device
+    unsigned long long gpu_exact;   // tests re-evaluated in reference order (filter could not certify)
     unsigned long long rec_count;   // sepset records written
     unsigned long long units[2];    // persistent-grid work cursors (pass A / B)
     int err_nan;                    // fisher_z would throw (NaN statistic)
@@ -51,6 +55,7 @@ struct LevelArgs {
     BinomTable binom;
     Thresholds th;
     Counters* cnt;
+    int filter;  // 1: cuPC-S may use the certified FMA filter (PCS_FILTER=0 disables; results identical)
 };
 
 // ---- corr.cu

@@ -170,6 +170,83 @@ static void test_against_oracle(Index p, double d, Index m, std::uint64_t seed, 
     EXPECT(rd.levels_run() >= 1);
 }
 
+// test_orient.cpp:25-181, written against the drop-in's orient API
+static AdjacencyMatrix make_skeleton(Index n, std::vector<std::pair<Index, Index>> edges) {
+    AdjacencyMatrix a(n);
+    for (auto [i, j] : edges) a.set_edge(i, j);
+    return a;
+}
+
+static void test_orientation() {
+    {
+        const AdjacencyMatrix skel = make_skeleton(3, {{0, 2}, {1, 2}});
+        SeparationSets sepsets(3);
+        sepsets.store(0, 1, {});
+        MixedGraph expected;
+        expected.n = 3;
+        expected.directed = {{0, 2}, {1, 2}};
+        EXPECT(find_v_structures(skel, sepsets) == expected);
+        sepsets.store(0, 1, {2});
+        expected.directed.clear();
+        expected.undirected = {{0, 2}, {1, 2}};
+        EXPECT(find_v_structures(skel, sepsets) == expected);
+        EXPECT_THROW(find_v_structures(skel, SeparationSets(3)), std::invalid_argument);
+        EXPECT_THROW(find_v_structures(skel, SeparationSets(4)), std::invalid_argument);
+    }
+    {
+        const AdjacencyMatrix skel = make_skeleton(4, {{0, 1}, {1, 2}, {0, 3}});
+        SeparationSets sepsets(4);
+        sepsets.store(0, 2, {});
+        sepsets.store(1, 3, {});
+        const MixedGraph g = find_v_structures(skel, sepsets);
+        EXPECT(g.has_undirected(0, 1) && g.has_directed(2, 1) && g.has_directed(3, 0));
+    }
+    {
+        MixedGraph g;
+        g.n = 4;
+        g.directed = {{2, 1}, {3, 1}};
+        g.undirected = {{0, 1}, {0, 2}, {0, 3}};
+        MixedGraph expected;
+        expected.n = 4;
+        expected.directed = {{0, 1}, {2, 1}, {3, 1}};
+        expected.undirected = {{0, 2}, {0, 3}};
+        const MixedGraph once = apply_meek_rules(g);
+        EXPECT(once == expected);
+        EXPECT(apply_meek_rules(once) == once);
+        g.directed = {{2, 3}, {3, 1}};
+        g.undirected = {{0, 1}, {0, 2}};
+        expected.directed = {{0, 1}, {2, 3}, {3, 1}};
+        expected.undirected = {{0, 2}};
+        EXPECT(apply_meek_rules(g) == expected);
+    }
+    {
+        const AdjacencyMatrix skel = make_skeleton(4, {{0, 1}, {1, 2}, {2, 3}});
+        SeparationSets sepsets(4);
+        sepsets.store(0, 2, {});
+        sepsets.store(1, 3, {2});
+        MixedGraph expected;
+        expected.n = 4;
+        expected.directed = {{0, 1}, {2, 1}};
+        expected.undirected = {{2, 3}};
+        EXPECT(orient_skeleton(skel, sepsets) == expected);
+    }
+    {
+        // OrientSkeleton.PreservesTheSkeletonExactly on a device skeleton (test_orient.cpp:183-202)
+        std::vector<double> w(12 * 12);
+        orc_random_dag(12, 0.25, 5, w.data());
+        std::vector<double> x(12 * 800);
+        orc_sample_linear_gaussian(w.data(), 12, 800, 6, x.data());
+        const SkeletonResult r = run_pc_stable(DataMatrix(800, 12, x), SkeletonConfig{});
+        const MixedGraph g = orient_skeleton(r.skeleton, r.sepsets);
+        EXPECT(g.n == 12);
+        EXPECT(g.directed.size() + g.undirected.size() == r.skeleton.edge_count());
+        for (Index i = 0; i < 12; ++i)
+            for (Index j = i + 1; j < 12; ++j) EXPECT(g.adjacent(i, j) == r.skeleton.at(i, j));
+        for (const auto& [a, b] : g.directed) EXPECT(!g.has_directed(b, a) && !g.has_undirected(a, b));
+        for (const auto& [a, b] : g.undirected) EXPECT(a < b);
+    }
+}
+
 int main() {
     const std::vector<std::pair<std::string, std::function<void()>>> tests = {
         {"star_graph_set", [] { test_star_graph(Strategy::SetShared); }},
@@ -181,6 +258,7 @@ int main() {
         {"oracle_p50_set", [] { test_against_oracle(50, 0.2, 1000, 7919, Strategy::SetShared); }},
         {"oracle_p100_edge", [] { test_against_oracle(100, 2.0 / 99.0, 1000, 0, Strategy::EdgeParallel); }},
         {"oracle_p120_set", [] { test_against_oracle(120, 0.1, 500, 15838, Strategy::SetShared); }},
+        {"orientation", test_orientation},
     };
     for (const auto& [name, fn] : tests) {
         const int before = g_failed;

@@ -1,5 +1,6 @@
 """Per-level workload of the BASELINE configs on the device (diagnostics, not a bench).
-usage: python tools/explore.py C2[,C3] [set|edge] [max_level]"""
+usage: python tools/explore.py C2[,C3] [set|edge] [max_level|-1] [repeats]
+(only the last repeat is printed: earlier ones warm up module loading and caches)"""
 import sys, time, os
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np
@@ -14,14 +15,16 @@ CONFIGS = {
 }
 names = sys.argv[1].split(",") if len(sys.argv) > 1 else list(CONFIGS)
 strategies = sys.argv[2].split(",") if len(sys.argv) > 2 else ["set"]
-max_level = int(sys.argv[3]) if len(sys.argv) > 3 else None
+max_level = int(sys.argv[3]) if len(sys.argv) > 3 and int(sys.argv[3]) >= 0 else None
+repeats = int(sys.argv[4]) if len(sys.argv) > 4 else 1
 for name in names:
     p, m, d, k = CONFIGS[name]
     seed = 7919 * k
     w = pcs.random_dag(p, d, seed)
     x = pcs.sample_linear_gaussian(w, m, seed + 1)
     c = pcs.compute_correlation(x)
-    for strat in strategies:
+    for strat, rep in [(st, r) for st in strategies for r in range(repeats)]:
+        quiet = rep < repeats - 1
         cfg = pcs.SkeletonConfig(alpha=0.01, strategy=pcs.Strategy(strat), max_level=max_level)
         s = pcs.Session(c, m, cfg)
         t0 = time.time()
@@ -35,10 +38,10 @@ for name in names:
             s.level_end()
             r = s.finish(with_sepsets=False)
             l = r.levels[-1]
-            print(f"{name} {strat} L{l.level}: keys={nk} serial_tests={l.ci_tests:.3e} dev_tests={l.device_ci_tests:.3e} "
-                  f"dev_pinv={l.device_pseudo_inverses:.3e} removed={l.edges_removed} elapsed={l.elapsed_s*1e3:.2f}ms "
+            if not quiet: print(f"{name} {strat} L{l.level}: keys={nk} serial_tests={l.ci_tests:.3e} dev_tests={l.device_ci_tests:.3e} "
+                  f"dev_pinv={l.device_pseudo_inverses:.3e} exact={l.device_exact_tests:.3e} removed={l.edges_removed} elapsed={l.elapsed_s*1e3:.2f}ms "
                   f"kernel={l.kernel_ms:.2f}ms edges_left={r.skeleton.edge_count()} "
                   f"rate={l.device_ci_tests / max(l.kernel_ms, 1e-9) * 1e3:.3e}/s", flush=True)
         r = s.finish(with_sepsets=False)
         s.close()
-        print(f"{name} {strat} total {time.time() - t0:.3f}s levels={r.levels_run()} stop={r.stop_reason.value}", flush=True)
+        if not quiet: print(f"{name} {strat} total {time.time() - t0:.3f}s levels={r.levels_run()} stop={r.stop_reason.value}", flush=True)

@@ -16,7 +16,7 @@ for s in $STEPS; do
       timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $OUT/smoke.log 2>&1; echo "smoke rc=$?" >> $OUT/smoke.log
       ;;
     explore)
-      timeout 600 python tools/explore.py C1,C3,C4 set,edge > $OUT/explore.log 2>&1
+      timeout 600 python tools/explore.py C1,C3,C4 set,edge -1 2 > $OUT/explore.log 2>&1
       timeout 600 python tools/explore.py C2 set 3 >> $OUT/explore.log 2>&1
       ;;
     c2)

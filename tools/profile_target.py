@@ -21,6 +21,9 @@ while True:
         s.set_shard(0, slices)
         s.level_pass(0)
         s.keys()
-        print("profiled level", ell, "keys", nk)
+        s.level_end()
+        l = s.finish(with_sepsets=False).levels[-1]
+        print("profiled level", ell, "keys", nk, "device tests", l.device_ci_tests, "exact", l.device_exact_tests,
+              "pinv", l.device_pseudo_inverses, "kernel_ms", l.kernel_ms)
         break
     s.level_pass(0); s.level_pass(1); s.level_end()
