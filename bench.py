@@ -212,6 +212,7 @@ def main():
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-secondary", action="store_true", help="skip the full C3/C4 runs reported beside the line")
     ap.add_argument("--verbose", action="store_true")
     args = ap.parse_args()
     name = args.workload
@@ -322,6 +323,37 @@ def main():
                "d2h_bytes_per_step": 4 * p * ((p + 31) // 32) + 4 * rec_ints + 72 * len(r.levels),
                "s_per_step": statistics.mean(et), "removed_pairs": sep_n}
 
+    # full (uncapped) runs of the other single-GPU BASELINE shapes, same device timing
+    secondary = []
+    if world == 1 and not args.no_secondary:
+        for sname in ("C3", "C4"):
+            if sname == name:
+                continue
+            swl = dict(WORKLOADS[sname])
+            sseed = 7919 * swl["case"]
+            sx = pcs.sample_linear_gaussian(pcs.random_dag(swl["p"], swl["d"], sseed), swl["m"], sseed + 1)
+            sx_dev = torch.from_numpy(np.ascontiguousarray(sx.T)).to(f"cuda:{dev}")
+            scfg = pcs.SkeletonConfig(alpha=swl["alpha"], max_level=swl["max_level"], strategy=cfg.strategy,
+                                      device=dev, stream=stream.cuda_stream)
+            st = []
+            with torch.cuda.stream(stream):
+                for k in range(2 + args.steps):
+                    flush.zero_()
+                    e0 = torch.cuda.Event(enable_timing=True)
+                    e1 = torch.cuda.Event(enable_timing=True)
+                    e0.record(stream)
+                    sr = pcs.run_pc_stable_data_device(sx_dev.data_ptr(), swl["m"], swl["p"], scfg)
+                    e1.record(stream)
+                    stream.synchronize()
+                    if k >= 2:
+                        st.append(e0.elapsed_time(e1))
+            sms = statistics.mean(st)
+            stests = sum(l.ci_tests for l in sr.levels)
+            secondary.append({"workload": describe(sname, swl), "skeleton_wall_s": sms * 1e-3,
+                              "value": stests / (sms * 1e-3), "unit": "tests/s", "serial_ci_tests": stests,
+                              "levels_run": sr.levels_run(), "stop_reason": sr.stop_reason.value,
+                              "edges_left": sr.skeleton.edge_count(), "steps": args.steps, "warmup": 2})
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         threads = os.cpu_count() or 1
@@ -349,6 +381,7 @@ def main():
                 "timing": "CUDA events on the library's stream per step, max over ranks",
             },
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
+            "secondary": secondary,
             "clocks": clk.summary(),
         }
         print(json.dumps(line), flush=True)

@@ -16,6 +16,7 @@ CSRC = os.path.join(PKG, "csrc")
 ROOT = os.path.dirname(PKG)
 LIB = os.path.join(PKG, "libpcstable_b200.so")
 BUILD = os.path.join(PKG, "build")
+CLI = os.path.join(PKG, "pcstable_b200")
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xptxas", "-v",
@@ -79,6 +80,15 @@ def build(verbose: bool = False, force: bool = False) -> str:
         if res.returncode != 0:
             sys.stderr.write(res.stderr)
             raise RuntimeError("link failed")
+    # the reference CLI (pcstable_main.cpp) on the device path: host C++20 over the drop-in header
+    cli_src = os.path.join(PKG, "cli", "pcstable_b200.cpp")
+    if force or _stale(CLI, [cli_src, LIB, os.path.join(ROOT, "include", "pcstable_b200.hpp")]):
+        cmd = ["g++", "-std=c++20", "-O2", "-Wall", "-Wextra", "-I", os.path.join(ROOT, "include"), cli_src, LIB,
+               "-Wl,-rpath,$ORIGIN", "-o", CLI]
+        res = subprocess.run(cmd, capture_output=True, text=True)
+        if res.returncode != 0:
+            sys.stderr.write(res.stderr)
+            raise RuntimeError("g++ failed for cli/pcstable_b200.cpp")
     return LIB
 
 

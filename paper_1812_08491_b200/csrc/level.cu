@@ -413,11 +413,12 @@ void launch_level1(const LevelArgs& A, int pass, const unsigned long long* prefi
 // (keys only decrease, ranks only increase) and advances the work cursor past the
 // row.
 template <int L>
-struct SetSlot {
-    double minv[L * L];
-    double ciS[L];
-    double p0[L];
-    double h00;
+struct alignas(16) SetSlot {
+    // column c of the set's test data, 16 B aligned for LDS.128:
+    //   {M2^+[0][c], ..., M2^+[L-1][c], C(i,S)[c], P0[c], (pad)}
+    static constexpr int CW = (L + 3) / 2 * 2;
+    double col[L][CW];
+    double h00, pad;
     int pos[L];
     int roff[L];  // row offsets mem[a] * ldc of the set's members
 };
@@ -440,15 +441,67 @@ struct SetWarpSmem {
     int te[SetCfg<L>::kStage];
 };
 
+// h_terms<L> (stats.hpp:292-307) for NT targets against one shared set, streamed one column
+// of M2^+ at a time: P1[col] is consumed as soon as it exists, so only one column of M2^+
+// (plus C(i,S)[col], P0[col]) is live.  Every accumulator (P1[col], d11, d01, d10) sees
+// exactly the reference's sequence of roundings (-fmad=false), so h01 / denom are
+// bit-identical to h_terms<L>.
+template <int L, int NT, int LP>
+__device__ __forceinline__ void h_terms_stream(const SetSlot<L>& sl, const double (&cp)[NT][LP],
+                                               const double (&cur)[NT], const double (&cij)[NT],
+                                               double (&h01)[NT], double (&den)[NT]) {
+    double d11[NT], d01[NT], d10[NT];
+#pragma unroll
+    for (int col = 0; col < L; ++col) {
+        double cv[SetSlot<L>::CW];  // one column: M2^+[.][col], C(i,S)[col], P0[col]
+#pragma unroll
+        for (int k = 0; k < SetSlot<L>::CW; k += 2) {
+            const double2 v = *reinterpret_cast<const double2*>(&sl.col[col][k]);
+            cv[k] = v.x;
+            cv[k + 1] = v.y;
+        }
+        const double* mc = cv;
+        const double ci = cv[L], pc = cv[L + 1];
+#pragma unroll
+        for (int t = 0; t < NT; ++t) {
+            double x[L];
+#pragma unroll
+            for (int a = 0; a < L - 1; ++a) x[a] = cp[t][a];
+            x[L - 1] = cur[t];
+            double pcol = x[0] * mc[0];
+#pragma unroll
+            for (int k = 1; k < L; ++k) pcol = pcol + x[k] * mc[k];
+            if (col == 0) {
+                d11[t] = pcol * x[0];
+                d01[t] = pc * x[0];
+                d10[t] = pcol * ci;
+            } else {
+                d11[t] = d11[t] + pcol * x[col];
+                d01[t] = d01[t] + pc * x[col];
+                d10[t] = d10[t] + pcol * ci;
+            }
+        }
+    }
+    const double h00 = sl.h00;
+#pragma unroll
+    for (int t = 0; t < NT; ++t) {
+        const double h11 = 1.0 - d11[t];
+        h01[t] = cij[t] - 0.5 * (d01[t] + d10[t]);
+        den[t] = h00 * h11;
+    }
+}
+
 // Phase 2 for one staged batch of targets, NT (<= SetCfg<L>::NT) per lane.
-// segmask: bit s set when set s starts a new run of equal leading L-1 members.
+// segmask: bit s set when set s starts a new run of equal leading L-1 members.  Inside a
+// run (lexicographic order) the last member's position advances by one per set: set
+// sg0 + d has last position base + d, so "target is a member" is one compare per set.
 template <int L, int NT>
 __device__ __forceinline__ void set_sweep(const LevelArgs& A, SetWarpSmem<L>& S, int lane, int nlive, int nvalid,
                                           unsigned segmask, unsigned long long K0, unsigned long long& tests,
                                           int& nan) {
     const double* __restrict__ C = A.C;
     const double hi2 = A.th.hi2;
-    int tq[NT], te[NT], rel[NT];
+    int rel[NT];           // tested while the set index is below rel (relative key)
     const double* Cj[NT];  // C + j: gathers C(mem, j) = Cj[t][mem * ldc] (one IMAD.WIDE each)
     double cij[NT];
 #pragma unroll
@@ -457,21 +510,17 @@ __device__ __forceinline__ void set_sweep(const LevelArgs& A, SetWarpSmem<L>& S,
         if (k < nlive) {
             const unsigned long long d = S.tkey[k] - K0;  // > 0 (staged targets are live)
             rel[t] = d > 0x3fffffffull ? 0x3fffffff : (int)d;
-            tq[t] = S.tq[k];
             Cj[t] = C + S.tj[k];
-            te[t] = S.te[k];
             cij[t] = S.tcij[k];
         } else {
             rel[t] = -1;
-            tq[t] = -1;
             Cj[t] = C;  // valid address: loads stay unconditional
-            te[t] = 0;
             cij[t] = 0.0;
         }
     }
     constexpr int LP = L > 1 ? L - 1 : 1;
     double cp[NT][LP];
-    double nxt[NT];
+    double nxt[NT], alt[NT];
     {
         const int ro = S.slot[0].roff[L - 1];
 #pragma unroll
@@ -481,58 +530,48 @@ __device__ __forceinline__ void set_sweep(const LevelArgs& A, SetWarpSmem<L>& S,
     segmask &= valid_mask;
     int sg = 0;
     while (sg < nvalid) {
-        // new run of sets sharing their first L-1 members: gather those once per target
+        const int sg0 = sg;
+        const unsigned later = segmask & ~((2u << sg0) - 1u);
+        const int seg_end = later ? __ffs(later) - 1 : nvalid;
+        int lim[NT], dm[NT];  // lim: tested while sg < lim; dm: the set whose last member is the target
+        unsigned hit = 0;     // bit t: target t found its separating set in this run (at set lim[t])
         {
-            const SetSlot<L>& sl = S.slot[sg];
+            // new run of sets sharing their first L-1 members: gather those once per target
+            const SetSlot<L>& sl = S.slot[sg0];
+            const int base = sl.pos[L - 1];
 #pragma unroll
             for (int a = 0; a < L - 1; ++a) {
                 const int ro = sl.roff[a];
 #pragma unroll
                 for (int t = 0; t < NT; ++t) cp[t][a] = __ldg(Cj[t] + ro);
             }
-        }
-        const unsigned later = segmask & ~((2u << sg) - 1u);
-        const int seg_end = later ? __ffs(later) - 1 : nvalid;
-        for (; sg < seg_end; ++sg) {
-            const SetSlot<L>& sl = S.slot[sg];
-            double cur[NT];
-#pragma unroll
-            for (int t = 0; t < NT; ++t) cur[t] = nxt[t];
-            {  // prefetch the next set's last-member gathers (clamped: always a valid slot)
-                const int ro = S.slot[min(sg + 1, nvalid - 1)].roff[L - 1];
-#pragma unroll
-                for (int t = 0; t < NT; ++t) nxt[t] = __ldg(Cj[t] + ro);
-            }
-            double minv[L * L], ciS[L], p0[L];
-            int pos[L];
-#pragma unroll
-            for (int q = 0; q < L * L; ++q) minv[q] = sl.minv[q];
-#pragma unroll
-            for (int a = 0; a < L; ++a) {
-                ciS[a] = sl.ciS[a];
-                p0[a] = sl.p0[a];
-                pos[a] = sl.pos[a];
-            }
-            const double h00 = sl.h00;
-            double h01[NT], den[NT];
 #pragma unroll
             for (int t = 0; t < NT; ++t) {
-                double cjS[L];
+                const int k = t * 32 + lane;
+                const int q = k < nlive ? S.tq[k] : -1;
+                bool pm = false;
 #pragma unroll
-                for (int a = 0; a < L - 1; ++a) cjS[a] = cp[t][a];
-                cjS[L - 1] = cur[t];
-                h_terms<L>(minv, ciS, p0, h00, cjS, cij[t], h01[t], den[t]);
+                for (int a = 0; a < L - 1; ++a) pm |= sl.pos[a] == q;
+                lim[t] = pm ? -1 : rel[t];  // a shared member is never tested in this run
+                dm[t] = sg0 + q - base;
             }
-            // branch-free common path: count the valid tests, flag the (rare) possible hits
+        }
+        // double-buffered last-member gathers: step(sg, cur, next) tests set sg with `cur` while
+        // prefetching set sg+1 into `next` (no register copies between steps)
+        auto step = [&](int sgx, const double (&cur)[NT], double (&pre)[NT]) {
+            const SetSlot<L>& sl = S.slot[sgx];
+            {  // prefetch the next set's last-member gathers (clamped: always a valid slot)
+                const int ro = S.slot[min(sgx + 1, nvalid - 1)].roff[L - 1];
+#pragma unroll
+                for (int t = 0; t < NT; ++t) pre[t] = __ldg(Cj[t] + ro);
+            }
+            double h01[NT], den[NT];
+            h_terms_stream<L, NT, LP>(sl, cp, cur, cij, h01, den);
+            // branch-free common path: flag the (rare) tests not certainly dependent
             unsigned cand = 0;
 #pragma unroll
-            for (int t = 0; t < NT; ++t) {
-                bool v = rel[t] > sg;
-#pragma unroll
-                for (int a = 0; a < L; ++a) v = v && pos[a] != tq[t];
-                tests += v;
-                cand |= (unsigned)(v && !surely_dependent(h01[t], den[t], hi2)) << t;
-            }
+            for (int t = 0; t < NT; ++t)
+                cand |= (unsigned)((sgx < lim[t]) & (sgx != dm[t]) & !surely_dependent(h01[t], den[t], hi2)) << t;
             if (__any_sync(0xffffffffu, cand)) {
 #pragma unroll
                 for (int t = 0; t < NT; ++t) {
@@ -540,12 +579,32 @@ __device__ __forceinline__ void set_sweep(const LevelArgs& A, SetWarpSmem<L>& S,
                         const int d = decide_fast(h01[t], den[t], A.th);
                         if (d != kDependent) {
                             if (d == kNanError) nan = 1;
-                            else atomicMin(A.keys + te[t], K0 + (unsigned long long)sg);
-                            rel[t] = sg;
+                            else atomicMin(A.keys + S.te[t * 32 + lane], K0 + (unsigned long long)sgx);
+                            rel[t] = sgx;
+                            lim[t] = sgx;
+                            hit |= 1u << t;
                         }
                     }
                 }
             }
+        };
+        while (sg < seg_end) {
+            step(sg, nxt, alt);
+            ++sg;
+            if (sg == seg_end) {
+#pragma unroll
+                for (int t = 0; t < NT; ++t) nxt[t] = alt[t];
+                break;
+            }
+            step(sg, alt, nxt);
+            ++sg;
+        }
+        // tests of this run, per target: sets [sg0, hi) minus the member set (serial order)
+#pragma unroll
+        for (int t = 0; t < NT; ++t) {
+            const int hi = ((hit >> t) & 1u) ? lim[t] + 1 : min(seg_end, lim[t]);
+            const int n = max(0, hi - sg0);
+            tests += (unsigned)(n - (dm[t] >= sg0 && dm[t] < sg0 + n ? 1 : 0));
         }
     }
 }
@@ -628,11 +687,14 @@ __global__ void __launch_bounds__(kSetWarps * 32, 3) level_set_kernel(LevelArgs 
                     p0_terms<L>(minv, ciS, p0, h00);
                     SetSlot<L>& sl = S.slot[lane];
 #pragma unroll
-                    for (int q = 0; q < L * L; ++q) sl.minv[q] = minv[q];
+                    for (int c = 0; c < L; ++c) {
+#pragma unroll
+                        for (int k = 0; k < L; ++k) sl.col[c][k] = minv[k * L + c];
+                        sl.col[c][L] = ciS[c];
+                        sl.col[c][L + 1] = p0[c];
+                    }
 #pragma unroll
                     for (int a = 0; a < L; ++a) {
-                        sl.ciS[a] = ciS[a];
-                        sl.p0[a] = p0[a];
                         sl.pos[a] = pos[a];
                         sl.roff[a] = mem[a] * (int)ldc;  // p * ldc < 2^31 (p <= 46340)
                     }

@@ -263,13 +263,18 @@ __device__ __forceinline__ int decide_fast(double h01, double denom, const Thres
     return decide_exact(h01, denom, th.tau);
 }
 
-// Branch-free common-case filter: true only when decide_exact() is certainly
-// kDependent (rho^2 provably above the upper band; NaN / degenerate / tiny
-// denominators fall through to decide_fast()).  With denom >= 1e-250 and
-// hi2 >= tanh(tau)^2 > 1e-4 the product is a normal number, so both sides carry
-// at most one rounding and the 1e-9 band dominates.
+// Branch-free common-case filter: true only when decide_fast() is certainly
+// kDependent.  If denom <= 0 (or NaN) decide_fast() returns kDependent anyway.
+// Otherwise g = RN(denom*hi2 + 1e-240) >= RN(denom*hi2) (monotone rounding), so
+// h01^2 >= g gives decide_fast()'s "A >= denom*hi2" branch when denom >= 1e-250;
+// when 0 < denom < 1e-250, A >= 1e-240 makes |rho| = |h01|/sqrt(denom) >= 1e5,
+// clamped to 1-1e-12, whose z exceeds every tau with a finite hi2 (hi2 is +inf
+// when tau reaches the clamp's z: then g = +inf and nothing is certified).
+// NaN h01 -> false.  denom <= 0 is the degenerate branch (stats.hpp:301-305),
+// dependent whatever h01 is -- frequent on rank-truncated inputs (C2), so it is
+// certified here rather than in the divergent slow path.
 __device__ __forceinline__ bool surely_dependent(double h01, double denom, double hi2) {
-    return (denom >= 1e-250) & (h01 * h01 >= denom * hi2);
+    return (h01 * h01 >= fma(denom, hi2, 1e-240)) | (denom <= 0.0);
 }
 
 // Level-0 decision on rho = clamp(c_ij) (stats.hpp:309-312).

@@ -31,7 +31,7 @@ for s in $STEPS; do
       ;;
     ncu)
       timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/launches.csv \
-        python bench.py --steps 1 --warmup 0 --no-cpu-baseline --no-e2e > $OUT/ncu_bench.log 2>&1
+        python bench.py --steps 1 --warmup 0 --no-cpu-baseline --no-e2e --no-secondary > $OUT/ncu_bench.log 2>&1
       timeout 900 ncu --set full --clock-control none --import-source on -k regex:level_set --launch-skip 2 -c 1 -f -o $OUT/top \
         python tools/profile_target.py 3 32 set > $OUT/ncu_full.log 2>&1
       ;;
