@@ -12,6 +12,7 @@
 #include <chrono>
 #include <cmath>
 #include <cstdio>
+#include <cstdarg>
 #include <cstdlib>
 #include <cstring>
 #include <string>
@@ -37,6 +38,21 @@ pcs_status fail(pcs_status st, const std::string& msg) {
         if (e_ != cudaSuccess)                                                              \
             return fail(PCS_ECUDA, std::string(#expr) + ": " + cudaGetErrorString(e_));     \
     } while (0)
+
+// PCS_TRACE=1: per-phase host timings on stderr (observability; no effect on results)
+void trace(const char* fmt, ...) {
+    static const bool on = [] {
+        const char* e = std::getenv("PCS_TRACE");
+        return e && *e && *e != '0';
+    }();
+    if (!on) return;
+    va_list ap;
+    va_start(ap, fmt);
+    std::fprintf(stderr, "[pcs] ");
+    std::vfprintf(stderr, fmt, ap);
+    std::fprintf(stderr, "\n");
+    va_end(ap);
+}
 
 double now_s() {
     return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
@@ -197,13 +213,19 @@ namespace {
 void free_session(pcs_session* s) {
     if (!s) return;
     cudaSetDevice(s->device);
+    // stream-ordered frees back into the device pool (no implicit device synchronisation)
+    auto rel = [&](void* ptr) {
+        if (!ptr) return;
+        if (s->st) cudaFreeAsync(ptr, s->st);
+        else cudaFree(ptr);
+    };
+    if (s->own_c) rel(s->dC);
+    rel(s->dAdj); rel(s->dDeg); rel(s->dLow); rel(s->dOff); rel(s->dUp);
+    rel(s->dInfo); rel(s->dCnt); rel(s->dPrefix); rel(s->dNbr); rel(s->dEid);
+    rel(s->dEuA); rel(s->dEuQa); rel(s->dEuQb); rel(s->dKeys); rel(s->dRec);
+    rel(s->dBinom);
+    rel(s->dScratch);
     if (s->st) cudaStreamSynchronize(s->st);
-    if (s->own_c) cudaFree(s->dC);
-    cudaFree(s->dAdj); cudaFree(s->dDeg); cudaFree(s->dLow); cudaFree(s->dOff); cudaFree(s->dUp);
-    cudaFree(s->dInfo); cudaFree(s->dCnt); cudaFree(s->dPrefix); cudaFree(s->dNbr); cudaFree(s->dEid);
-    cudaFree(s->dEuA); cudaFree(s->dEuQa); cudaFree(s->dEuQb); cudaFree(s->dKeys); cudaFree(s->dRec);
-    cudaFree(s->dBinom);
-    cudaFree(s->dScratch);
     if (s->ev_begin) cudaEventDestroy(s->ev_begin);
     if (s->ev_end) cudaEventDestroy(s->ev_end);
     if (s->ev_k0) cudaEventDestroy(s->ev_k0);
@@ -228,11 +250,25 @@ pcs_status validate_config(const pcs_config* c) {  // core.hpp:370-383
 }
 
 template <class T>
-pcs_status realloc_dev(T** ptr, long long n) {
-    cudaFree(*ptr);
+pcs_status realloc_dev(pcs_session* s, T** ptr, long long n) {
+    if (*ptr) cudaFreeAsync(*ptr, s->st);
     *ptr = nullptr;
-    CUDA_TRY(cudaMalloc(ptr, sizeof(T) * (size_t)std::max<long long>(n, 1)));
+    CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(ptr), sizeof(T) * (size_t)std::max<long long>(n, 1), s->st));
     return PCS_OK;
+}
+
+// Device buffers come from the stream-ordered pool: frees do not synchronise the device and
+// the pool keeps its memory between calls (release threshold = unlimited), so repeated runs
+// neither pay cudaMalloc/cudaFree latency nor stall on the driver's deferred reclamation.
+void keep_pool(int device) {
+    static bool done[64] = {};
+    if (device < 0 || device >= 64 || done[device]) return;
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+        unsigned long long thr = ~0ull;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+    done[device] = true;
 }
 
 pcs_status session_alloc(pcs_session* s) {
@@ -244,18 +280,19 @@ pcs_status session_alloc(pcs_session* s) {
     } else {
         CUDA_TRY(cudaStreamCreateWithFlags(&s->st, cudaStreamNonBlocking));
     }
+    keep_pool(s->device);
     CUDA_TRY(cudaEventCreate(&s->ev_begin));
     CUDA_TRY(cudaEventCreate(&s->ev_end));
     CUDA_TRY(cudaEventCreate(&s->ev_k0));
     CUDA_TRY(cudaEventCreate(&s->ev_k1));
-    CUDA_TRY(cudaMalloc(&s->dAdj, sizeof(uint32_t) * (size_t)p * s->W));
-    CUDA_TRY(cudaMalloc(&s->dDeg, sizeof(int32_t) * (size_t)(p + 1)));
-    CUDA_TRY(cudaMalloc(&s->dLow, sizeof(int32_t) * (size_t)(p + 1)));
-    CUDA_TRY(cudaMalloc(&s->dOff, sizeof(int32_t) * (size_t)(p + 1)));
-    CUDA_TRY(cudaMalloc(&s->dUp, sizeof(int32_t) * (size_t)(p + 1)));
-    CUDA_TRY(cudaMalloc(&s->dInfo, sizeof(SnapInfo)));
-    CUDA_TRY(cudaMalloc(&s->dCnt, sizeof(Counters)));
-    CUDA_TRY(cudaMalloc(&s->dPrefix, sizeof(unsigned long long) * (size_t)(p + 1)));
+    CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&s->dAdj), sizeof(uint32_t) * (size_t)p * s->W, s->st));
+    CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&s->dDeg), sizeof(int32_t) * (size_t)(p + 1), s->st));
+    CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&s->dLow), sizeof(int32_t) * (size_t)(p + 1), s->st));
+    CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&s->dOff), sizeof(int32_t) * (size_t)(p + 1), s->st));
+    CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&s->dUp), sizeof(int32_t) * (size_t)(p + 1), s->st));
+    CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&s->dInfo), sizeof(SnapInfo), s->st));
+    CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&s->dCnt), sizeof(Counters), s->st));
+    CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&s->dPrefix), sizeof(unsigned long long) * (size_t)(p + 1), s->st));
     return PCS_OK;
 }
 
@@ -298,7 +335,7 @@ pcs_status build_binomials(pcs_session* s, int ell, int maxw) {
             t[(size_t)k * stride + n] = (a > UINT64_MAX - b) ? UINT64_MAX : a + b;
         }
     if (t.size() > s->capBinom) {
-        pcs_status st = realloc_dev(&s->dBinom, (long long)t.size());
+        pcs_status st = realloc_dev(s, &s->dBinom, (long long)t.size());
         if (st) return st;
         s->capBinom = t.size();
     }
@@ -372,18 +409,18 @@ pcs_status pcs_threshold_tau(double alpha, int32_t m, int32_t ell, double* tau) 
 
 static pcs_status session_upload_corr(pcs_session* s, const double* c) {
     s->ldc = (s->p + 3) / 4 * 4;
-    CUDA_TRY(cudaMalloc(&s->dC, sizeof(double) * (size_t)s->p * s->ldc));
+    CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&s->dC), sizeof(double) * (size_t)s->p * s->ldc, s->st));
     CUDA_TRY(cudaEventRecord(s->ev_begin, s->st));
     CUDA_TRY(cudaMemcpy2DAsync(s->dC, sizeof(double) * s->ldc, c, sizeof(double) * s->p, sizeof(double) * s->p, s->p,
                                cudaMemcpyHostToDevice, s->st));
     int* dErr = nullptr;
-    CUDA_TRY(cudaMalloc(&dErr, sizeof(int)));
+    CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&dErr), sizeof(int), s->st));
     CUDA_TRY(cudaMemsetAsync(dErr, 0, sizeof(int), s->st));
     launch_normalize_corr(s->dC, s->ldc, s->p, dErr, s->st);
     int err = 0;
     CUDA_TRY(cudaMemcpyAsync(&err, dErr, sizeof(int), cudaMemcpyDeviceToHost, s->st));
+    cudaFreeAsync(dErr, s->st);
     CUDA_TRY(cudaStreamSynchronize(s->st));
-    cudaFree(dErr);
     if (err & 2) return fail(PCS_EINVAL, "CorrelationMatrix: diagonal must be 1");
     if (err & 4) return fail(PCS_EINVAL, "CorrelationMatrix: matrix must be symmetric");
     if (err & 8) return fail(PCS_EINVAL, "CorrelationMatrix: entries must lie in [-1, 1]");
@@ -464,20 +501,20 @@ pcs_status pcs_session_level_begin(pcs_session* s, int32_t* running, int32_t* el
     if (ell > kMaxTemplLevel) {
         const long long need = level_rt_scratch_bytes(ell, s->num_sms, nullptr);
         if (need > s->capScratch) {
-            if ((st = realloc_dev(&s->dScratch, need))) return st;
+            if ((st = realloc_dev(s, &s->dScratch, need))) return st;
             s->capScratch = need;
         }
     }
     if (s->info.e_dir > s->capDir) {
-        if ((st = realloc_dev(&s->dNbr, s->info.e_dir))) return st;
-        if ((st = realloc_dev(&s->dEid, s->info.e_dir))) return st;
+        if ((st = realloc_dev(s, &s->dNbr, s->info.e_dir))) return st;
+        if ((st = realloc_dev(s, &s->dEid, s->info.e_dir))) return st;
         s->capDir = s->info.e_dir;
     }
     if (s->info.e_und > s->capUnd) {
-        if ((st = realloc_dev(&s->dEuA, s->info.e_und))) return st;
-        if ((st = realloc_dev(&s->dEuQa, s->info.e_und))) return st;
-        if ((st = realloc_dev(&s->dEuQb, s->info.e_und))) return st;
-        if ((st = realloc_dev(&s->dKeys, s->info.e_und))) return st;
+        if ((st = realloc_dev(s, &s->dEuA, s->info.e_und))) return st;
+        if ((st = realloc_dev(s, &s->dEuQa, s->info.e_und))) return st;
+        if ((st = realloc_dev(s, &s->dEuQb, s->info.e_und))) return st;
+        if ((st = realloc_dev(s, &s->dKeys, s->info.e_und))) return st;
         s->capUnd = s->info.e_und;
     }
     {
@@ -485,12 +522,11 @@ pcs_status pcs_session_level_begin(pcs_session* s, int32_t* running, int32_t* el
         if (need > s->capRec) {  // grow the record pool, keeping earlier levels' records
             const long long cap = std::max(need, s->capRec * 3 / 2);
             int32_t* np = nullptr;
-            CUDA_TRY(cudaMalloc(&np, sizeof(int32_t) * (size_t)cap));
+            CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&np), sizeof(int32_t) * (size_t)cap, s->st));
             if (s->recUsed)
                 CUDA_TRY(cudaMemcpyAsync(np, s->dRec, sizeof(int32_t) * (size_t)s->recUsed, cudaMemcpyDeviceToDevice,
                                          s->st));
-            CUDA_TRY(cudaStreamSynchronize(s->st));
-            cudaFree(s->dRec);
+            if (s->dRec) cudaFreeAsync(s->dRec, s->st);
             s->dRec = np;
             s->capRec = cap;
         }
@@ -611,6 +647,9 @@ pcs_status pcs_session_level_end(pcs_session* s) {
         L.kernel_ms = ms;
     }
     L.elapsed_s = now_s() - s->t_level;
+    trace("level %d: %.3f ms host (kernels %.3f ms), %llu serial / %llu device tests, %llu removed", L.level,
+          L.elapsed_s * 1e3, L.kernel_ms, (unsigned long long)L.ci_tests, (unsigned long long)L.device_ci_tests,
+          (unsigned long long)L.edges_removed);
     s->levels.push_back(L);
     s->in_level = false;
     return PCS_OK;
@@ -699,11 +738,16 @@ static pcs_status correlation_device(cudaStream_t stream, const double* x, int m
     double *dX = nullptr, *dXc = nullptr, *dG = nullptr, *dMean = nullptr;
     int* dErr = nullptr;
     pcs_status st = PCS_OK;
-    auto cleanup = [&]() { cudaFree(dX); cudaFree(dXc); cudaFree(dG); cudaFree(dMean); cudaFree(dErr); };
-    if ((!x_on_device && cudaMalloc(&dX, sizeof(double) * (size_t)m * p)) ||
-        cudaMalloc(&dXc, sizeof(double) * (size_t)p * ldk) ||
-        cudaMalloc(&dG, sizeof(double) * (size_t)p * ldg) || cudaMalloc(&dMean, sizeof(double) * (size_t)p) ||
-        cudaMalloc(&dErr, sizeof(int) * 2)) {
+    auto cleanup = [&]() {
+        for (void* q : {(void*)dX, (void*)dXc, (void*)dG, (void*)dMean, (void*)dErr})
+            if (q) cudaFreeAsync(q, stream);
+    };
+    auto alloc = [&](auto** ptr, size_t bytes) {
+        return cudaMallocAsync(reinterpret_cast<void**>(ptr), bytes, stream) != cudaSuccess;
+    };
+    if ((!x_on_device && alloc(&dX, sizeof(double) * (size_t)m * p)) || alloc(&dXc, sizeof(double) * (size_t)p * ldk) ||
+        alloc(&dG, sizeof(double) * (size_t)p * ldg) || alloc(&dMean, sizeof(double) * (size_t)p) ||
+        alloc(&dErr, sizeof(int) * 2)) {
         cleanup();
         return fail(PCS_ENOMEM, "cudaMalloc failed in compute_correlation");
     }
@@ -713,8 +757,8 @@ static pcs_status correlation_device(cudaStream_t stream, const double* x, int m
     launch_correlation(x_on_device ? x : dX, m, p, dXc, dG, ldg, dMean, dC, ldc, dErr, stream);
     int err[2];
     cudaMemcpyAsync(err, dErr, sizeof(err), cudaMemcpyDeviceToHost, stream);
-    cudaError_t ce = cudaStreamSynchronize(stream);
     cleanup();
+    cudaError_t ce = cudaStreamSynchronize(stream);
     if (ce != cudaSuccess) return fail(PCS_ECUDA, std::string("compute_correlation: ") + cudaGetErrorString(ce));
     if (err[0] & 1) st = fail(PCS_EINVAL, "DataMatrix: values must be finite");
     else if (err[1] != INT32_MAX) {
@@ -748,17 +792,23 @@ static pcs_status run_data(const double* x, bool on_device, int32_t m, int32_t p
                            pcs_result** out, int32_t* zero_var_col) {
     *out = nullptr;
     pcs_session* s = nullptr;
+    const double t0 = now_s();
     pcs_status st = session_new(p, m, cfg, &s);
     if (st) return st;
     s->ldc = (p + 3) / 4 * 4;
-    if (cudaMalloc(&s->dC, sizeof(double) * (size_t)p * s->ldc) != cudaSuccess) {
+    if (cudaMallocAsync(reinterpret_cast<void**>(&s->dC), sizeof(double) * (size_t)p * s->ldc, s->st) != cudaSuccess) {
         free_session(s);
         return fail(PCS_ENOMEM, "cudaMalloc failed");
     }
+    const double t1 = now_s();
     cudaEventRecord(s->ev_begin, s->st);
     st = correlation_device(s->st, x, m, p, s->dC, s->ldc, zero_var_col, on_device);
+    const double t2 = now_s();
     if (!st) st = run_session(s, out);
+    const double t3 = now_s();
     free_session(s);
+    trace("run_pc_stable_data: setup %.2f ms, correlation %.2f ms, levels+finish %.2f ms, teardown %.2f ms",
+          (t1 - t0) * 1e3, (t2 - t1) * 1e3, (t3 - t2) * 1e3, (now_s() - t3) * 1e3);
     return st;
 }
 

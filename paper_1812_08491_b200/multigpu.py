@@ -53,9 +53,26 @@ def torch_allreduce_min(group=None):
     return _reduce
 
 
+def host_staged_allreduce_min(group=None):
+    """MIN all-reduce through host memory (gloo): ranks sharing one GPU in tests, or any transport
+    without device-buffer support.  Same result as torch_allreduce_min."""
+    import torch
+    import torch.distributed as dist
+
+    def _reduce(ptr: int, n: int):
+        dev = torch.as_tensor(_CudaArray(ptr, n), device="cuda")
+        host = dev.cpu()
+        dist.all_reduce(host, op=dist.ReduceOp.MIN, group=group)
+        dev.copy_(host)
+        torch.cuda.current_stream().synchronize()
+
+    return _reduce
+
+
 def run_pc_stable_sharded(c_ptr: int, ldc: int, p: int, sample_count: int, cfg=None, group=None,
-                          with_sepsets: bool = True):
-    """run_pc_stable over all ranks of `group` (torch.distributed initialised, one GPU per rank)."""
+                          with_sepsets: bool = True, allreduce_min=None):
+    """run_pc_stable over all ranks of `group` (torch.distributed initialised, one GPU per rank).
+    allreduce_min: key reducer (default: NCCL on the device buffers)."""
     import torch.distributed as dist
 
     from . import Session, SkeletonConfig
@@ -66,7 +83,8 @@ def run_pc_stable_sharded(c_ptr: int, ldc: int, p: int, sample_count: int, cfg=N
     s = Session(sample_count=sample_count, cfg=cfg, shard_index=rank, shard_count=world, device_ptr=c_ptr, ldc=ldc,
                 p=p)
     try:
-        level_loop(s, torch_allreduce_min(group) if world > 1 else None, world)
+        red = allreduce_min or torch_allreduce_min(group)
+        level_loop(s, red if world > 1 else None, world)
         return s.finish(with_sepsets)
     finally:
         s.close()
