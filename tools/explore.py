@@ -12,6 +12,9 @@ CONFIGS = {
     "C2": (1000, 10000, 0.1, 1),
     "C3": (1643, 850, 0.01, 2),
     "C4": (5361, 63, 0.002, 3),
+    "C5a": (2000, 5000, 0.05, 4),   # scaling-sweep shapes (BASELINE configs[4]); reference generator
+    "C5b": (5000, 5000, 0.05, 5),
+    "C5c": (2000, 5000, 0.2, 6),
 }
 names = sys.argv[1].split(",") if len(sys.argv) > 1 else list(CONFIGS)
 strategies = sys.argv[2].split(",") if len(sys.argv) > 2 else ["set"]
