@@ -75,8 +75,9 @@ typedef struct {
     uint64_t device_ci_tests;         /* CI tests the device actually executed */
     uint64_t device_pseudo_inverses;  /* pseudo-inverses the device actually executed */
     double kernel_ms;                 /* CUDA-event time of the level's CI-test kernels */
-    uint64_t device_exact_tests;      /* tests re-evaluated in the reference's operation order (not
-                                         certified dependent by the FMA filter) */
+    uint64_t device_exact_tests;      /* tests whose statistic the device evaluated (in the reference's
+                                         operation order); the rest of device_ci_tests were decided
+                                         without arithmetic (set with h00 == 0: degenerate) */
 } pcs_level_stats;
 
 typedef struct pcs_result pcs_result;

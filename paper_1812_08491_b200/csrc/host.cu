@@ -195,6 +195,9 @@ struct pcs_session {
     size_t capBinom = 0;
     unsigned char* dScratch = nullptr;  // generic-ell per-lane scratch
     long long capScratch = 0;
+    unsigned long long* dShardCost = nullptr;  // multi-GPU: per-row / per-edge cost prefix of a pass
+    long long capShardCost = 0;
+    unsigned long long* dBounds = nullptr;     // multi-GPU: this shard's [first, end) work unit
     // level state
     int ell = -1;
     bool stopped = false, in_level = false;
@@ -225,6 +228,8 @@ void free_session(pcs_session* s) {
     rel(s->dEuA); rel(s->dEuQa); rel(s->dEuQb); rel(s->dKeys); rel(s->dRec);
     rel(s->dBinom);
     rel(s->dScratch);
+    rel(s->dShardCost);
+    rel(s->dBounds);
     if (s->st) cudaStreamSynchronize(s->st);
     if (s->ev_begin) cudaEventDestroy(s->ev_begin);
     if (s->ev_end) cudaEventDestroy(s->ev_end);
@@ -551,13 +556,33 @@ pcs_status pcs_session_level_pass(pcs_session* s, int32_t pass) {
     LevelArgs A = level_args(s);
     const int shard = s->cfg.shard_index, nsh = s->cfg.shard_count;
     if (!s->kernel_timing) { CUDA_TRY(cudaEventRecord(s->ev_k0, s->st)); }
+    // Multi-GPU: every rank derives the same cost-weighted split of the pass's work units (contiguous
+    // ranges, so a row's early exits stay on one GPU); units are not equally expensive (a band of row i
+    // tests its ntar targets, which differ by orders of magnitude between rows), so splitting by unit
+    // count would leave the ranks up to ~1.8x apart at 8 GPUs (C2 level 3).
+    pcs_status st = PCS_OK;
+    if (nsh > 1) {
+        const long long need = std::max<long long>(s->p + 1, s->info.e_und + 1);
+        if (need > s->capShardCost) {
+            if ((st = realloc_dev(s, &s->dShardCost, need))) return st;
+            s->capShardCost = need;
+        }
+        if (!s->dBounds && (st = realloc_dev(s, &s->dBounds, 2))) return st;
+    }
     if (s->cfg.variant == PCS_VARIANT_SET || s->ell == 1 || s->ell > kMaxTemplLevel) {
-        launch_row_work(A, pass, s->cfg.variant, 0, s->p, s->dPrefix, s->st);
-        unsigned long long total = 0;
-        CUDA_TRY(cudaMemcpyAsync(&total, s->dPrefix + s->p, sizeof(total), cudaMemcpyDeviceToHost, s->st));
-        CUDA_TRY(cudaStreamSynchronize(s->st));
-        const unsigned long long u0 = (unsigned long long)((__int128)total * shard / nsh);
-        const unsigned long long u1 = (unsigned long long)((__int128)total * (shard + 1) / nsh);
+        unsigned long long u0 = 0, u1 = 0;
+        if (nsh > 1) {
+            unsigned long long b[2] = {0, 0};
+            launch_row_work_sharded(A, pass, s->cfg.variant, s->dPrefix, s->dShardCost, shard, nsh, s->dBounds, s->st);
+            CUDA_TRY(cudaMemcpyAsync(b, s->dBounds, sizeof(b), cudaMemcpyDeviceToHost, s->st));
+            CUDA_TRY(cudaStreamSynchronize(s->st));
+            u0 = b[0];
+            u1 = b[1];
+        } else {
+            launch_row_work(A, pass, s->cfg.variant, 0, s->p, s->dPrefix, s->st);
+            CUDA_TRY(cudaMemcpyAsync(&u1, s->dPrefix + s->p, sizeof(u1), cudaMemcpyDeviceToHost, s->st));
+            CUDA_TRY(cudaStreamSynchronize(s->st));
+        }
         if (u1 > u0) {
             if (s->ell == 1) {
                 launch_level1(A, pass, s->dPrefix, u0, u1, s->st);
@@ -572,7 +597,15 @@ pcs_status pcs_session_level_pass(pcs_session* s, int32_t pass) {
         }
     } else {
         const long long E = s->info.e_und;
-        const long long e0 = (long long)((__int128)E * shard / nsh), e1 = (long long)((__int128)E * (shard + 1) / nsh);
+        long long e0 = 0, e1 = E;
+        if (nsh > 1) {  // cost-weighted: an edge's pass costs C(w - 1, ell) tests in the tested row
+            unsigned long long b[2] = {0, 0};
+            launch_edge_bounds(A, pass, E, s->dShardCost, shard, nsh, s->dBounds, s->st);
+            CUDA_TRY(cudaMemcpyAsync(b, s->dBounds, sizeof(b), cudaMemcpyDeviceToHost, s->st));
+            CUDA_TRY(cudaStreamSynchronize(s->st));
+            e0 = (long long)b[0];
+            e1 = (long long)b[1];
+        }
         if (e1 > e0 && launch_level_edge(A, pass, e0, e1, s->num_sms, s->st))
             return fail(PCS_EUNSUPPORTED, "level not supported by the edge kernel");
     }

@@ -259,19 +259,68 @@ void launch_fill_keys(unsigned long long* keys, long long n, cudaStream_t s) {
 constexpr int kL1Threads = 128;   // targets per ell=1 tile
 constexpr int kSetBand = 32;      // conditioning sets per ell>=2 unit
 
+// units[i]: work units of row i in this pass; cost[i] (optional, multi-GPU sharding): units[i] times
+// the relative cost of one of its units -- an ell = 1 tile tests its targets against the row's w
+// candidate sets, an ell >= 2 band tests the row's ntar targets against 32 sets (+ 32 pseudo-inverses
+// and the staging, the constant term)
 __global__ void row_work_kernel(LevelArgs A, int pass, int variant, int row_begin, int row_end,
-                                unsigned long long* units) {
+                                unsigned long long* units, unsigned long long* cost) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= A.p) return;
-    unsigned long long u = 0;
+    unsigned long long u = 0, c = 0;
     const int w = A.off[i + 1] - A.off[i];
     const int lc = A.lowcnt[i];
     const int ntar = pass == 0 ? w - lc : lc;
     if (i >= row_begin && i < row_end && w >= A.ell + 1 && ntar > 0) {
-        if (A.ell == 1) u = (unsigned long long)((ntar + kL1Threads - 1) / kL1Threads);
-        else u = (A.binom(w, A.ell) + kSetBand - 1) / kSetBand;
+        if (A.ell == 1) {
+            u = (unsigned long long)((ntar + kL1Threads - 1) / kL1Threads);
+            c = u * (unsigned long long)(w + 8);
+        } else {
+            u = (A.binom(w, A.ell) + kSetBand - 1) / kSetBand;
+            c = u * (unsigned long long)(ntar + 32);
+        }
     }
     units[i] = u;
+    if (cost) cost[i] = c;
+}
+
+// per-edge cost of a cuPC-E pass (multi-GPU sharding): C(w - 1, ell) tests in the tested row
+__global__ void edge_cost_kernel(LevelArgs A, int pass, long long E, unsigned long long* cost) {
+    for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < E; e += (long long)gridDim.x * blockDim.x) {
+        const int a = A.eu_a[e];
+        const int x = pass == 0 ? a : A.nbr[A.off[a] + A.eu_qa[e]];
+        const int w = A.off[x + 1] - A.off[x];
+        const unsigned long long b = w >= A.ell + 1 ? A.binom(w - 1, A.ell) : 0ull;
+        cost[e] = (b > (1ull << 40) ? (1ull << 40) : b) + 1ull;
+    }
+}
+
+// unit index at cost position b: pc = cost prefix (n+1 entries), pu = unit prefix (n+1) or null
+// (unit k = entry k).  Inside an entry the units are equally expensive; monotone in b, 0 at b = 0
+// and the total unit count at b = pc[n], so consecutive shards tile [0, units) exactly.
+__device__ unsigned long long unit_at_cost(const unsigned long long* pu, const unsigned long long* pc, long long n,
+                                           unsigned long long b) {
+    if (b >= pc[n]) return pu ? pu[n] : (unsigned long long)n;
+    long long lo = 0, hi = n - 1;
+    while (lo < hi) {
+        const long long mid = (lo + hi + 1) >> 1;
+        if (pc[mid] <= b) lo = mid; else hi = mid - 1;
+    }
+    const unsigned long long rc = pc[lo + 1] - pc[lo], d = b - pc[lo];  // pc[lo] <= b < pc[lo + 1]
+    const unsigned long long nu = pu ? pu[lo + 1] - pu[lo] : 1ull;
+    unsigned long long k = (unsigned long long)((double)d / (double)rc * (double)nu + 0.5);
+    if (k > nu) k = nu;
+    return (pu ? pu[lo] : (unsigned long long)lo) + k;
+}
+
+__global__ void shard_bounds_kernel(const unsigned long long* pu, const unsigned long long* pc, long long n, int shard,
+                                    int nsh, unsigned long long* out) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    const unsigned long long T = pc[n];
+    const unsigned long long b0 = (unsigned long long)((unsigned __int128)T * shard / nsh);
+    const unsigned long long b1 = (unsigned long long)((unsigned __int128)T * (shard + 1) / nsh);
+    out[0] = shard == 0 ? 0ull : unit_at_cost(pu, pc, n, b0);
+    out[1] = shard == nsh - 1 ? (pu ? pu[n] : (unsigned long long)n) : unit_at_cost(pu, pc, n, b1);
 }
 
 // exclusive scan in place over n+1 entries (entry n receives the total); one block
@@ -302,9 +351,31 @@ __global__ void scan_u64_kernel(unsigned long long* a, int n) {
 void launch_row_work(const LevelArgs& A, int pass, int variant, int row_begin, int row_end,
                      unsigned long long* prefix, cudaStream_t s) {
     ++g_kernel_launches;
-    row_work_kernel<<<(A.p + 255) / 256, 256, 0, s>>>(A, pass, variant, row_begin, row_end, prefix);
+    row_work_kernel<<<(A.p + 255) / 256, 256, 0, s>>>(A, pass, variant, row_begin, row_end, prefix, nullptr);
     ++g_kernel_launches;
     scan_u64_kernel<<<1, 1024, 0, s>>>(prefix, A.p);
+}
+
+void launch_row_work_sharded(const LevelArgs& A, int pass, int variant, unsigned long long* prefix,
+                             unsigned long long* cost, int shard, int nsh, unsigned long long* bounds,
+                             cudaStream_t s) {
+    ++g_kernel_launches;
+    row_work_kernel<<<(A.p + 255) / 256, 256, 0, s>>>(A, pass, variant, 0, A.p, prefix, cost);
+    g_kernel_launches += 3;
+    scan_u64_kernel<<<1, 1024, 0, s>>>(prefix, A.p);
+    scan_u64_kernel<<<1, 1024, 0, s>>>(cost, A.p);
+    shard_bounds_kernel<<<1, 32, 0, s>>>(prefix, cost, A.p, shard, nsh, bounds);
+}
+
+void launch_edge_bounds(const LevelArgs& A, int pass, long long E, unsigned long long* cost, int shard, int nsh,
+                        unsigned long long* bounds, cudaStream_t s) {
+    long long blocks = (E + 255) / 256;
+    if (blocks > 148 * 8) blocks = 148 * 8;
+    if (blocks < 1) blocks = 1;
+    g_kernel_launches += 3;
+    edge_cost_kernel<<<(int)blocks, 256, 0, s>>>(A, pass, E, cost);
+    scan_u64_kernel<<<1, 1024, 0, s>>>(cost, (int)E);
+    shard_bounds_kernel<<<1, 32, 0, s>>>(nullptr, cost, E, shard, nsh, bounds);
 }
 
 // =========================================================== ell = 1
@@ -378,6 +449,7 @@ __global__ void __launch_bounds__(kL1Threads) level1_kernel(LevelArgs A, int pas
         __syncthreads();
     }
     add_counter(&A.cnt->gpu_tests, tests);
+    add_counter(&A.cnt->gpu_exact, tests);
     if (nan) atomicOr(&A.cnt->err_nan, 1);
 }
 
@@ -446,10 +518,14 @@ struct SetWarpSmem {
 // (plus C(i,S)[col], P0[col]) is live.  Every accumulator (P1[col], d11, d01, d10) sees
 // exactly the reference's sequence of roundings (-fmad=false), so h01 / denom are
 // bit-identical to h_terms<L>.
+//
+// Outputs s01 = d01 + d10 and h2 = RN(2 c_ij - s01) = 2 h01 exactly (see surely_dependent2), so the
+// common path skips the reference's 0.5 * (.) multiply; the rare exact path rebuilds
+// h01 = c_ij - 0.5 * s01 bit for bit (c_ij = 0.5 * cij2 is exact).
 template <int L, int NT, int LP>
 __device__ __forceinline__ void h_terms_stream(const SetSlot<L>& sl, const double (&cp)[NT][LP],
-                                               const double (&cur)[NT], const double (&cij)[NT],
-                                               double (&h01)[NT], double (&den)[NT]) {
+                                               const double (&cur)[NT], const double (&cij2)[NT],
+                                               double (&s01)[NT], double (&h2)[NT], double (&den)[NT]) {
     double d11[NT], d01[NT], d10[NT];
 #pragma unroll
     for (int col = 0; col < L; ++col) {
@@ -486,7 +562,8 @@ __device__ __forceinline__ void h_terms_stream(const SetSlot<L>& sl, const doubl
 #pragma unroll
     for (int t = 0; t < NT; ++t) {
         const double h11 = 1.0 - d11[t];
-        h01[t] = cij[t] - 0.5 * (d01[t] + d10[t]);
+        s01[t] = d01[t] + d10[t];
+        h2[t] = cij2[t] - s01[t];
         den[t] = h00 * h11;
     }
 }
@@ -495,15 +572,20 @@ __device__ __forceinline__ void h_terms_stream(const SetSlot<L>& sl, const doubl
 // segmask: bit s set when set s starts a new run of equal leading L-1 members.  Inside a
 // run (lexicographic order) the last member's position advances by one per set: set
 // sg0 + d has last position base + d, so "target is a member" is one compare per set.
+// livemask: bit s set when set s has h00 != 0.  h00 == 0 (exactly) makes denom = h00 * h11 a
+// zero or NaN for every target, so every test of such a set is the reference's degenerate
+// "dependent" (stats.hpp:301-305) without any arithmetic: those sets are counted, never visited
+// (rank-truncated inputs hit this often: ~29% of C2's level-3 sets), and the last-member
+// prefetch always targets the next LIVE set, so skipped sets cost no L2 round trip either.
 template <int L, int NT>
 __device__ __forceinline__ void set_sweep(const LevelArgs& A, SetWarpSmem<L>& S, int lane, int nlive, int nvalid,
-                                          unsigned segmask, unsigned long long K0, unsigned long long& tests,
-                                          int& nan) {
+                                          unsigned segmask, unsigned livemask, unsigned long long K0,
+                                          unsigned long long& tests, unsigned long long& degen, int& nan) {
     const double* __restrict__ C = A.C;
-    const double hi2 = A.th.hi2;
+    const double hi2x4 = 4.0 * A.th.hi2;  // exact (power-of-two scaling)
     int rel[NT];           // tested while the set index is below rel (relative key)
     const double* Cj[NT];  // C + j: gathers C(mem, j) = Cj[t][mem * ldc] (one IMAD.WIDE each)
-    double cij[NT];
+    double cij2[NT];       // 2 c_ij (exact)
 #pragma unroll
     for (int t = 0; t < NT; ++t) {
         const int k = t * 32 + lane;
@@ -511,23 +593,30 @@ __device__ __forceinline__ void set_sweep(const LevelArgs& A, SetWarpSmem<L>& S,
             const unsigned long long d = S.tkey[k] - K0;  // > 0 (staged targets are live)
             rel[t] = d > 0x3fffffffull ? 0x3fffffff : (int)d;
             Cj[t] = C + S.tj[k];
-            cij[t] = S.tcij[k];
+            const double c = S.tcij[k];
+            cij2[t] = c + c;
         } else {
             rel[t] = -1;
             Cj[t] = C;  // valid address: loads stay unconditional
-            cij[t] = 0.0;
+            cij2[t] = 0.0;
         }
     }
     constexpr int LP = L > 1 ? L - 1 : 1;
+    const unsigned valid_mask = nvalid >= 32 ? 0xffffffffu : ((1u << nvalid) - 1u);
+    segmask &= valid_mask;
+    const unsigned live = livemask & valid_mask, dead = valid_mask & ~livemask;
+    auto next_live = [&](int s) -> int {  // first live set after s (nvalid: none)
+        const unsigned m = live & ~((2u << s) - 1u);
+        return m ? __ffs(m) - 1 : nvalid;
+    };
     double cp[NT][LP];
     double nxt[NT], alt[NT];
-    {
-        const int ro = S.slot[0].roff[L - 1];
+    int nl = live ? __ffs(live) - 1 : nvalid;  // next live set to test
+    if (nl < nvalid) {
+        const int ro = S.slot[nl].roff[L - 1];
 #pragma unroll
         for (int t = 0; t < NT; ++t) nxt[t] = __ldg(Cj[t] + ro);
     }
-    const unsigned valid_mask = nvalid >= 32 ? 0xffffffffu : ((1u << nvalid) - 1u);
-    segmask &= valid_mask;
     int sg = 0;
     while (sg < nvalid) {
         const int sg0 = sg;
@@ -539,11 +628,13 @@ __device__ __forceinline__ void set_sweep(const LevelArgs& A, SetWarpSmem<L>& S,
             // new run of sets sharing their first L-1 members: gather those once per target
             const SetSlot<L>& sl = S.slot[sg0];
             const int base = sl.pos[L - 1];
+            if (nl < seg_end) {
 #pragma unroll
-            for (int a = 0; a < L - 1; ++a) {
-                const int ro = sl.roff[a];
+                for (int a = 0; a < L - 1; ++a) {
+                    const int ro = sl.roff[a];
 #pragma unroll
-                for (int t = 0; t < NT; ++t) cp[t][a] = __ldg(Cj[t] + ro);
+                    for (int t = 0; t < NT; ++t) cp[t][a] = __ldg(Cj[t] + ro);
+                }
             }
 #pragma unroll
             for (int t = 0; t < NT; ++t) {
@@ -556,27 +647,28 @@ __device__ __forceinline__ void set_sweep(const LevelArgs& A, SetWarpSmem<L>& S,
                 dm[t] = sg0 + q - base;
             }
         }
-        // double-buffered last-member gathers: step(sg, cur, next) tests set sg with `cur` while
-        // prefetching set sg+1 into `next` (no register copies between steps)
-        auto step = [&](int sgx, const double (&cur)[NT], double (&pre)[NT]) {
+        // double-buffered last-member gathers: step(s, n, cur, pre) tests live set s with `cur` while
+        // prefetching live set n (the next one, possibly in a later run) into `pre`
+        auto step = [&](int sgx, int nxs, const double (&cur)[NT], double (&pre)[NT]) {
             const SetSlot<L>& sl = S.slot[sgx];
-            {  // prefetch the next set's last-member gathers (clamped: always a valid slot)
-                const int ro = S.slot[min(sgx + 1, nvalid - 1)].roff[L - 1];
+            {  // clamped: always a valid slot
+                const int ro = S.slot[min(nxs, nvalid - 1)].roff[L - 1];
 #pragma unroll
                 for (int t = 0; t < NT; ++t) pre[t] = __ldg(Cj[t] + ro);
             }
-            double h01[NT], den[NT];
-            h_terms_stream<L, NT, LP>(sl, cp, cur, cij, h01, den);
+            double s01[NT], h2[NT], den[NT];
+            h_terms_stream<L, NT, LP>(sl, cp, cur, cij2, s01, h2, den);
             // branch-free common path: flag the (rare) tests not certainly dependent
             unsigned cand = 0;
 #pragma unroll
             for (int t = 0; t < NT; ++t)
-                cand |= (unsigned)((sgx < lim[t]) & (sgx != dm[t]) & !surely_dependent(h01[t], den[t], hi2)) << t;
+                cand |= (unsigned)((sgx < lim[t]) & (sgx != dm[t]) & !surely_dependent2(h2[t], den[t], hi2x4)) << t;
             if (__any_sync(0xffffffffu, cand)) {
 #pragma unroll
                 for (int t = 0; t < NT; ++t) {
                     if ((cand >> t) & 1u) {
-                        const int d = decide_fast(h01[t], den[t], A.th);
+                        const double h01 = 0.5 * cij2[t] - 0.5 * s01[t];  // == c_ij - 0.5 * (d01 + d10)
+                        const int d = decide_fast(h01, den[t], A.th);
                         if (d != kDependent) {
                             if (d == kNanError) nan = 1;
                             else atomicMin(A.keys + S.te[t * 32 + lane], K0 + (unsigned long long)sgx);
@@ -588,24 +680,31 @@ __device__ __forceinline__ void set_sweep(const LevelArgs& A, SetWarpSmem<L>& S,
                 }
             }
         };
-        while (sg < seg_end) {
-            step(sg, nxt, alt);
-            ++sg;
-            if (sg == seg_end) {
+        while (nl < seg_end) {
+            int s = nl;
+            nl = next_live(s);
+            step(s, nl, nxt, alt);
+            if (nl >= seg_end) {
 #pragma unroll
                 for (int t = 0; t < NT; ++t) nxt[t] = alt[t];
                 break;
             }
-            step(sg, alt, nxt);
-            ++sg;
+            s = nl;
+            nl = next_live(s);
+            step(s, nl, alt, nxt);
         }
-        // tests of this run, per target: sets [sg0, hi) minus the member set (serial order)
+        // tests of this run, per target: sets [sg0, hi) minus the member set (serial order); the
+        // dead (h00 == 0) ones among them were decided without arithmetic
 #pragma unroll
         for (int t = 0; t < NT; ++t) {
             const int hi = ((hit >> t) & 1u) ? lim[t] + 1 : min(seg_end, lim[t]);
             const int n = max(0, hi - sg0);
-            tests += (unsigned)(n - (dm[t] >= sg0 && dm[t] < sg0 + n ? 1 : 0));
+            const bool in = dm[t] >= sg0 && dm[t] < sg0 + n;
+            tests += (unsigned)(n - (in ? 1 : 0));
+            const unsigned rm = n >= 32 ? 0xffffffffu : (((1u << n) - 1u) << sg0);
+            degen += (unsigned)(__popc(dead & rm) - ((in && ((dead >> dm[t]) & 1u)) ? 1 : 0));
         }
+        sg = seg_end;
     }
 }
 
@@ -622,7 +721,7 @@ __global__ void __launch_bounds__(kSetWarps * 32, 3) level_set_kernel(LevelArgs 
     const long long ldc = A.ldc;
     const unsigned long long dirbits = (unsigned long long)pass << kDirShift;
     const unsigned lt_mask = (1u << lane) - 1u;
-    unsigned long long tests = 0, pinvs = 0;
+    unsigned long long tests = 0, pinvs = 0, degen = 0;
     int nan = 0;
     unsigned long long* cursor = &A.cnt->units[pass];
     for (;;) {
@@ -638,7 +737,7 @@ __global__ void __launch_bounds__(kSetWarps * 32, 3) level_set_kernel(LevelArgs 
         const unsigned long long total = A.binom(w, L);
         const int nvalid = (int)min(32ull, total - t0);
         bool have_sets = false;
-        unsigned segmask = 1u;
+        unsigned segmask = 1u, livemask = 0u;
         for (int tb = qbeg; tb < qend; tb += kStage) {
             const int tend = min(tb + kStage, qend);
             // ---- stage the live targets of [tb, tend), compacted
@@ -713,18 +812,19 @@ __global__ void __launch_bounds__(kSetWarps * 32, 3) level_set_kernel(LevelArgs 
                     }
                 }
                 segmask = __ballot_sync(0xffffffffu, starts);
+                livemask = __ballot_sync(0xffffffffu, lane < nvalid && S.slot[lane].h00 != 0.0);
             }
             __syncwarp();
             // ---- phase 2: sets in rank order, NT targets per lane
             const int nt = (nlive + 31) >> 5;
             if constexpr (SetCfg<L>::NT == 4) {
-                if (nt == 4) set_sweep<L, 4>(A, S, lane, nlive, nvalid, segmask, K0, tests, nan);
-                else if (nt == 3) set_sweep<L, 3>(A, S, lane, nlive, nvalid, segmask, K0, tests, nan);
-                else if (nt == 2) set_sweep<L, 2>(A, S, lane, nlive, nvalid, segmask, K0, tests, nan);
-                else set_sweep<L, 1>(A, S, lane, nlive, nvalid, segmask, K0, tests, nan);
+                if (nt == 4) set_sweep<L, 4>(A, S, lane, nlive, nvalid, segmask, livemask, K0, tests, degen, nan);
+                else if (nt == 3) set_sweep<L, 3>(A, S, lane, nlive, nvalid, segmask, livemask, K0, tests, degen, nan);
+                else if (nt == 2) set_sweep<L, 2>(A, S, lane, nlive, nvalid, segmask, livemask, K0, tests, degen, nan);
+                else set_sweep<L, 1>(A, S, lane, nlive, nvalid, segmask, livemask, K0, tests, degen, nan);
             } else {
-                if (nt == 2) set_sweep<L, 2>(A, S, lane, nlive, nvalid, segmask, K0, tests, nan);
-                else set_sweep<L, 1>(A, S, lane, nlive, nvalid, segmask, K0, tests, nan);
+                if (nt == 2) set_sweep<L, 2>(A, S, lane, nlive, nvalid, segmask, livemask, K0, tests, degen, nan);
+                else set_sweep<L, 1>(A, S, lane, nlive, nvalid, segmask, livemask, K0, tests, degen, nan);
             }
             __syncwarp();
         }
@@ -735,7 +835,7 @@ __global__ void __launch_bounds__(kSetWarps * 32, 3) level_set_kernel(LevelArgs 
         }
     }
     add_counter(&A.cnt->gpu_tests, tests);
-    add_counter(&A.cnt->gpu_exact, tests);  // every test is evaluated in the reference's operation order
+    add_counter(&A.cnt->gpu_exact, tests - degen);  // evaluated in the reference's operation order
     if (lane == 0 && pinvs) atomicAdd(&A.cnt->gpu_pinv, pinvs);
     if (nan) atomicOr(&A.cnt->err_nan, 1);
 }
@@ -836,6 +936,7 @@ __global__ void __launch_bounds__(128) level_edge_kernel(LevelArgs A, int pass, 
         }
     }
     add_counter(&A.cnt->gpu_tests, tests);
+    add_counter(&A.cnt->gpu_exact, tests);
     add_counter(&A.cnt->gpu_pinv, pinvs);
     if (nan) atomicOr(&A.cnt->err_nan, 1);
 }
@@ -894,7 +995,7 @@ __global__ void __launch_bounds__(128) level_set_rt_kernel(LevelArgs A, int pass
     const double* __restrict__ C = A.C;
     const long long ldc = A.ldc;
     const unsigned long long dirbits = (unsigned long long)pass << kDirShift;
-    unsigned long long tests = 0, pinvs = 0;
+    unsigned long long tests = 0, pinvs = 0, degen = 0;
     int nan = 0;
     unsigned long long* cursor = &A.cnt->units[pass];
     for (;;) {
@@ -953,13 +1054,14 @@ __global__ void __launch_bounds__(128) level_set_rt_kernel(LevelArgs A, int pass
                 bool member = false;
                 for (int a = 0; a < n; ++a) member |= Spos[a] == q;
                 if (member) continue;
-                for (int a = 0; a < n; ++a) cjS[a] = __ldg(C + (size_t)Spos[n + a] * ldc + j);
-                double h01, denom;
                 const double* Sminv = S + n * n;
                 const double* SciS = S + 7 * n * n;
+                ++tests;
+                if (SciS[2 * n] == 0.0) { ++degen; continue; }  // h00 == 0: degenerate (see set_sweep)
+                for (int a = 0; a < n; ++a) cjS[a] = __ldg(C + (size_t)Spos[n + a] * ldc + j);
+                double h01, denom;
                 h_terms_rt(Sminv, SciS, SciS + n, SciS[2 * n], cjS, n, cij, P1, h01, denom);
                 const int d = decide_fast(h01, denom, A.th);
-                ++tests;
                 if (d != kDependent) {
                     live = false;
                     if (d == kNanError) nan = 1;
@@ -970,6 +1072,7 @@ __global__ void __launch_bounds__(128) level_set_rt_kernel(LevelArgs A, int pass
         __syncwarp();
     }
     add_counter(&A.cnt->gpu_tests, tests);
+    add_counter(&A.cnt->gpu_exact, tests - degen);
     if (lane == 0 && pinvs) atomicAdd(&A.cnt->gpu_pinv, pinvs);
     if (nan) atomicOr(&A.cnt->err_nan, 1);
 }

@@ -277,6 +277,20 @@ __device__ __forceinline__ bool surely_dependent(double h01, double denom, doubl
     return (h01 * h01 >= fma(denom, hi2, 1e-240)) | (denom <= 0.0);
 }
 
+// surely_dependent with h01 and the threshold scaled by 2 (h2 = 2 h01, hi2x4 = 4 hi2) and the
+// degenerate test on the bit pattern (ALU pipe instead of a DSETP): (int64)bits(denom) <= 0 holds
+// exactly for +0, -0, negative denominators and negative-signed NaNs, all of which the reference
+// treats as degenerate -> dependent (!(denom > 0), stats.hpp:301); a positive NaN falls through to
+// the comparison, which is false, so it takes the exact path.  Soundness of the scaled
+// comparison: when it holds, h2^2 >= 4e-240 so |h2| >= 2e-120 is normal; then h2 = RN(2c - s) =
+// 2 RN(c - s/2) = 2 h01 exactly (if s/2 is inexact, s is subnormal and both sides round to c),
+// h2^2 = 4 RN(h01^2) and RN(denom * 4hi2 + 4e-240) = 4 RN(denom * hi2 + 1e-240), so the
+// unscaled filter holds as well.
+__device__ __forceinline__ bool surely_dependent2(double h2, double denom, double hi2x4) {
+    constexpr double kTiny4 = 4.0 * 1e-240;
+    return (h2 * h2 >= fma(denom, hi2x4, kTiny4)) | (__double_as_longlong(denom) <= 0);
+}
+
 // Level-0 decision on rho = clamp(c_ij) (stats.hpp:309-312).
 __device__ __forceinline__ int decide0(double c, const Thresholds& th) {
     const double ac = fabs(c);

@@ -22,7 +22,7 @@ struct Counters {
     unsigned long long removed;     // edges removed
     unsigned long long gpu_tests;   // CI tests executed on the device
     unsigned long long gpu_pinv;    // pseudo-inverses executed on the device
-    unsigned long long gpu_exact;   // tests re-evaluated in reference order (filter could not certify)
+    unsigned long long gpu_exact;   // tests whose statistic was evaluated (not a zero-h00 set)
     unsigned long long rec_count;   // sepset records written
     unsigned long long units[2];    // persistent-grid work cursors (pass A / B)
     int err_nan;                    // fisher_z would throw (NaN statistic)
@@ -77,6 +77,13 @@ void launch_fill_keys(unsigned long long* keys, long long n, cudaStream_t s);
 // restricted to [row_begin,row_end) for sharding); returns nothing, writes prefix[p+1]
 void launch_row_work(const LevelArgs& A, int pass, int variant, int row_begin, int row_end,
                      unsigned long long* prefix, cudaStream_t s);
+// multi-GPU: the same prefix plus a cost prefix, and this shard's cost-weighted unit range -> bounds[2]
+void launch_row_work_sharded(const LevelArgs& A, int pass, int variant, unsigned long long* prefix,
+                             unsigned long long* cost, int shard, int nsh, unsigned long long* bounds,
+                             cudaStream_t s);
+// multi-GPU cuPC-E: cost-weighted range of undirected edges for this shard -> bounds[2]
+void launch_edge_bounds(const LevelArgs& A, int pass, long long E, unsigned long long* cost, int shard, int nsh,
+                        unsigned long long* bounds, cudaStream_t s);
 void launch_level1(const LevelArgs& A, int pass, const unsigned long long* prefix, unsigned long long u_begin,
                    unsigned long long u_end, cudaStream_t s);
 int launch_level_set(const LevelArgs& A, int pass, const unsigned long long* prefix, unsigned long long u_begin,

@@ -26,6 +26,11 @@ for s in $STEPS; do
       timeout 900 ncu --set full --clock-control none --import-source on -k regex:level_set --launch-skip 2 -c 1 -f -o $OUT/top \
         python tools/profile_target.py 3 32 set > $OUT/ncu_full.log 2>&1
       ;;
+    balance)
+      timeout 900 python tools/shard_balance.py 8 C2 3 set > $OUT/balance.json 2> $OUT/balance.err
+      timeout 600 python tools/shard_balance.py 8 C3 -1 set >> $OUT/balance.json 2>> $OUT/balance.err
+      timeout 600 python tools/shard_balance.py 8 C2 2 edge >> $OUT/balance.json 2>> $OUT/balance.err
+      ;;
     bench)
       timeout 900 python bench.py > $OUT/bench.json 2> $OUT/bench.err
       ;;
