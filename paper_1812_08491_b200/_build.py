@@ -92,5 +92,33 @@ def build(verbose: bool = False, force: bool = False) -> str:
     return LIB
 
 
+def build_variant(name: str, defines: list[str]) -> str:
+    """Tuning experiments (tools/variants.py): the library with level.cu rebuilt under extra -D knobs
+    into variants/libpcstable_b200_<name>.so (knobs never change results)."""
+    build()
+    vdir = os.path.join(BUILD, "var_" + name)
+    os.makedirs(vdir, exist_ok=True)
+    out_dir = os.path.join(PKG, "variants")
+    os.makedirs(out_dir, exist_ok=True)
+    lib = os.path.join(out_dir, f"libpcstable_b200_{name}.so")
+    obj = os.path.join(vdir, "level.o")
+    cmd = [nvcc(), *ARCH, *COMMON, *UNITS["level.cu"], *[f"-D{d}" for d in defines], "-c",
+           os.path.join(CSRC, "level.cu"), "-o", obj]
+    res = subprocess.run(cmd, capture_output=True, text=True)
+    with open(os.path.join(vdir, "level.cu.ptxas.log"), "w") as f:
+        f.write(" ".join(cmd) + "\n" + res.stdout + res.stderr)
+    if res.returncode != 0:
+        sys.stderr.write(res.stderr)
+        raise RuntimeError(f"nvcc failed for variant {name}")
+    objs = [obj] + [os.path.join(BUILD, u.replace(".cu", ".o")) for u in UNITS if u != "level.cu"]
+    objs.append(os.path.join(BUILD, "datagen.o"))
+    cmd = [nvcc(), *ARCH, "-shared", "-o", lib, *objs, "-lcudart_static", "-lrt", "-ldl", "-lpthread"]
+    res = subprocess.run(cmd, capture_output=True, text=True)
+    if res.returncode != 0:
+        sys.stderr.write(res.stderr)
+        raise RuntimeError("variant link failed")
+    return lib
+
+
 if __name__ == "__main__":
     print(build(verbose="-v" in sys.argv, force="-f" in sys.argv))

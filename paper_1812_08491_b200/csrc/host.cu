@@ -183,6 +183,8 @@ struct pcs_session {
     Counters* dCnt = nullptr;
     unsigned long long* dPrefix = nullptr;
     int32_t *dNbr = nullptr, *dEid = nullptr;
+    unsigned long long* dKdir = nullptr;  // per directed entry: mirror of its edge's key (cuPC-S staging)
+    double* dCnbr = nullptr;              // per directed entry: C(i, nbr)
     long long capDir = 0;
     int32_t *dEuA = nullptr, *dEuQa = nullptr, *dEuQb = nullptr;
     unsigned long long* dKeys = nullptr;
@@ -224,7 +226,7 @@ void free_session(pcs_session* s) {
     };
     if (s->own_c) rel(s->dC);
     rel(s->dAdj); rel(s->dDeg); rel(s->dLow); rel(s->dOff); rel(s->dUp);
-    rel(s->dInfo); rel(s->dCnt); rel(s->dPrefix); rel(s->dNbr); rel(s->dEid);
+    rel(s->dInfo); rel(s->dCnt); rel(s->dPrefix); rel(s->dNbr); rel(s->dEid); rel(s->dKdir); rel(s->dCnbr);
     rel(s->dEuA); rel(s->dEuQa); rel(s->dEuQb); rel(s->dKeys); rel(s->dRec);
     rel(s->dBinom);
     rel(s->dScratch);
@@ -365,6 +367,8 @@ LevelArgs level_args(pcs_session* s) {
     A.eu_qa = s->dEuQa;
     A.eu_qb = s->dEuQb;
     A.keys = s->dKeys;
+    A.kdir = s->dKdir;
+    A.cnbr = s->dCnbr;
     A.binom.t = s->dBinom;
     A.binom.stride = s->binom_stride;
     A.th = s->th;
@@ -513,6 +517,8 @@ pcs_status pcs_session_level_begin(pcs_session* s, int32_t* running, int32_t* el
     if (s->info.e_dir > s->capDir) {
         if ((st = realloc_dev(s, &s->dNbr, s->info.e_dir))) return st;
         if ((st = realloc_dev(s, &s->dEid, s->info.e_dir))) return st;
+        if ((st = realloc_dev(s, &s->dKdir, s->info.e_dir))) return st;
+        if ((st = realloc_dev(s, &s->dCnbr, s->info.e_dir))) return st;
         s->capDir = s->info.e_dir;
     }
     if (s->info.e_und > s->capUnd) {
@@ -539,7 +545,7 @@ pcs_status pcs_session_level_begin(pcs_session* s, int32_t* running, int32_t* el
     if ((st = build_binomials(s, ell, maxw))) return st;
     launch_snapshot_fill(s->dAdj, s->p, s->W, s->dOff, s->dNbr, s->st);
     LevelArgs A = level_args(s);
-    launch_edge_index(A, s->dEid, s->dEuA, s->dEuQa, s->dEuQb, s->st);
+    launch_edge_index(A, s->dEid, s->dEuA, s->dEuQa, s->dEuQb, ell >= 2 ? s->dCnbr : nullptr, s->st);
     launch_fill_keys(s->dKeys, s->info.e_und, s->st);
     CUDA_TRY(cudaGetLastError());
     s->in_level = true;
@@ -591,6 +597,7 @@ pcs_status pcs_session_level_pass(pcs_session* s, int32_t pass) {
                 if (launch_level_set_rt(A, pass, s->dPrefix, u0, u1, s->num_sms, s->dScratch, s->st))
                     return fail(PCS_EUNSUPPORTED, "level not supported by the generic set kernel");
             } else {
+                launch_refresh_kdir(A, s->info.e_dir, s->st);
                 if (launch_level_set(A, pass, s->dPrefix, u0, u1, s->num_sms, s->st))
                     return fail(PCS_EUNSUPPORTED, "level not supported by the set kernel");
             }

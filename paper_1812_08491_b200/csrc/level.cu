@@ -211,13 +211,15 @@ void launch_snapshot_fill(const uint32_t* adj, int p, int W, const int32_t* off,
     snapshot_fill_kernel<<<(p * 32 + 255) / 256, 256, 0, s>>>(adj, p, W, off, nbr);
 }
 
-__global__ void edge_index_kernel(LevelArgs A, int32_t* eid, int32_t* eu_a, int32_t* eu_qa, int32_t* eu_qb) {
+__global__ void edge_index_kernel(LevelArgs A, int32_t* eid, int32_t* eu_a, int32_t* eu_qa, int32_t* eu_qb,
+                                  double* cnbr) {
     const int lane = threadIdx.x & 31;
     const int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     if (i >= A.p) return;
     const int oi = A.off[i], w = A.off[i + 1] - oi, lci = A.lowcnt[i];
     for (int q = lane; q < w; q += 32) {
         const int j = A.nbr[oi + q];
+        if (cnbr) cnbr[oi + q] = __ldg(A.C + (size_t)i * A.ldc + j);
         if (j > i) {
             const int e = A.upoff[i] + (q - lci);
             eid[oi + q] = e;
@@ -238,9 +240,23 @@ __global__ void edge_index_kernel(LevelArgs A, int32_t* eid, int32_t* eu_a, int3
 }
 
 void launch_edge_index(const LevelArgs& A, int32_t* eid, int32_t* eu_a, int32_t* eu_qa, int32_t* eu_qb,
-                       cudaStream_t s) {
+                       double* cnbr, cudaStream_t s) {
     ++g_kernel_launches;
-    edge_index_kernel<<<(A.p * 32 + 255) / 256, 256, 0, s>>>(A, eid, eu_a, eu_qa, eu_qb);
+    edge_index_kernel<<<(A.p * 32 + 255) / 256, 256, 0, s>>>(A, eid, eu_a, eu_qa, eu_qb, cnbr);
+}
+
+__global__ void refresh_kdir_kernel(const int32_t* __restrict__ eid, const unsigned long long* __restrict__ keys,
+                                    unsigned long long* kdir, long long n) {
+    for (long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += (long long)gridDim.x * blockDim.x)
+        kdir[k] = keys[eid[k]];
+}
+
+void launch_refresh_kdir(const LevelArgs& A, long long e_dir, cudaStream_t s) {
+    if (e_dir <= 0) return;
+    long long blocks = (e_dir + 255) / 256;
+    if (blocks > 148 * 16) blocks = 148 * 16;
+    ++g_kernel_launches;
+    refresh_kdir_kernel<<<(int)blocks, 256, 0, s>>>(A.eid, A.keys, A.kdir, e_dir);
 }
 
 __global__ void fill_keys_kernel(unsigned long long* keys, long long n) {
@@ -497,9 +513,24 @@ struct alignas(16) SetSlot {
 
 constexpr int kSetWarps = 4;
 
+#ifndef PCS_SET_DBUF
+#define PCS_SET_DBUF 0      // 1: two unrolled step copies ping-ponging the prefetch registers
+#endif
+
+// The rare candidates' exact decision, out of line: inlined, its log/sqrt/div sequences would be
+// copied into every step instance and crowd the hot loop out of the instruction cache.
+__device__ __noinline__ int decide_slow(double h01, double denom, Thresholds th) { return decide_fast(h01, denom, th); }
+
+#ifndef PCS_SET_NT_SMALL
+#define PCS_SET_NT_SMALL 3  // targets per lane per set for L <= 3 (tuning knob, results identical)
+#endif
+#ifndef PCS_SET_MINB
+#define PCS_SET_MINB 4      // resident blocks per SM the set kernel is register-budgeted for
+#endif
+
 template <int L>
 struct SetCfg {
-    static constexpr int NT = L <= 3 ? 4 : 2;  // targets per lane per set
+    static constexpr int NT = L <= 3 ? PCS_SET_NT_SMALL : 2;  // targets per lane per set
     static constexpr int kStage = 32 * NT;     // live targets staged per pass over the band
 };
 
@@ -578,7 +609,7 @@ __device__ __forceinline__ void h_terms_stream(const SetSlot<L>& sl, const doubl
 // (rank-truncated inputs hit this often: ~29% of C2's level-3 sets), and the last-member
 // prefetch always targets the next LIVE set, so skipped sets cost no L2 round trip either.
 template <int L, int NT>
-__device__ __forceinline__ void set_sweep(const LevelArgs& A, SetWarpSmem<L>& S, int lane, int nlive, int nvalid,
+__device__ __forceinline__ void set_sweep(const LevelArgs& A, SetWarpSmem<L>& S, int lane, int oi, int nlive, int nvalid,
                                           unsigned segmask, unsigned livemask, unsigned long long K0,
                                           unsigned long long& tests, unsigned long long& degen, int& nan) {
     const double* __restrict__ C = A.C;
@@ -668,10 +699,14 @@ __device__ __forceinline__ void set_sweep(const LevelArgs& A, SetWarpSmem<L>& S,
                 for (int t = 0; t < NT; ++t) {
                     if ((cand >> t) & 1u) {
                         const double h01 = 0.5 * cij2[t] - 0.5 * s01[t];  // == c_ij - 0.5 * (d01 + d10)
-                        const int d = decide_fast(h01, den[t], A.th);
+                        const int d = decide_slow(h01, den[t], A.th);
                         if (d != kDependent) {
                             if (d == kNanError) nan = 1;
-                            else atomicMin(A.keys + S.te[t * 32 + lane], K0 + (unsigned long long)sgx);
+                            else {
+                                const int k = t * 32 + lane;
+                                atomicMin(A.keys + S.te[k], K0 + (unsigned long long)sgx);
+                                atomicMin(A.kdir + oi + S.tq[k], K0 + (unsigned long long)sgx);
+                            }
                             rel[t] = sgx;
                             lim[t] = sgx;
                             hit |= 1u << t;
@@ -680,6 +715,7 @@ __device__ __forceinline__ void set_sweep(const LevelArgs& A, SetWarpSmem<L>& S,
                 }
             }
         };
+#if PCS_SET_DBUF
         while (nl < seg_end) {
             int s = nl;
             nl = next_live(s);
@@ -693,6 +729,17 @@ __device__ __forceinline__ void set_sweep(const LevelArgs& A, SetWarpSmem<L>& S,
             nl = next_live(s);
             step(s, nl, alt, nxt);
         }
+#else
+        // one copy of the step body (instruction-cache footprint); the prefetched gathers move to
+        // `nxt` with NT register moves
+        while (nl < seg_end) {
+            const int s = nl;
+            nl = next_live(s);
+            step(s, nl, nxt, alt);
+#pragma unroll
+            for (int t = 0; t < NT; ++t) nxt[t] = alt[t];
+        }
+#endif
         // tests of this run, per target: sets [sg0, hi) minus the member set (serial order); the
         // dead (h00 == 0) ones among them were decided without arithmetic
 #pragma unroll
@@ -709,7 +756,7 @@ __device__ __forceinline__ void set_sweep(const LevelArgs& A, SetWarpSmem<L>& S,
 }
 
 template <int L>
-__global__ void __launch_bounds__(kSetWarps * 32, 3) level_set_kernel(LevelArgs A, int pass,
+__global__ void __launch_bounds__(kSetWarps * 32, PCS_SET_MINB) level_set_kernel(LevelArgs A, int pass,
                                                                      const unsigned long long* prefix,
                                                                      unsigned long long u_begin,
                                                                      unsigned long long u_end) {
@@ -740,29 +787,39 @@ __global__ void __launch_bounds__(kSetWarps * 32, 3) level_set_kernel(LevelArgs 
         unsigned segmask = 1u, livemask = 0u;
         for (int tb = qbeg; tb < qend; tb += kStage) {
             const int tend = min(tb + kStage, qend);
-            // ---- stage the live targets of [tb, tend), compacted
+            // ---- stage the live targets of [tb, tend), compacted: per directed entry the key mirror,
+            // edge id, neighbour and C(i, j) are independent coalesced loads (one round trip)
             int nlive = 0;
-            for (int q0 = tb; q0 < tend; q0 += 32) {
-                const int q = q0 + lane;
-                bool live = false;
-                int e = 0;
-                unsigned long long key = 0;
-                if (q < tend) {
-                    e = A.eid[oi + q];
-                    key = A.keys[e];
-                    live = key > K0;
+            {
+                constexpr int NC = kStage / 32;
+                unsigned long long kk[NC];
+                int ee[NC], jj[NC];
+                double cc[NC];
+#pragma unroll
+                for (int c = 0; c < NC; ++c) {
+                    const int q = tb + c * 32 + lane;
+                    kk[c] = 0;
+                    if (q < tend) {
+                        kk[c] = A.kdir[oi + q];
+                        ee[c] = A.eid[oi + q];
+                        jj[c] = A.nbr[oi + q];
+                        cc[c] = A.cnbr[oi + q];
+                    }
                 }
-                const unsigned bal = __ballot_sync(0xffffffffu, live);
-                if (live) {
-                    const int at = nlive + __popc(bal & lt_mask);
-                    const int j = A.nbr[oi + q];
-                    S.tkey[at] = key;
-                    S.tq[at] = q;
-                    S.tj[at] = j;
-                    S.te[at] = e;
-                    S.tcij[at] = __ldg(C + (size_t)i * ldc + j);
+#pragma unroll
+                for (int c = 0; c < NC; ++c) {
+                    const bool live = kk[c] > K0;
+                    const unsigned bal = __ballot_sync(0xffffffffu, live);
+                    if (live) {
+                        const int at = nlive + __popc(bal & lt_mask);
+                        S.tkey[at] = kk[c];
+                        S.tq[at] = tb + c * 32 + lane;
+                        S.tj[at] = jj[c];
+                        S.te[at] = ee[c];
+                        S.tcij[at] = cc[c];
+                    }
+                    nlive += __popc(bal);
                 }
-                nlive += __popc(bal);
             }
             if (nlive == 0) continue;
             // ---- phase 1 (once per unit): lane-parallel pseudo-inverses of the band's sets
@@ -818,13 +875,17 @@ __global__ void __launch_bounds__(kSetWarps * 32, 3) level_set_kernel(LevelArgs 
             // ---- phase 2: sets in rank order, NT targets per lane
             const int nt = (nlive + 31) >> 5;
             if constexpr (SetCfg<L>::NT == 4) {
-                if (nt == 4) set_sweep<L, 4>(A, S, lane, nlive, nvalid, segmask, livemask, K0, tests, degen, nan);
-                else if (nt == 3) set_sweep<L, 3>(A, S, lane, nlive, nvalid, segmask, livemask, K0, tests, degen, nan);
-                else if (nt == 2) set_sweep<L, 2>(A, S, lane, nlive, nvalid, segmask, livemask, K0, tests, degen, nan);
-                else set_sweep<L, 1>(A, S, lane, nlive, nvalid, segmask, livemask, K0, tests, degen, nan);
+                if (nt == 4) set_sweep<L, 4>(A, S, lane, oi, nlive, nvalid, segmask, livemask, K0, tests, degen, nan);
+                else if (nt == 3) set_sweep<L, 3>(A, S, lane, oi, nlive, nvalid, segmask, livemask, K0, tests, degen, nan);
+                else if (nt == 2) set_sweep<L, 2>(A, S, lane, oi, nlive, nvalid, segmask, livemask, K0, tests, degen, nan);
+                else set_sweep<L, 1>(A, S, lane, oi, nlive, nvalid, segmask, livemask, K0, tests, degen, nan);
+            } else if constexpr (SetCfg<L>::NT == 3) {
+                if (nt == 3) set_sweep<L, 3>(A, S, lane, oi, nlive, nvalid, segmask, livemask, K0, tests, degen, nan);
+                else if (nt == 2) set_sweep<L, 2>(A, S, lane, oi, nlive, nvalid, segmask, livemask, K0, tests, degen, nan);
+                else set_sweep<L, 1>(A, S, lane, oi, nlive, nvalid, segmask, livemask, K0, tests, degen, nan);
             } else {
-                if (nt == 2) set_sweep<L, 2>(A, S, lane, nlive, nvalid, segmask, livemask, K0, tests, degen, nan);
-                else set_sweep<L, 1>(A, S, lane, nlive, nvalid, segmask, livemask, K0, tests, degen, nan);
+                if (nt == 2) set_sweep<L, 2>(A, S, lane, oi, nlive, nvalid, segmask, livemask, K0, tests, degen, nan);
+                else set_sweep<L, 1>(A, S, lane, oi, nlive, nvalid, segmask, livemask, K0, tests, degen, nan);
             }
             __syncwarp();
         }

@@ -52,6 +52,9 @@ struct LevelArgs {
     const int32_t* eu_qa;    // E: position of b in row a
     const int32_t* eu_qb;    // E: position of a in row b
     unsigned long long* keys;  // E
+    unsigned long long* kdir;  // 2E: keys[eid[k]] mirrored per directed entry (cuPC-S staging reads it
+                               //     coalesced, no dependent gather); refreshed before every pass
+    const double* cnbr;        // 2E: C(i, nbr[k]) of the directed entry k of row i (filled per level)
     BinomTable binom;
     Thresholds th;
     Counters* cnt;
@@ -71,7 +74,9 @@ void launch_snapshot_scan(const int32_t* deg, const int32_t* lowcnt, int p, int3
                           SnapInfo* info, cudaStream_t s);
 void launch_snapshot_fill(const uint32_t* adj, int p, int W, const int32_t* off, int32_t* nbr, cudaStream_t s);
 void launch_edge_index(const LevelArgs& A, int32_t* eid, int32_t* eu_a, int32_t* eu_qa, int32_t* eu_qb,
-                       cudaStream_t s);
+                       double* cnbr, cudaStream_t s);
+// kdir[k] = keys[eid[k]] for every directed entry (before each cuPC-S pass)
+void launch_refresh_kdir(const LevelArgs& A, long long e_dir, cudaStream_t s);
 void launch_fill_keys(unsigned long long* keys, long long n, cudaStream_t s);
 // per-row work prefix for a pass (units of work: target tiles for ell=1, set bands for ell>=2,
 // restricted to [row_begin,row_end) for sharding); returns nothing, writes prefix[p+1]

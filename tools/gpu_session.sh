@@ -31,6 +31,9 @@ for s in $STEPS; do
       timeout 600 python tools/shard_balance.py 8 C3 -1 set >> $OUT/balance.json 2>> $OUT/balance.err
       timeout 600 python tools/shard_balance.py 8 C2 2 edge >> $OUT/balance.json 2>> $OUT/balance.err
       ;;
+    variants)
+      timeout 900 python tools/variants.py run --workload C2 --max-level 3 --repeats 2 > $OUT/variants.json 2> $OUT/variants.err
+      ;;
     bench)
       timeout 900 python bench.py > $OUT/bench.json 2> $OUT/bench.err
       ;;
