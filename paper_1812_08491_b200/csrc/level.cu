@@ -23,6 +23,25 @@ namespace pcs {
 
 unsigned long long g_kernel_launches = 0;
 
+#ifndef PCS_SET_DBUF
+#define PCS_SET_DBUF 0      // 1: two unrolled step copies ping-ponging the prefetch registers
+#endif
+
+// The rare candidates' exact decision, out of line: inlined, its log/sqrt/div sequences would be
+// copied into every step instance and crowd the hot loop out of the instruction cache.
+__device__ __noinline__ int decide_slow(double h01, double denom, Thresholds th) { return decide_fast(h01, denom, th); }
+
+#ifndef PCS_SET_NT_SMALL
+#define PCS_SET_NT_SMALL 3  // targets per lane per set for L <= 3 (tuning knob, results identical)
+#endif
+#ifndef PCS_SET_SP
+#define PCS_SET_SP 2        // sets per step for one-target-per-lane batches (L <= 3)
+#endif
+#ifndef PCS_SET_MINB
+#define PCS_SET_MINB 4      // resident blocks per SM the set kernel is register-budgeted for
+#endif
+
+
 namespace {
 
 __device__ __forceinline__ unsigned long long warp_sum(unsigned long long v) {
@@ -39,6 +58,20 @@ __device__ __forceinline__ void add_counter(unsigned long long* dst, unsigned lo
 // largest r in [0, n) with prefix[r] <= u (prefix non-decreasing, prefix[0] = 0)
 __device__ __forceinline__ int find_row(const unsigned long long* prefix, int n, unsigned long long u) {
     int lo = 0, hi = n - 1;
+    while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (__ldg(prefix + mid) <= u) lo = mid; else hi = mid - 1;
+    }
+    return lo;
+}
+
+// Same, for a warp whose units only increase: `hint` is the row of its previous unit.  The hint's
+// bracket is two independent loads (one round trip) and almost always hits (a C2 level-3 row has
+// ~20k units); otherwise a binary search over the rows after the hint.
+__device__ __forceinline__ int find_row_from(const unsigned long long* prefix, int n, unsigned long long u, int hint) {
+    const unsigned long long a = __ldg(prefix + hint), b = __ldg(prefix + hint + 1);
+    if (a <= u && u < b) return hint;
+    int lo = u < a ? 0 : hint + 1, hi = n - 1;
     while (lo < hi) {
         const int mid = (lo + hi + 1) >> 1;
         if (__ldg(prefix + mid) <= u) lo = mid; else hi = mid - 1;
@@ -292,8 +325,11 @@ __global__ void row_work_kernel(LevelArgs A, int pass, int variant, int row_begi
             u = (unsigned long long)((ntar + kL1Threads - 1) / kL1Threads);
             c = u * (unsigned long long)(w + 8);
         } else {
+            // a band's sweep walks its 32 sets once per staged batch of targets (a step costs about the
+            // same whatever the batch's fill), plus a fixed part (cursor, staging, 32 pseudo-inverses)
+            const int stage = A.ell <= 3 ? 32 * PCS_SET_NT_SMALL : 64;
             u = (A.binom(w, A.ell) + kSetBand - 1) / kSetBand;
-            c = u * (unsigned long long)(ntar + 32);
+            c = u * (unsigned long long)(8 * ((ntar + stage - 1) / stage) + 3);
         }
     }
     units[i] = u;
@@ -513,21 +549,6 @@ struct alignas(16) SetSlot {
 
 constexpr int kSetWarps = 4;
 
-#ifndef PCS_SET_DBUF
-#define PCS_SET_DBUF 0      // 1: two unrolled step copies ping-ponging the prefetch registers
-#endif
-
-// The rare candidates' exact decision, out of line: inlined, its log/sqrt/div sequences would be
-// copied into every step instance and crowd the hot loop out of the instruction cache.
-__device__ __noinline__ int decide_slow(double h01, double denom, Thresholds th) { return decide_fast(h01, denom, th); }
-
-#ifndef PCS_SET_NT_SMALL
-#define PCS_SET_NT_SMALL 3  // targets per lane per set for L <= 3 (tuning knob, results identical)
-#endif
-#ifndef PCS_SET_MINB
-#define PCS_SET_MINB 4      // resident blocks per SM the set kernel is register-budgeted for
-#endif
-
 template <int L>
 struct SetCfg {
     static constexpr int NT = L <= 3 ? PCS_SET_NT_SMALL : 2;  // targets per lane per set
@@ -596,6 +617,172 @@ __device__ __forceinline__ void h_terms_stream(const SetSlot<L>& sl, const doubl
         s01[t] = d01[t] + d10[t];
         h2[t] = cij2[t] - s01[t];
         den[t] = h00 * h11;
+    }
+}
+
+// h_terms for ONE target against SP sets of the same run (shared leading members cp, per-set
+// last-member gather cur[k]): the same per-accumulator rounding sequence as h_terms_stream.
+template <int L, int SP, int LP>
+__device__ __forceinline__ void h_terms_sp(const SetSlot<L>* const (&sl)[SP], const double (&cp)[LP],
+                                           const double (&cur)[SP], double cij2, double (&s01)[SP],
+                                           double (&h2)[SP], double (&den)[SP]) {
+    double d11[SP], d01[SP], d10[SP];
+#pragma unroll
+    for (int col = 0; col < L; ++col) {
+#pragma unroll
+        for (int k = 0; k < SP; ++k) {
+            double cv[SetSlot<L>::CW];
+#pragma unroll
+            for (int c = 0; c < SetSlot<L>::CW; c += 2) {
+                const double2 v = *reinterpret_cast<const double2*>(&sl[k]->col[col][c]);
+                cv[c] = v.x;
+                cv[c + 1] = v.y;
+            }
+            const double ci = cv[L], pc = cv[L + 1];
+            double x[L];
+#pragma unroll
+            for (int a = 0; a < L - 1; ++a) x[a] = cp[a];
+            x[L - 1] = cur[k];
+            double pcol = x[0] * cv[0];
+#pragma unroll
+            for (int q = 1; q < L; ++q) pcol = pcol + x[q] * cv[q];
+            if (col == 0) {
+                d11[k] = pcol * x[0];
+                d01[k] = pc * x[0];
+                d10[k] = pcol * ci;
+            } else {
+                d11[k] = d11[k] + pcol * x[col];
+                d01[k] = d01[k] + pc * x[col];
+                d10[k] = d10[k] + pcol * ci;
+            }
+        }
+    }
+#pragma unroll
+    for (int k = 0; k < SP; ++k) {
+        const double h11 = 1.0 - d11[k];
+        s01[k] = d01[k] + d10[k];
+        h2[k] = cij2 - s01[k];
+        den[k] = sl[k]->h00 * h11;
+    }
+}
+
+// Phase 2 for a batch of at most 32 targets (one per lane): a one-target step would be a single
+// dependent FP64 chain per lane (latency-bound), so each step tests the lane's target against SP
+// consecutive live sets of the current run instead (SP independent chains).  Sets are still settled
+// in rank order: the first separating set among the SP wins and later ones are discarded.  Same
+// results and counters as set_sweep<L, 1>.
+template <int L, int SP>
+__device__ __forceinline__ void set_sweep_sp(const LevelArgs& A, SetWarpSmem<L>& S, int lane, int oi, int nlive,
+                                             int nvalid, unsigned segmask, unsigned livemask,
+                                             unsigned long long K0, unsigned long long& tests,
+                                             unsigned long long& degen, int& nan) {
+    const double* __restrict__ C = A.C;
+    const double hi2x4 = 4.0 * A.th.hi2;
+    const bool have = lane < nlive;
+    int rel = -1;
+    const double* Cj = C;
+    double cij2 = 0.0;
+    if (have) {
+        const unsigned long long d = S.tkey[lane] - K0;
+        rel = d > 0x3fffffffull ? 0x3fffffff : (int)d;
+        Cj = C + S.tj[lane];
+        const double c = S.tcij[lane];
+        cij2 = c + c;
+    }
+    const int q = have ? S.tq[lane] : -1;
+    constexpr int LP = L > 1 ? L - 1 : 1;
+    const unsigned valid_mask = nvalid >= 32 ? 0xffffffffu : ((1u << nvalid) - 1u);
+    segmask &= valid_mask;
+    const unsigned live = livemask & valid_mask, dead = valid_mask & ~livemask;
+    auto next_live = [&](int x) -> int {
+        const unsigned m = live & ~((2u << x) - 1u);
+        return m ? __ffs(m) - 1 : nvalid;
+    };
+    auto run_end = [&](int x) -> int {
+        const unsigned m = segmask & ~((2u << x) - 1u);
+        return m ? __ffs(m) - 1 : nvalid;
+    };
+    // a group: up to SP consecutive live sets of one run (g[k] = nvalid: empty item); returns the
+    // first live set after the group
+    auto gather_group = [&](int first, int (&g)[SP], double (&buf)[SP]) -> int {
+        const int re = first < nvalid ? run_end(first) : nvalid;
+        int x = first;
+#pragma unroll
+        for (int k = 0; k < SP; ++k) {
+            const bool ok = x < re;
+            g[k] = ok ? x : nvalid;
+            buf[k] = __ldg(Cj + S.slot[ok ? x : (first < nvalid ? first : nvalid - 1)].roff[L - 1]);
+            if (ok) x = next_live(x);
+        }
+        return x;
+    };
+    double cp[LP];
+    int g[SP];
+    double nxt[SP];
+    int after = gather_group(live ? __ffs(live) - 1 : nvalid, g, nxt);
+    int sg = 0;
+    while (sg < nvalid) {
+        const int sg0 = sg;
+        const int seg_end = run_end(sg0);
+        const SetSlot<L>& sl0 = S.slot[sg0];
+        const int base = sl0.pos[L - 1];
+        if (g[0] < seg_end) {
+#pragma unroll
+            for (int a = 0; a < L - 1; ++a) cp[a] = __ldg(Cj + sl0.roff[a]);
+        }
+        bool pm = false;
+#pragma unroll
+        for (int a = 0; a < L - 1; ++a) pm |= sl0.pos[a] == q;
+        int lim = pm ? -1 : rel;
+        const int dm = sg0 + q - base;
+        bool hit = false;
+        while (g[0] < seg_end) {
+            int gn[SP];
+            double alt[SP];
+            const int after2 = gather_group(after, gn, alt);
+            const SetSlot<L>* sls[SP];
+#pragma unroll
+            for (int k = 0; k < SP; ++k) sls[k] = &S.slot[g[k] < nvalid ? g[k] : g[0]];
+            double s01[SP], h2[SP], den[SP];
+            h_terms_sp<L, SP, LP>(sls, cp, nxt, cij2, s01, h2, den);
+            unsigned cand = 0;
+#pragma unroll
+            for (int k = 0; k < SP; ++k)
+                cand |= (unsigned)((g[k] < seg_end) & (g[k] < lim) & (g[k] != dm) &
+                                   !surely_dependent2(h2[k], den[k], hi2x4)) << k;
+            if (__any_sync(0xffffffffu, cand)) {
+#pragma unroll
+                for (int k = 0; k < SP; ++k) {
+                    if (((cand >> k) & 1u) && g[k] < lim) {
+                        const double h01 = 0.5 * cij2 - 0.5 * s01[k];
+                        const int d = decide_slow(h01, den[k], A.th);
+                        if (d != kDependent) {
+                            if (d == kNanError) nan = 1;
+                            else {
+                                atomicMin(A.keys + S.te[lane], K0 + (unsigned long long)g[k]);
+                                atomicMin(A.kdir + oi + q, K0 + (unsigned long long)g[k]);
+                            }
+                            rel = g[k];
+                            lim = g[k];
+                            hit = true;
+                        }
+                    }
+                }
+            }
+#pragma unroll
+            for (int k = 0; k < SP; ++k) {
+                g[k] = gn[k];
+                nxt[k] = alt[k];
+            }
+            after = after2;
+        }
+        const int hi = hit ? lim + 1 : min(seg_end, lim);
+        const int n = max(0, hi - sg0);
+        const bool in = dm >= sg0 && dm < sg0 + n;
+        tests += (unsigned)(n - (in ? 1 : 0));
+        const unsigned rm = n >= 32 ? 0xffffffffu : (((1u << n) - 1u) << sg0);
+        degen += (unsigned)(__popc(dead & rm) - ((in && ((dead >> dm) & 1u)) ? 1 : 0));
+        sg = seg_end;
     }
 }
 
@@ -771,12 +958,17 @@ __global__ void __launch_bounds__(kSetWarps * 32, PCS_SET_MINB) level_set_kernel
     unsigned long long tests = 0, pinvs = 0, degen = 0;
     int nan = 0;
     unsigned long long* cursor = &A.cnt->units[pass];
+    int row_hint = 0;
+    // the next unit is grabbed one unit ahead (lane 0's atomic result is only read at the top of the
+    // next iteration), so the cursor round trip overlaps the current unit's work
+    unsigned long long grabbed = 0;
+    if (lane == 0) grabbed = atomicAdd(cursor, 1ull);
     for (;;) {
-        unsigned long long u = 0;
-        if (lane == 0) u = u_begin + atomicAdd(cursor, 1ull);
-        u = __shfl_sync(0xffffffffu, u, 0);
+        const unsigned long long u = u_begin + __shfl_sync(0xffffffffu, grabbed, 0);
         if (u >= u_end) break;
-        const int i = find_row(prefix, A.p, u);
+        if (lane == 0) grabbed = atomicAdd(cursor, 1ull);
+        const int i = find_row_from(prefix, A.p, u, row_hint);
+        row_hint = i;
         const unsigned long long t0 = (u - prefix[i]) * kSetBand;
         const int oi = A.off[i], w = A.off[i + 1] - oi, lc = A.lowcnt[i];
         const int qbeg = pass == 0 ? lc : 0, qend = pass == 0 ? w : lc;
@@ -882,10 +1074,10 @@ __global__ void __launch_bounds__(kSetWarps * 32, PCS_SET_MINB) level_set_kernel
             } else if constexpr (SetCfg<L>::NT == 3) {
                 if (nt == 3) set_sweep<L, 3>(A, S, lane, oi, nlive, nvalid, segmask, livemask, K0, tests, degen, nan);
                 else if (nt == 2) set_sweep<L, 2>(A, S, lane, oi, nlive, nvalid, segmask, livemask, K0, tests, degen, nan);
-                else set_sweep<L, 1>(A, S, lane, oi, nlive, nvalid, segmask, livemask, K0, tests, degen, nan);
+                else set_sweep_sp<L, PCS_SET_SP>(A, S, lane, oi, nlive, nvalid, segmask, livemask, K0, tests, degen, nan);
             } else {
                 if (nt == 2) set_sweep<L, 2>(A, S, lane, oi, nlive, nvalid, segmask, livemask, K0, tests, degen, nan);
-                else set_sweep<L, 1>(A, S, lane, oi, nlive, nvalid, segmask, livemask, K0, tests, degen, nan);
+                else set_sweep_sp<L, 2>(A, S, lane, oi, nlive, nvalid, segmask, livemask, K0, tests, degen, nan);
             }
             __syncwarp();
         }
