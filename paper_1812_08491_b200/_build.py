@@ -92,9 +92,10 @@ def build(verbose: bool = False, force: bool = False) -> str:
     return LIB
 
 
-def build_variant(name: str, defines: list[str]) -> str:
+def build_variant(name: str, defines: list[str], source: str | None = None) -> str:
     """Tuning experiments (tools/variants.py): the library with level.cu rebuilt under extra -D knobs
-    into variants/libpcstable_b200_<name>.so (knobs never change results)."""
+    (or from another level.cu `source`, e.g. an older revision for A/B timing) into
+    variants/libpcstable_b200_<name>.so (knobs never change results)."""
     build()
     vdir = os.path.join(BUILD, "var_" + name)
     os.makedirs(vdir, exist_ok=True)
@@ -103,7 +104,7 @@ def build_variant(name: str, defines: list[str]) -> str:
     lib = os.path.join(out_dir, f"libpcstable_b200_{name}.so")
     obj = os.path.join(vdir, "level.o")
     cmd = [nvcc(), *ARCH, *COMMON, *UNITS["level.cu"], *[f"-D{d}" for d in defines], "-c",
-           os.path.join(CSRC, "level.cu"), "-o", obj]
+           source or os.path.join(CSRC, "level.cu"), "-o", obj]
     res = subprocess.run(cmd, capture_output=True, text=True)
     with open(os.path.join(vdir, "level.cu.ptxas.log"), "w") as f:
         f.write(" ".join(cmd) + "\n" + res.stdout + res.stderr)

@@ -1,6 +1,7 @@
 """Tuning experiments: build (here) and time (on the GPU box) level.cu variants under -D knobs.
 
   python tools/variants.py build NAME=DEF1,DEF2 ...    # e.g. nt3=PCS_SET_NT_SMALL=3 minb4=PCS_SET_MINB=4
+  python tools/variants.py build NAME=@REV              # level.cu of git revision REV (A/B timing)
   python tools/variants.py run [NAME ...] [--workload C2 --max-level 3 --repeats 2]
 
 `run` times the full level loop of the workload per variant (CUDA-event kernel time per level) and
@@ -22,10 +23,21 @@ def cmd_build(specs):
 
     from paper_1812_08491_b200 import _build
     _build.build()
+    import subprocess
     jobs = []
     for spec in specs:
         name, _, defs = spec.partition("=")
-        jobs.append((name, [d for d in defs.split(",") if d]))
+        if defs.startswith("@"):  # NAME=@REV: level.cu (and pcs_device.cuh) as of git revision REV
+            rev = defs[1:]
+            d = os.path.join(ROOT, "paper_1812_08491_b200", "build", "rev_" + name)
+            os.makedirs(d, exist_ok=True)
+            for f in ("level.cu", "pcs_device.cuh", "pcs_internal.h"):
+                src = subprocess.run(["git", "show", f"{rev}:paper_1812_08491_b200/csrc/{f}"], cwd=ROOT,
+                                     capture_output=True, text=True, check=True).stdout
+                open(os.path.join(d, f), "w").write(src)
+            jobs.append((name, [], os.path.join(d, "level.cu")))
+        else:
+            jobs.append((name, [d for d in defs.split(",") if d], None))
     with ThreadPoolExecutor(max_workers=8) as ex:
         for lib in ex.map(lambda j: _build.build_variant(*j), jobs):
             print("built", lib)
