@@ -15,7 +15,10 @@
 #include <cstdarg>
 #include <cstdlib>
 #include <cstring>
+#include <memory>
+#include <new>
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "../../include/pcstable_b200.h"
@@ -157,13 +160,28 @@ bool binomial_exact(int n, int k, unsigned long long* out) {
 }  // namespace
 
 // ================================================================ result
+template <class T>
+struct NoInitAlloc : std::allocator<T> {
+    template <class U>
+    struct rebind { using other = NoInitAlloc<U>; };
+    NoInitAlloc() = default;
+    template <class U>
+    NoInitAlloc(const NoInitAlloc<U>&) noexcept {}
+    template <class U>
+    void construct(U* ptr) noexcept { ::new (static_cast<void*>(ptr)) U; }
+    template <class U, class... Args>
+    void construct(U* ptr, Args&&... args) { ::new (static_cast<void*>(ptr)) U(std::forward<Args>(args)...); }
+};
+
 struct pcs_result {
     int p = 0;
     int W = 0;
     int stop_reason = PCS_STOP_MAX_DEGREE;
     std::vector<pcs_level_stats> levels;
     std::vector<uint32_t> adj;                 // final live bitmask, p x W
-    std::vector<int32_t> recs;                 // flattened (a, b, ell, members...) of level >= 1 removals
+    // flattened (a, b, ell, members...) of level >= 1 removals, copied straight from the device pool
+    // (default-initialised elements: no zero fill before the copy)
+    std::vector<int32_t, NoInitAlloc<int32_t>> recs;
     double device_seconds = 0.0;
 };
 
@@ -189,10 +207,8 @@ struct pcs_session {
     int32_t *dEuA = nullptr, *dEuQa = nullptr, *dEuQb = nullptr;
     unsigned long long* dKeys = nullptr;
     long long capUnd = 0;
-    int32_t* dRec = nullptr;       // record pool: per level, count x (2 + ell) ints
+    int32_t* dRec = nullptr;       // record pool: per level, count x (3 + ell) ints
     long long capRec = 0, recUsed = 0;
-    struct LevelRecs { int ell; long long offset, count; };
-    std::vector<LevelRecs> recLevels;
     unsigned long long* dBinom = nullptr;
     size_t capBinom = 0;
     unsigned char* dScratch = nullptr;  // generic-ell per-lane scratch
@@ -529,7 +545,7 @@ pcs_status pcs_session_level_begin(pcs_session* s, int32_t* running, int32_t* el
         s->capUnd = s->info.e_und;
     }
     {
-        const long long need = s->recUsed + s->info.e_und * (2 + ell);
+        const long long need = s->recUsed + s->info.e_und * (3 + ell);
         if (need > s->capRec) {  // grow the record pool, keeping earlier levels' records
             const long long cap = std::max(need, s->capRec * 3 / 2);
             int32_t* np = nullptr;
@@ -676,8 +692,7 @@ pcs_status pcs_session_level_end(pcs_session* s) {
         L.device_pseudo_inverses = c.gpu_pinv;
         L.device_exact_tests = c.gpu_exact;
         if (c.rec_count) {
-            s->recLevels.push_back({s->ell, s->recUsed, (long long)c.rec_count});
-            s->recUsed += (long long)c.rec_count * (2 + s->ell);
+            s->recUsed += (long long)c.rec_count * (3 + s->ell);
         }
     }
     L.edges_removed = c.removed;
@@ -703,23 +718,10 @@ pcs_status pcs_session_finish(pcs_session* s, pcs_result** out) {
     r->W = s->W;
     r->stop_reason = s->stop_reason;
     r->levels = s->levels;
-    if (s->recUsed) {  // one copy of the record pool, re-laid out as (a, b, ell, members...)
-        std::vector<int32_t> pool((size_t)s->recUsed);
-        CUDA_TRY(cudaMemcpyAsync(pool.data(), s->dRec, sizeof(int32_t) * pool.size(), cudaMemcpyDeviceToHost, s->st));
-        CUDA_TRY(cudaStreamSynchronize(s->st));
-        size_t total = 0;
-        for (const auto& L : s->recLevels) total += (size_t)L.count * (3 + L.ell);
-        r->recs.resize(total);
-        size_t at = 0;
-        for (const auto& L : s->recLevels) {
-            const int32_t* src = pool.data() + L.offset;
-            for (long long k = 0; k < L.count; ++k, src += 2 + L.ell) {
-                r->recs[at++] = src[0];
-                r->recs[at++] = src[1];
-                r->recs[at++] = L.ell;
-                for (int q = 0; q < L.ell; ++q) r->recs[at++] = src[2 + q];
-            }
-        }
+    if (s->recUsed) {  // the pool already holds (a, b, ell, members...) records, level after level
+        r->recs.resize((size_t)s->recUsed);
+        CUDA_TRY(cudaMemcpyAsync(r->recs.data(), s->dRec, sizeof(int32_t) * r->recs.size(), cudaMemcpyDeviceToHost,
+                                 s->st));
     }
     r->adj.resize((size_t)s->p * s->W);
     CUDA_TRY(cudaMemcpyAsync(r->adj.data(), s->dAdj, sizeof(uint32_t) * r->adj.size(), cudaMemcpyDeviceToHost, s->st));
@@ -735,17 +737,28 @@ pcs_status pcs_session_finish(pcs_session* s, pcs_result** out) {
 void pcs_session_free(pcs_session* s) { free_session(s); }
 
 static pcs_status run_session(pcs_session* s, pcs_result** out) {
+    double tb = 0, tp = 0, te = 0;  // PCS_TRACE: host time in level_begin / passes / level_end
     for (;;) {
         int32_t running = 0, ell = 0;
         int64_t nk = 0;
+        double t = now_s();
         pcs_status st = pcs_session_level_begin(s, &running, &ell, &nk);
+        tb += now_s() - t;
         if (st) return st;
         if (!running) break;
+        t = now_s();
         if ((st = pcs_session_level_pass(s, 0))) return st;
         if ((st = pcs_session_level_pass(s, 1))) return st;
+        tp += now_s() - t;
+        t = now_s();
         if ((st = pcs_session_level_end(s))) return st;
+        te += now_s() - t;
     }
-    return pcs_session_finish(s, out);
+    const double t = now_s();
+    pcs_status st = pcs_session_finish(s, out);
+    trace("run_session: level_begin %.2f ms, passes %.2f ms, level_end %.2f ms, finish %.2f ms", tb * 1e3, tp * 1e3,
+          te * 1e3, (now_s() - t) * 1e3);
+    return st;
 }
 
 pcs_status pcs_run_pc_stable(const double* c, int32_t p, int32_t m, const pcs_config* cfg, pcs_result** out) {

@@ -1410,7 +1410,7 @@ int launch_pinv_batch_rt(const double* a, int ell, long long n, double* out, dou
 // =========================================================== commit
 // One thread per undirected snapshot edge: decode the key (full-row rank in
 // the deciding row), clear the edge in the live bitmask, append the sepset
-// record (a, b, members...) and accumulate the serial strategy's ci_tests
+// record (a, b, ell, members...) and accumulate the serial strategy's ci_tests
 // (test_edge_over_sets counts, skeleton.hpp:140-158).
 __global__ void commit_kernel(LevelArgs A, uint32_t* adj, int W, long long e_und, int32_t* rec) {
     const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
@@ -1439,11 +1439,12 @@ __global__ void commit_kernel(LevelArgs A, uint32_t* adj, int W, long long e_und
             atomicAnd(adj + (size_t)a * W + (b >> 5), ~(1u << (b & 31)));
             atomicAnd(adj + (size_t)b * W + (a >> 5), ~(1u << (a & 31)));
             const unsigned long long slot = atomicAdd(&A.cnt->rec_count, 1ull);
-            int32_t* out = rec + slot * (size_t)(2 + ell);
+            int32_t* out = rec + slot * (size_t)(3 + ell);  // the result's final layout: no host re-layout
             out[0] = a;
             out[1] = b;
+            out[2] = ell;
             const int orow = A.off[r];
-            for (int k = 0; k < ell; ++k) out[2 + k] = A.nbr[orow + pos[k]];
+            for (int k = 0; k < ell; ++k) out[3 + k] = A.nbr[orow + pos[k]];
         }
     }
     add_counter(&A.cnt->ci_serial, tests);

@@ -22,6 +22,15 @@ for s in $STEPS; do
     c2)
       timeout 600 python tools/explore.py C2 set 3 > $OUT/explore_c2.log 2>&1
       ;;
+    ncutraffic)
+      timeout 900 ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum --clock-control none \
+        -k regex:level_set_kernel --csv --log-file $OUT/traffic.csv \
+        python bench.py --steps 1 --warmup 0 --no-cpu-baseline --no-e2e --no-secondary > $OUT/ncu_traffic.log 2>&1
+      ;;
+    trace)
+      PCS_TRACE=1 timeout 600 python bench.py --workload C3 --steps 2 --warmup 2 --no-cpu-baseline --no-e2e \
+        --no-secondary > $OUT/trace_c3.json 2> $OUT/trace_c3.err
+      ;;
     ncufull)
       timeout 900 ncu --set full --clock-control none --import-source on -k regex:level_set --launch-skip 2 -c 1 -f -o $OUT/top \
         python tools/profile_target.py 3 32 set > $OUT/ncu_full.log 2>&1
