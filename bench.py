@@ -48,14 +48,29 @@ WORKLOADS = {
     "C2": dict(p=1000, m=10000, d=0.1, alpha=0.01, case=1, max_level=3),
     "C3": dict(p=1643, m=850, d=0.01, alpha=0.01, case=2, max_level=None),
     "C4": dict(p=5361, m=63, d=0.002, alpha=0.01, case=3, max_level=None),
+    # BASELINE configs[4] (scaling sweep p=2000-20000, n=5000): the p=5000, density 0.05 point, per-column-
+    # rescaled generator (same correlation, no overflow at the sweep's larger shapes), capped at level 1
+    # (level 2 of this shape is 7.4e13 serial CI tests, ~100 s on one B200)
+    "C5": dict(p=5000, m=5000, d=0.05, alpha=0.01, case=4, max_level=1, rescaled=True),
 }
 SNAPSHOT_FIXTURE = os.path.join(ROOT, "tests", "golden", "c2_level3_snapshot.npz")
 
 
 def describe(name: str, wl: dict) -> str:
     cap = f", max_level={wl['max_level']}" if wl["max_level"] is not None else ""
+    gen = ", rescaled generator" if wl.get("rescaled") else ""
     return (f"{name}: p={wl['p']}, m={wl['m']} (BASELINE n), density={wl['d']:.6g}, alpha={wl['alpha']}"
-            f"{cap}, seed={7919 * wl['case']}")
+            f"{cap}, seed={7919 * wl['case']}{gen}")
+
+
+def generate(pcs, wl: dict):
+    """(m, p) data of a workload with the reference generator (datagen.hpp:42-82), or its per-column-
+    rescaled variant for the scaling shapes."""
+    seed = 7919 * wl["case"]
+    w = pcs.random_dag(wl["p"], wl["d"], seed)
+    if wl.get("rescaled"):
+        return pcs.sample_linear_gaussian_rescaled(w, wl["m"], seed + 1)[0]
+    return pcs.sample_linear_gaussian(w, wl["m"], seed + 1)
 
 
 def flops_per_level(ell: int, tests: int, pinvs: int) -> float:
@@ -237,8 +252,7 @@ def main():
     dev = torch.cuda.current_device()
     p, m = wl["p"], wl["m"]
     seed = 7919 * wl["case"]
-    w = pcs.random_dag(p, wl["d"], seed)
-    x = pcs.sample_linear_gaussian(w, m, seed + 1)  # (m, p), column-major like Eigen
+    x = generate(pcs, wl)  # (m, p), column-major like Eigen
     x_host = np.ascontiguousarray(x.T)               # row j = variable j
     x_dev = torch.from_numpy(x_host).to(f"cuda:{dev}")
     ldc = (p + 3) // 4 * 4
@@ -328,12 +342,11 @@ def main():
     # full (uncapped) runs of the other single-GPU BASELINE shapes, same device timing
     secondary = []
     if world == 1 and not args.no_secondary:
-        for sname in ("C3", "C4"):
+        for sname in ("C3", "C4", "C5"):
             if sname == name:
                 continue
             swl = dict(WORKLOADS[sname])
-            sseed = 7919 * swl["case"]
-            sx = pcs.sample_linear_gaussian(pcs.random_dag(swl["p"], swl["d"], sseed), swl["m"], sseed + 1)
+            sx = generate(pcs, swl)
             sx_dev = torch.from_numpy(np.ascontiguousarray(sx.T)).to(f"cuda:{dev}")
             scfg = pcs.SkeletonConfig(alpha=swl["alpha"], max_level=swl["max_level"], strategy=cfg.strategy,
                                       device=dev, stream=stream.cuda_stream)

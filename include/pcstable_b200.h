@@ -144,6 +144,11 @@ pcs_status pcs_pseudo_inverse_batch(const double* a, int32_t ell, int64_t n, dou
    j causes i, j < i); sample_linear_gaussian (datagen.hpp:62-82) -> x m x n column-major. */
 pcs_status pcs_random_dag(int32_t n, double density, uint64_t seed, double* weights);
 pcs_status pcs_sample_linear_gaussian(const double* weights, int32_t n, int32_t m, uint64_t seed, double* x);
+/* Overflow-safe sample_linear_gaussian for the scaling shapes (no reference counterpart):
+ * same noise stream, every variable scaled to unit RMS, log_scale[n] = log of the reference variable's RMS,
+ * so x_ref[i] = x[i] * exp(log_scale[i]) and the correlation matrix is the reference generator's. */
+pcs_status pcs_sample_linear_gaussian_rescaled(const double* weights, int32_t n, int32_t m, uint64_t seed, double* x,
+                                               double* log_scale);
 
 /* Level-stepped session: the building block of multi-GPU runs (one process per GPU, the caller
    all-reduces the per-level key array with MIN between passes).  pcs_run_pc_stable is a session

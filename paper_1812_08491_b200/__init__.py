@@ -114,6 +114,7 @@ def library():
     L.pcs_run_pc_stable_data_device.argtypes = [vp, ct.c_int32, ct.c_int32, ct.POINTER(_Config), ct.POINTER(vp), ip]
     L.pcs_random_dag.argtypes = [ct.c_int32, ct.c_double, ct.c_uint64, dp]
     L.pcs_sample_linear_gaussian.argtypes = [dp, ct.c_int32, ct.c_int32, ct.c_uint64, dp]
+    L.pcs_sample_linear_gaussian_rescaled.argtypes = [dp, ct.c_int32, ct.c_int32, ct.c_uint64, dp, dp]
     L.pcs_run_pc_stable_device.argtypes = [vp, ct.c_int64, ct.c_int32, ct.c_int32, ct.POINTER(_Config),
                                            ct.POINTER(vp)]
     L.pcs_result_p.argtypes = [vp]
@@ -493,6 +494,20 @@ def sample_linear_gaussian(weights: np.ndarray, m: int, seed: int) -> np.ndarray
     if rc:
         raise ValueError("sample_linear_gaussian: need m >= 4 and strictly lower-triangular weights")
     return xt.T
+
+
+def sample_linear_gaussian_rescaled(weights: np.ndarray, m: int, seed: int) -> tuple[np.ndarray, np.ndarray]:
+    """Overflow-safe sample_linear_gaussian for the BASELINE scaling shapes: the same noise
+    stream with every variable kept at unit RMS; returns ((m, n) data, log_scale[n]) with
+    x_reference[:, i] == x[:, i] * exp(log_scale[i]) (to rounding) and the same correlation matrix."""
+    w = np.ascontiguousarray(weights, np.float64)
+    n = w.shape[0]
+    xt = np.empty((n, m), np.float64)
+    ls = np.empty(n, np.float64)
+    rc = library().pcs_sample_linear_gaussian_rescaled(_dp(w), n, m, seed, _dp(xt), _dp(ls))
+    if rc:
+        raise ValueError("sample_linear_gaussian_rescaled: need m >= 4, strictly lower-triangular weights")
+    return xt.T, ls
 
 
 def run_pc_stable_device(c_ptr: int, ldc: int, p: int, sample_count: int, cfg: Optional[SkeletonConfig] = None,

@@ -8,9 +8,11 @@
 // runs on the host.  Parents are visited in ascending cause order exactly like
 // the dense inner loop of datagen.hpp:75-78, so the sums round identically.
 // Built with -ffp-contract=off (no FMA), like the reference's Release build.
+#include <algorithm>
 #include <cmath>
 #include <cstdint>
 #include <cstring>
+#include <thread>
 #include <vector>
 
 #include "../../include/pcstable_b200.h"
@@ -96,6 +98,76 @@ pcs_status pcs_sample_linear_gaussian(const double* weights, int32_t n, int32_t 
             for (int64_t e = start[i]; e < start[i + 1]; ++e) value += pw[e] * x[(size_t)par[e] * m + r];
             x[(size_t)i * m + r] = value;
         }
+    return PCS_OK;
+}
+
+// Overflow-safe variant for the BASELINE scaling shapes ("C5 needs the per-column-
+// rescaled generator"): the same noise draws in the same (sample-major) stream order, but every
+// variable is kept at unit RMS and its scale is carried as a logarithm.  With x_i the reference's
+// variable (x_i = sum_j w_ij x_j + n_i) and s_i its RMS over the m samples, this computes
+// x'_i = x_i / s_i through x'_i = (sum_j w_ij (s_j / F) x'_j + n_i / F) / rms(.) with F = the largest of
+// the parents' scales and the noise's, so no intermediate overflows.  Correlations are scale-invariant:
+// corr(x') = corr(x) in exact arithmetic (equal to rounding where the reference stays finite, finite
+// where the reference overflows).  Variable-major, the m samples of one variable in parallel chunks.
+pcs_status pcs_sample_linear_gaussian_rescaled(const double* weights, int32_t n, int32_t m, uint64_t seed, double* x,
+                                               double* log_scale) {
+    if (m < 4 || n < 2) return PCS_EINVAL;
+    std::vector<int64_t> start((size_t)n + 1);
+    std::vector<int32_t> par;
+    std::vector<double> pw;
+    for (int i = 0; i < n; ++i) {
+        start[i] = (int64_t)par.size();
+        for (int j = 0; j < n; ++j) {
+            const double w = weights[(size_t)i * n + j];
+            if (w == 0.0) continue;
+            if (j >= i) return PCS_EINVAL;
+            par.push_back(j);
+            pw.push_back(w);
+        }
+    }
+    start[n] = (int64_t)par.size();
+    {  // the reference's noise stream, one normal per (sample, variable) in sample-major order
+        Xoshiro g(seed);
+        for (int r = 0; r < m; ++r)
+            for (int i = 0; i < n; ++i) x[(size_t)i * m + r] = g.normal();
+    }
+    unsigned nt = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+    if ((long long)m * (long long)(start[n] / std::max(1, n) + 1) < 200000) nt = 1;
+    std::vector<double> coef, part(nt);
+    for (int i = 0; i < n; ++i) {
+        const int64_t b = start[i], e = start[i + 1];
+        double F = 0.0;  // log of the largest contributing scale (noise: scale 1)
+        for (int64_t k = b; k < e; ++k) F = std::max(F, log_scale[par[k]]);
+        coef.resize((size_t)(e - b));
+        for (int64_t k = b; k < e; ++k) coef[(size_t)(k - b)] = pw[k] * std::exp(log_scale[par[k]] - F);
+        const double nz = std::exp(-F);
+        double* xi = x + (size_t)i * m;
+        auto work = [&](unsigned t) {
+            const int r0 = (int)((long long)m * t / nt), r1 = (int)((long long)m * (t + 1) / nt);
+            double ss = 0.0;
+            for (int r = r0; r < r1; ++r) {
+                double v = xi[r] * nz;
+                for (int64_t k = b; k < e; ++k) v += coef[(size_t)(k - b)] * x[(size_t)par[k] * m + r];
+                xi[r] = v;
+                ss += v * v;
+            }
+            part[t] = ss;
+        };
+        if (nt == 1) {
+            work(0);
+        } else {
+            std::vector<std::thread> th;
+            for (unsigned t = 0; t < nt; ++t) th.emplace_back(work, t);
+            for (auto& t : th) t.join();
+        }
+        double ss = 0.0;
+        for (unsigned t = 0; t < nt; ++t) ss += part[t];
+        const double rms = std::sqrt(ss / m);
+        if (!(rms > 0.0) || !std::isfinite(rms)) return PCS_EINVAL;
+        const double inv = 1.0 / rms;
+        for (int r = 0; r < m; ++r) xi[r] *= inv;
+        log_scale[i] = F + std::log(rms);
+    }
     return PCS_OK;
 }
 

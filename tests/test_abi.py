@@ -66,3 +66,25 @@ def test_device_path_fails_loudly_without_gpu():
         pcs.run_pc_stable(np.eye(4), 100)
     with pytest.raises(pcs.PcsError):
         pcs.compute_correlation(np.random.default_rng(0).normal(size=(10, 3)))
+
+
+def test_rescaled_generator_is_the_reference_generator_scaled(oracle):
+    """pcs_sample_linear_gaussian_rescaled (the C5 scaling shapes' generator): same noise stream as
+    datagen.hpp:62-82, every column divided by the reference column's RMS, so the correlation matrix is
+    the reference generator's; finite where the reference overflows."""
+    import paper_1812_08491_b200 as pcs
+    w = oracle.random_dag(60, 0.15, 77)
+    ref = oracle.sample_linear_gaussian(w, 400, 78).T  # (m, n) like the product's
+    x, ls = pcs.sample_linear_gaussian_rescaled(w, 400, 78)
+    scale = np.exp(ls)
+    assert np.allclose(np.sqrt((ref ** 2).mean(axis=0)), scale, rtol=1e-12, atol=0)
+    assert np.max(np.abs(x * scale - ref) / scale) < 1e-12
+    assert np.abs(oracle.compute_correlation(x.T) - oracle.compute_correlation(ref.T)).max() < 1e-12
+    # dense and deep: the reference generator's values overflow, the rescaled ones stay at unit RMS
+    w = oracle.random_dag(1800, 0.95, 5)
+    with np.errstate(all="ignore"):
+        big = oracle.sample_linear_gaussian(w, 8, 6)
+    assert not np.isfinite(big).all()
+    x, ls = pcs.sample_linear_gaussian_rescaled(w, 8, 6)
+    assert np.isfinite(x).all() and np.isfinite(ls).all() and ls.max() > 709.0
+    assert np.allclose((x ** 2).mean(axis=0), 1.0, rtol=1e-12)

@@ -12,9 +12,12 @@ CONFIGS = {
     "C2": (1000, 10000, 0.1, 1),
     "C3": (1643, 850, 0.01, 2),
     "C4": (5361, 63, 0.002, 3),
-    "C5a": (2000, 5000, 0.05, 4),   # scaling-sweep shapes (BASELINE configs[4]); reference generator
+    # scaling-sweep shapes (BASELINE configs[4]); per-column-rescaled generator (same correlation)
+    "C5a": (2000, 5000, 0.05, 4),
     "C5b": (5000, 5000, 0.05, 5),
     "C5c": (2000, 5000, 0.2, 6),
+    "C5d": (10000, 5000, 0.05, 7),
+    "C5e": (20000, 5000, 0.05, 8),
 }
 names = sys.argv[1].split(",") if len(sys.argv) > 1 else list(CONFIGS)
 strategies = sys.argv[2].split(",") if len(sys.argv) > 2 else ["set"]
@@ -24,7 +27,13 @@ for name in names:
     p, m, d, k = CONFIGS[name]
     seed = 7919 * k
     w = pcs.random_dag(p, d, seed)
-    x = pcs.sample_linear_gaussian(w, m, seed + 1)
+    tg = time.time()
+    if name.startswith("C5"):
+        x, _ = pcs.sample_linear_gaussian_rescaled(w, m, seed + 1)
+    else:
+        x = pcs.sample_linear_gaussian(w, m, seed + 1)
+    del w
+    print(f"{name}: generated in {time.time() - tg:.1f}s", flush=True)
     c = pcs.compute_correlation(x)
     for strat, rep in [(st, r) for st in strategies for r in range(repeats)]:
         quiet = rep < repeats - 1

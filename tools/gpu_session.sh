@@ -19,6 +19,11 @@ for s in $STEPS; do
       timeout 600 python tools/explore.py C1,C3,C4 set,edge -1 2 > $OUT/explore.log 2>&1
       timeout 600 python tools/explore.py C2 set 3 >> $OUT/explore.log 2>&1
       ;;
+    c5)
+      timeout 900 python tools/explore.py C5a,C5b,C5c set 2 > $OUT/explore_c5.log 2>&1
+      timeout 900 python tools/explore.py C5d set 1 >> $OUT/explore_c5.log 2>&1
+      timeout 900 python tools/explore.py C5e set 0 >> $OUT/explore_c5.log 2>&1
+      ;;
     c2)
       timeout 600 python tools/explore.py C2 set 3 > $OUT/explore_c2.log 2>&1
       ;;
@@ -42,6 +47,9 @@ for s in $STEPS; do
       ;;
     variants)
       timeout 900 python tools/variants.py run --workload C2 --max-level 3 --repeats 2 > $OUT/variants.json 2> $OUT/variants.err
+      ;;
+    balance5)
+      timeout 1500 python tools/shard_balance.py 8 C5 2 set > $OUT/balance_c5.json 2> $OUT/balance_c5.err
       ;;
     bench)
       timeout 900 python bench.py > $OUT/bench.json 2> $OUT/bench.err

@@ -19,14 +19,17 @@ import torch  # noqa: E402
 import paper_1812_08491_b200 as pcs  # noqa: E402
 from paper_1812_08491_b200.multigpu import _CudaArray  # noqa: E402
 
-SHAPES = {"C2": (1000, 10000, 0.1, 1), "C3": (1643, 850, 0.01, 2), "C4": (5361, 63, 0.002, 3)}
+SHAPES = {"C2": (1000, 10000, 0.1, 1), "C3": (1643, 850, 0.01, 2), "C4": (5361, 63, 0.002, 3),
+          "C5": (5000, 5000, 0.05, 4)}  # C5: the scaling sweep's p=5000 point, rescaled generator
 nsh = int(sys.argv[1]) if len(sys.argv) > 1 else 8
 name = sys.argv[2] if len(sys.argv) > 2 else "C2"
 cap = int(sys.argv[3]) if len(sys.argv) > 3 else 3
 variant = sys.argv[4] if len(sys.argv) > 4 else "set"
 p, m, d, case = SHAPES[name]
 seed = 7919 * case
-x = pcs.sample_linear_gaussian(pcs.random_dag(p, d, seed), m, seed + 1)
+w = pcs.random_dag(p, d, seed)
+x = pcs.sample_linear_gaussian_rescaled(w, m, seed + 1)[0] if name == "C5" else pcs.sample_linear_gaussian(w, m, seed + 1)
+del w
 c = pcs.compute_correlation(x)
 cfg = pcs.SkeletonConfig(alpha=0.01, max_level=None if cap < 0 else cap, strategy=pcs.Strategy(variant))
 single = pcs.run_pc_stable(c, m, cfg)
