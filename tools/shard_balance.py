@@ -1,8 +1,8 @@
 """Load balance of the multi-GPU split on ONE GPU: N sessions play the N ranks of bench.py --gpus N in
 lockstep (keys MIN-merged between passes, like the NCCL all-reduce) and every shard's pass runs alone
 on the device (synchronised), so its CUDA-event kernel time is what that rank's GPU would spend.
-Prints, per level, each shard's pass time (host wall clock around a synchronised pass: kernels +
-launch overhead) and max/mean (1.0 = perfect balance), plus the modelled
+Prints, per level, each shard's pass time (CUDA events on the shard session's own stream around
+each synchronised pass: kernels + in-pass host gaps) and max/mean (1.0 = perfect balance), plus the modelled
 strong-scaling efficiency of the sharded levels (>= 1):
   sum(single-GPU kernel ms) / (N * sum over levels of max-shard ms).
 
@@ -33,7 +33,10 @@ del w
 c = pcs.compute_correlation(x)
 cfg = pcs.SkeletonConfig(alpha=0.01, max_level=None if cap < 0 else cap, strategy=pcs.Strategy(variant))
 single = pcs.run_pc_stable(c, m, cfg)
-sessions = [pcs.Session(c, m, cfg, shard_index=r, shard_count=nsh) for r in range(nsh)]
+streams = [torch.cuda.Stream() for _ in range(nsh)]
+cfgs = [pcs.SkeletonConfig(alpha=0.01, max_level=cfg.max_level, strategy=cfg.strategy, stream=st.cuda_stream)
+        for st in streams]
+sessions = [pcs.Session(c, m, cfgs[r], shard_index=r, shard_count=nsh) for r in range(nsh)]
 shard_ms = {}
 while True:
     states = [s.level_begin() for s in sessions]
@@ -43,10 +46,12 @@ while True:
     for pass_index in (0, 1):
         for r, s in enumerate(sessions):
             torch.cuda.synchronize()
-            t0 = time.perf_counter()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(streams[r])
             s.level_pass(pass_index)
+            e1.record(streams[r])
             torch.cuda.synchronize()
-            shard_ms.setdefault(ell, [0.0] * nsh)[r] += (time.perf_counter() - t0) * 1e3
+            shard_ms.setdefault(ell, [0.0] * nsh)[r] += e0.elapsed_time(e1)
         if nk:
             views = [torch.as_tensor(_CudaArray(*s.keys()), device="cuda") for s in sessions]
             merged = torch.stack(views).min(0).values
