@@ -34,6 +34,9 @@ __device__ __noinline__ int decide_slow(double h01, double denom, Thresholds th)
 #ifndef PCS_SET_NT_SMALL
 #define PCS_SET_NT_SMALL 3  // targets per lane per set for L <= 3 (tuning knob, results identical)
 #endif
+#ifndef PCS_UNRANK_BSEARCH
+#define PCS_UNRANK_BSEARCH 0  // 1: phase-1 unrank by per-member binary search over the binomial table
+#endif
 #ifndef PCS_SET_SP
 #define PCS_SET_SP 2        // sets per step for one-target-per-lane batches (L <= 3)
 #endif
@@ -1019,7 +1022,11 @@ __global__ void __launch_bounds__(kSetWarps * 32, PCS_SET_MINB) level_set_kernel
                 have_sets = true;
                 if (lane < nvalid) {
                     int pos[L];
+#if PCS_UNRANK_BSEARCH
                     unrank<L>(A.binom, w, t0 + lane, pos);
+#else
+                    unrank_est<L>(A.binom, w, t0 + lane, pos);
+#endif
                     int mem[L];
                     double m2[L * L], minv[L * L], ciS[L], p0[L], h00;
 #pragma unroll

@@ -61,6 +61,38 @@ __device__ __forceinline__ void unrank(const BinomTable& C, int w, unsigned long
     }
 }
 
+// Same map, with each member's binary search replaced by a closed-form estimate and a local fix-up:
+// the largest v with C(w - v, k) >= need has x = w - v with C(x, k) ~ need, and C(x, k) ~ (x - (k-1)/2)^k / k!
+// gives x ~ (k! need)^(1/k) + (k-1)/2 (FP32, MUFU); the exact table entries around the estimate then
+// settle v (usually one round of two independent loads instead of ~log2(w) dependent ones).
+template <int L>
+__device__ __forceinline__ void unrank_est(const BinomTable& C, int w, unsigned long long t, int (&pos)[L]) {
+    int start = 0;
+#pragma unroll
+    for (int c = 0; c < L; ++c) {
+        const int k = L - c;
+        const unsigned long long total = C(w - start, k);
+        const unsigned long long need = total - t;  // >= 1
+        float fk = 1.0f;
+#pragma unroll
+        for (int q = 2; q <= L; ++q)
+            if (q <= k) fk *= (float)q;
+        const float xf = k == 1 ? (float)need : exp2f(__log2f(fk * (float)need) / (float)k) + 0.5f * (float)(k - 1);
+        int v = w - (int)floorf(xf);
+        v = v < start ? start : (v > w - k ? w - k : v);
+        for (;;) {
+            const unsigned long long a = C(w - v, k);
+            const unsigned long long b = v < w - k ? C(w - v - 1, k) : 0ull;
+            if (a < need) { --v; continue; }
+            if (b >= need) { ++v; continue; }
+            break;
+        }
+        pos[c] = v;
+        t -= total - C(w - v, k);
+        start = v + 1;
+    }
+}
+
 // Inverse map: lexicographic rank of ascending positions in width w.
 template <int L>
 __device__ __forceinline__ unsigned long long rank_of(const BinomTable& C, int w, const int (&pos)[L]) {
