@@ -324,7 +324,8 @@ def level_keys(c: np.ndarray, offsets: np.ndarray, indices: np.ndarray, ell: int
     p = c.shape[0]
     off = np.ascontiguousarray(offsets, np.int32)
     idx = np.ascontiguousarray(indices if len(indices) else np.zeros(1, np.int32), np.int32)
-    ne = int(sum(1 for a in range(p) for q in range(off[a], off[a + 1]) if idx[q] > a))
+    rows = np.repeat(np.arange(p, dtype=np.int64), np.diff(off.astype(np.int64)))
+    ne = int((idx[:len(rows)] > rows).sum())
     e_end = ne if e_end is None else min(e_end, ne)
     keys = np.full(max(e_end - e_begin, 1), NONE_KEY, np.int64)
     _check(lib().orc_level_keys(_dp(c), p, _ip(off), _ip(idx), ell, tau, e_begin, e_end,
