@@ -368,6 +368,16 @@ pcs_status build_binomials(pcs_session* s, int ell, int maxw) {
     return PCS_OK;
 }
 
+// PCS_MERGE_PASSES=0: cuPC-S levels >= 2 as two direction passes (as the cuPC-E and generic-ell
+// kernels run); default 1 (one sweep over both directions).  No effect on results.
+bool merge_passes() {
+    static const bool on = [] {
+        const char* e = std::getenv("PCS_MERGE_PASSES");
+        return !(e && std::atoi(e) == 0);
+    }();
+    return on;
+}
+
 LevelArgs level_args(pcs_session* s) {
     LevelArgs A{};
     A.C = s->dC;
@@ -574,6 +584,13 @@ pcs_status pcs_session_level_pass(pcs_session* s, int32_t pass) {
     if (!s || !s->in_level) return fail(PCS_EINVAL, "no level in progress");
     if (pass != 0 && pass != 1) return fail(PCS_EINVAL, "pass must be 0 or 1");
     if (s->ell == 0) return PCS_OK;
+    // cuPC-S with a register-template kernel tests both directions in ONE sweep (pass 0 does it as
+    // "pass 2"; pass 1 has nothing left): every set's pseudo-inverse is computed once per level instead
+    // of once per direction, at the price of testing direction 1 of edges that direction 0 separates
+    // in the same level (their keys stay the direction-0 ones: MIN).  Results are unchanged.
+    const bool merged = s->cfg.variant == PCS_VARIANT_SET && s->ell >= 2 && s->ell <= kMaxTemplLevel && merge_passes();
+    if (merged && pass == 1) return PCS_OK;
+    const int kpass = merged ? 2 : pass;
     CUDA_TRY(cudaSetDevice(s->device));
     LevelArgs A = level_args(s);
     const int shard = s->cfg.shard_index, nsh = s->cfg.shard_count;
@@ -595,13 +612,13 @@ pcs_status pcs_session_level_pass(pcs_session* s, int32_t pass) {
         unsigned long long u0 = 0, u1 = 0;
         if (nsh > 1) {
             unsigned long long b[2] = {0, 0};
-            launch_row_work_sharded(A, pass, s->cfg.variant, s->dPrefix, s->dShardCost, shard, nsh, s->dBounds, s->st);
+            launch_row_work_sharded(A, kpass, s->cfg.variant, s->dPrefix, s->dShardCost, shard, nsh, s->dBounds, s->st);
             CUDA_TRY(cudaMemcpyAsync(b, s->dBounds, sizeof(b), cudaMemcpyDeviceToHost, s->st));
             CUDA_TRY(cudaStreamSynchronize(s->st));
             u0 = b[0];
             u1 = b[1];
         } else {
-            launch_row_work(A, pass, s->cfg.variant, 0, s->p, s->dPrefix, s->st);
+            launch_row_work(A, kpass, s->cfg.variant, 0, s->p, s->dPrefix, s->st);
             CUDA_TRY(cudaMemcpyAsync(&u1, s->dPrefix + s->p, sizeof(u1), cudaMemcpyDeviceToHost, s->st));
             CUDA_TRY(cudaStreamSynchronize(s->st));
         }
@@ -614,7 +631,7 @@ pcs_status pcs_session_level_pass(pcs_session* s, int32_t pass) {
                     return fail(PCS_EUNSUPPORTED, "level not supported by the generic set kernel");
             } else {
                 launch_refresh_kdir(A, s->info.e_dir, s->st);
-                if (launch_level_set(A, pass, s->dPrefix, u0, u1, s->num_sms, s->st))
+                if (launch_level_set(A, kpass, s->dPrefix, u0, u1, s->num_sms, s->st))
                     return fail(PCS_EUNSUPPORTED, "level not supported by the set kernel");
             }
         }

@@ -322,7 +322,7 @@ __global__ void row_work_kernel(LevelArgs A, int pass, int variant, int row_begi
     unsigned long long u = 0, c = 0;
     const int w = A.off[i + 1] - A.off[i];
     const int lc = A.lowcnt[i];
-    const int ntar = pass == 0 ? w - lc : lc;
+    const int ntar = pass == 2 ? w : (pass == 0 ? w - lc : lc);  // pass 2: both directions at once
     if (i >= row_begin && i < row_end && w >= A.ell + 1 && ntar > 0) {
         if (A.ell == 1) {
             u = (unsigned long long)((ntar + kL1Threads - 1) / kL1Threads);
@@ -675,8 +675,8 @@ __device__ __forceinline__ void h_terms_sp(const SetSlot<L>* const (&sl)[SP], co
 // in rank order: the first separating set among the SP wins and later ones are discarded.  Same
 // results and counters as set_sweep<L, 1>.
 template <int L, int SP>
-__device__ __forceinline__ void set_sweep_sp(const LevelArgs& A, SetWarpSmem<L>& S, int lane, int oi, int nlive,
-                                             int nvalid, unsigned segmask, unsigned livemask,
+__device__ __forceinline__ void set_sweep_sp(const LevelArgs& A, SetWarpSmem<L>& S, int lane, int oi, int lc,
+                                             int nlive, int nvalid, unsigned segmask, unsigned livemask,
                                              unsigned long long K0, unsigned long long& tests,
                                              unsigned long long& degen, int& nan) {
     const double* __restrict__ C = A.C;
@@ -685,14 +685,16 @@ __device__ __forceinline__ void set_sweep_sp(const LevelArgs& A, SetWarpSmem<L>&
     int rel = -1;
     const double* Cj = C;
     double cij2 = 0.0;
+    const int q = have ? S.tq[lane] : -1;
+    const bool dir1 = q >= 0 && q < lc;
+    const unsigned long long kb = dir1 ? (K0 | (1ull << kDirShift)) : K0;  // this target's key base
     if (have) {
-        const unsigned long long d = S.tkey[lane] - K0;
+        const unsigned long long d = S.tkey[lane] - kb;
         rel = d > 0x3fffffffull ? 0x3fffffff : (int)d;
         Cj = C + S.tj[lane];
         const double c = S.tcij[lane];
         cij2 = c + c;
     }
-    const int q = have ? S.tq[lane] : -1;
     constexpr int LP = L > 1 ? L - 1 : 1;
     const unsigned valid_mask = nvalid >= 32 ? 0xffffffffu : ((1u << nvalid) - 1u);
     segmask &= valid_mask;
@@ -761,10 +763,7 @@ __device__ __forceinline__ void set_sweep_sp(const LevelArgs& A, SetWarpSmem<L>&
                         const int d = decide_slow(h01, den[k], A.th);
                         if (d != kDependent) {
                             if (d == kNanError) nan = 1;
-                            else {
-                                atomicMin(A.keys + S.te[lane], K0 + (unsigned long long)g[k]);
-                                atomicMin(A.kdir + oi + q, K0 + (unsigned long long)g[k]);
-                            }
+                            else record_find(A, oi, q, S.te[lane], S.tj[lane], dir1, kb + (unsigned long long)g[k]);
                             rel = g[k];
                             lim = g[k];
                             hit = true;
@@ -798,9 +797,18 @@ __device__ __forceinline__ void set_sweep_sp(const LevelArgs& A, SetWarpSmem<L>&
 // "dependent" (stats.hpp:301-305) without any arithmetic: those sets are counted, never visited
 // (rank-truncated inputs hit this often: ~29% of C2's level-3 sets), and the last-member
 // prefetch always targets the next LIVE set, so skipped sets cost no L2 round trip either.
+// Key of a find: the target's direction (q < lc: j < i, direction 1 of edge (j, i)) and the set's
+// full-row rank; both directions' mirror entries of the edge are lowered with the key.
+__device__ __forceinline__ void record_find(const LevelArgs& A, int oi, int q, int e, int j, bool dir1,
+                                            unsigned long long key) {
+    atomicMin(A.keys + e, key);
+    atomicMin(A.kdir + oi + q, key);
+    atomicMin(A.kdir + A.off[j] + (dir1 ? A.eu_qa[e] : A.eu_qb[e]), key);
+}
+
 template <int L, int NT>
-__device__ __forceinline__ void set_sweep(const LevelArgs& A, SetWarpSmem<L>& S, int lane, int oi, int nlive, int nvalid,
-                                          unsigned segmask, unsigned livemask, unsigned long long K0,
+__device__ __forceinline__ void set_sweep(const LevelArgs& A, SetWarpSmem<L>& S, int lane, int oi, int lc, int nlive,
+                                          int nvalid, unsigned segmask, unsigned livemask, unsigned long long K0,
                                           unsigned long long& tests, unsigned long long& degen, int& nan) {
     const double* __restrict__ C = A.C;
     const double hi2x4 = 4.0 * A.th.hi2;  // exact (power-of-two scaling)
@@ -811,7 +819,8 @@ __device__ __forceinline__ void set_sweep(const LevelArgs& A, SetWarpSmem<L>& S,
     for (int t = 0; t < NT; ++t) {
         const int k = t * 32 + lane;
         if (k < nlive) {
-            const unsigned long long d = S.tkey[k] - K0;  // > 0 (staged targets are live)
+            const unsigned long long kb = S.tq[k] < lc ? (K0 | (1ull << kDirShift)) : K0;  // target's key base
+            const unsigned long long d = S.tkey[k] - kb;  // > 0 (staged targets are live)
             rel[t] = d > 0x3fffffffull ? 0x3fffffff : (int)d;
             Cj[t] = C + S.tj[k];
             const double c = S.tcij[k];
@@ -894,8 +903,9 @@ __device__ __forceinline__ void set_sweep(const LevelArgs& A, SetWarpSmem<L>& S,
                             if (d == kNanError) nan = 1;
                             else {
                                 const int k = t * 32 + lane;
-                                atomicMin(A.keys + S.te[k], K0 + (unsigned long long)sgx);
-                                atomicMin(A.kdir + oi + S.tq[k], K0 + (unsigned long long)sgx);
+                                const bool dir1 = S.tq[k] < lc;
+                                record_find(A, oi, S.tq[k], S.te[k], S.tj[k], dir1,
+                                            (dir1 ? (K0 | (1ull << kDirShift)) : K0) + (unsigned long long)sgx);
                             }
                             rel[t] = sgx;
                             lim[t] = sgx;
@@ -956,11 +966,13 @@ __global__ void __launch_bounds__(kSetWarps * 32, PCS_SET_MINB) level_set_kernel
     SetWarpSmem<L>& S = reinterpret_cast<SetWarpSmem<L>*>(smem_raw)[wib];
     const double* __restrict__ C = A.C;
     const long long ldc = A.ldc;
-    const unsigned long long dirbits = (unsigned long long)pass << kDirShift;
+    // pass 2: both directions in one sweep (every set's pseudo-inverse computed once per level);
+    // a target's key base carries its own direction bit, dir-0 (K0) or dir-1 (K0 | 1 << 62)
+    const unsigned long long dirbits = pass == 1 ? (1ull << kDirShift) : 0ull;
     const unsigned lt_mask = (1u << lane) - 1u;
     unsigned long long tests = 0, pinvs = 0, degen = 0;
     int nan = 0;
-    unsigned long long* cursor = &A.cnt->units[pass];
+    unsigned long long* cursor = &A.cnt->units[pass & 1];
     int row_hint = 0;
     // the next unit is grabbed one unit ahead (lane 0's atomic result is only read at the top of the
     // next iteration), so the cursor round trip overlaps the current unit's work
@@ -974,7 +986,7 @@ __global__ void __launch_bounds__(kSetWarps * 32, PCS_SET_MINB) level_set_kernel
         row_hint = i;
         const unsigned long long t0 = (u - prefix[i]) * kSetBand;
         const int oi = A.off[i], w = A.off[i + 1] - oi, lc = A.lowcnt[i];
-        const int qbeg = pass == 0 ? lc : 0, qend = pass == 0 ? w : lc;
+        const int qbeg = pass == 2 ? 0 : (pass == 0 ? lc : 0), qend = pass == 2 ? w : (pass == 0 ? w : lc);
         const unsigned long long K0 = dirbits | t0;
         const unsigned long long total = A.binom(w, L);
         const int nvalid = (int)min(32ull, total - t0);
@@ -985,6 +997,11 @@ __global__ void __launch_bounds__(kSetWarps * 32, PCS_SET_MINB) level_set_kernel
             // ---- stage the live targets of [tb, tend), compacted: per directed entry the key mirror,
             // edge id, neighbour and C(i, j) are independent coalesced loads (one round trip)
             int nlive = 0;
+#ifdef PCS_STAGE_REPS  // cost probe (tools/variants.py): staging repeated, results unchanged
+            for (int rep = 0; rep < PCS_STAGE_REPS; ++rep) {
+            asm volatile("" ::: "memory");
+            nlive = 0;
+#endif
             {
                 constexpr int NC = kStage / 32;
                 unsigned long long kk[NC];
@@ -1003,7 +1020,8 @@ __global__ void __launch_bounds__(kSetWarps * 32, PCS_SET_MINB) level_set_kernel
                 }
 #pragma unroll
                 for (int c = 0; c < NC; ++c) {
-                    const bool live = kk[c] > K0;
+                    // a target's key base: K0 with the target's own direction bit (q < lc: j < i)
+                    const bool live = kk[c] > (K0 | (tb + c * 32 + lane < lc ? (1ull << kDirShift) : 0ull));
                     const unsigned bal = __ballot_sync(0xffffffffu, live);
                     if (live) {
                         const int at = nlive + __popc(bal & lt_mask);
@@ -1016,10 +1034,17 @@ __global__ void __launch_bounds__(kSetWarps * 32, PCS_SET_MINB) level_set_kernel
                     nlive += __popc(bal);
                 }
             }
+#ifdef PCS_STAGE_REPS
+            }
+#endif
             if (nlive == 0) continue;
             // ---- phase 1 (once per unit): lane-parallel pseudo-inverses of the band's sets
             if (!have_sets) {
                 have_sets = true;
+#ifdef PCS_PHASE1_REPS  // cost probe (tools/variants.py): phase 1 repeated, results unchanged
+                for (int rep = 0; rep < PCS_PHASE1_REPS; ++rep) {
+                asm volatile("" ::: "memory");
+#endif
                 if (lane < nvalid) {
                     int pos[L];
 #if PCS_UNRANK_BSEARCH
@@ -1055,6 +1080,9 @@ __global__ void __launch_bounds__(kSetWarps * 32, PCS_SET_MINB) level_set_kernel
                     }
                     sl.h00 = h00;
                 }
+#ifdef PCS_PHASE1_REPS
+                }
+#endif
                 if (lane == 0) pinvs += nvalid;
                 // runs of consecutive sets with equal leading L-1 members (lexicographic order)
                 bool starts = lane == 0;
@@ -1074,17 +1102,17 @@ __global__ void __launch_bounds__(kSetWarps * 32, PCS_SET_MINB) level_set_kernel
             // ---- phase 2: sets in rank order, NT targets per lane
             const int nt = (nlive + 31) >> 5;
             if constexpr (SetCfg<L>::NT == 4) {
-                if (nt == 4) set_sweep<L, 4>(A, S, lane, oi, nlive, nvalid, segmask, livemask, K0, tests, degen, nan);
-                else if (nt == 3) set_sweep<L, 3>(A, S, lane, oi, nlive, nvalid, segmask, livemask, K0, tests, degen, nan);
-                else if (nt == 2) set_sweep<L, 2>(A, S, lane, oi, nlive, nvalid, segmask, livemask, K0, tests, degen, nan);
-                else set_sweep<L, 1>(A, S, lane, oi, nlive, nvalid, segmask, livemask, K0, tests, degen, nan);
+                if (nt == 4) set_sweep<L, 4>(A, S, lane, oi, lc, nlive, nvalid, segmask, livemask, K0, tests, degen, nan);
+                else if (nt == 3) set_sweep<L, 3>(A, S, lane, oi, lc, nlive, nvalid, segmask, livemask, K0, tests, degen, nan);
+                else if (nt == 2) set_sweep<L, 2>(A, S, lane, oi, lc, nlive, nvalid, segmask, livemask, K0, tests, degen, nan);
+                else set_sweep<L, 1>(A, S, lane, oi, lc, nlive, nvalid, segmask, livemask, K0, tests, degen, nan);
             } else if constexpr (SetCfg<L>::NT == 3) {
-                if (nt == 3) set_sweep<L, 3>(A, S, lane, oi, nlive, nvalid, segmask, livemask, K0, tests, degen, nan);
-                else if (nt == 2) set_sweep<L, 2>(A, S, lane, oi, nlive, nvalid, segmask, livemask, K0, tests, degen, nan);
-                else set_sweep_sp<L, PCS_SET_SP>(A, S, lane, oi, nlive, nvalid, segmask, livemask, K0, tests, degen, nan);
+                if (nt == 3) set_sweep<L, 3>(A, S, lane, oi, lc, nlive, nvalid, segmask, livemask, K0, tests, degen, nan);
+                else if (nt == 2) set_sweep<L, 2>(A, S, lane, oi, lc, nlive, nvalid, segmask, livemask, K0, tests, degen, nan);
+                else set_sweep_sp<L, PCS_SET_SP>(A, S, lane, oi, lc, nlive, nvalid, segmask, livemask, K0, tests, degen, nan);
             } else {
-                if (nt == 2) set_sweep<L, 2>(A, S, lane, oi, nlive, nvalid, segmask, livemask, K0, tests, degen, nan);
-                else set_sweep_sp<L, 2>(A, S, lane, oi, nlive, nvalid, segmask, livemask, K0, tests, degen, nan);
+                if (nt == 2) set_sweep<L, 2>(A, S, lane, oi, lc, nlive, nvalid, segmask, livemask, K0, tests, degen, nan);
+                else set_sweep_sp<L, 2>(A, S, lane, oi, lc, nlive, nvalid, segmask, livemask, K0, tests, degen, nan);
             }
             __syncwarp();
         }

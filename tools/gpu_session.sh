@@ -24,6 +24,10 @@ for s in $STEPS; do
       timeout 900 python tools/explore.py C5d set 1 >> $OUT/explore_c5.log 2>&1
       timeout 900 python tools/explore.py C5e set 0 >> $OUT/explore_c5.log 2>&1
       ;;
+    merge)
+      PCS_MERGE_PASSES=0 timeout 600 python tools/explore.py C2 set 3 2 > $OUT/merge_ab.log 2>&1
+      timeout 600 python tools/explore.py C2 set 3 2 >> $OUT/merge_ab.log 2>&1
+      ;;
     c2)
       timeout 600 python tools/explore.py C2 set 3 > $OUT/explore_c2.log 2>&1
       ;;
