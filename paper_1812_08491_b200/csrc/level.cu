@@ -37,6 +37,9 @@ __device__ __noinline__ int decide_slow(double h01, double denom, Thresholds th)
 #ifndef PCS_UNRANK_BSEARCH
 #define PCS_UNRANK_BSEARCH 0  // 1: phase-1 unrank by per-member binary search over the binomial table
 #endif
+#ifndef PCS_NT2_SP
+#define PCS_NT2_SP 1        // sets per step for two-targets-per-lane batches (L <= 3); 1: plain set_sweep
+#endif
 #ifndef PCS_SET_SP
 #define PCS_SET_SP 2        // sets per step for one-target-per-lane batches (L <= 3)
 #endif
@@ -623,13 +626,23 @@ __device__ __forceinline__ void h_terms_stream(const SetSlot<L>& sl, const doubl
     }
 }
 
-// h_terms for ONE target against SP sets of the same run (shared leading members cp, per-set
-// last-member gather cur[k]): the same per-accumulator rounding sequence as h_terms_stream.
-template <int L, int SP, int LP>
-__device__ __forceinline__ void h_terms_sp(const SetSlot<L>* const (&sl)[SP], const double (&cp)[LP],
-                                           const double (&cur)[SP], double cij2, double (&s01)[SP],
-                                           double (&h2)[SP], double (&den)[SP]) {
-    double d11[SP], d01[SP], d10[SP];
+// Key of a find: the target's direction (q < lc: j < i, direction 1 of edge (j, i)) and the set's
+// full-row rank; both directions' mirror entries of the edge are lowered with the key.
+__device__ __forceinline__ void record_find(const LevelArgs& A, int oi, int q, int e, int j, bool dir1,
+                                            unsigned long long key) {
+    atomicMin(A.keys + e, key);
+    atomicMin(A.kdir + oi + q, key);
+    atomicMin(A.kdir + A.off[j] + (dir1 ? A.eu_qa[e] : A.eu_qb[e]), key);
+}
+
+// h_terms for NT targets per lane against SP sets of the same run (shared leading members cp[t],
+// per-(target, set) last-member gather cur[t][k]): the same per-accumulator rounding sequence as
+// h_terms_stream; each set's column data is loaded once and shared by the NT targets.
+template <int L, int NT, int SP, int LP>
+__device__ __forceinline__ void h_terms_tsp(const SetSlot<L>* const (&sl)[SP], const double (&cp)[NT][LP],
+                                            const double (&cur)[NT][SP], const double (&cij2)[NT],
+                                            double (&s01)[NT][SP], double (&h2)[NT][SP], double (&den)[NT][SP]) {
+    double d11[NT][SP], d01[NT][SP], d10[NT][SP];
 #pragma unroll
     for (int col = 0; col < L; ++col) {
 #pragma unroll
@@ -642,58 +655,71 @@ __device__ __forceinline__ void h_terms_sp(const SetSlot<L>* const (&sl)[SP], co
                 cv[c + 1] = v.y;
             }
             const double ci = cv[L], pc = cv[L + 1];
-            double x[L];
 #pragma unroll
-            for (int a = 0; a < L - 1; ++a) x[a] = cp[a];
-            x[L - 1] = cur[k];
-            double pcol = x[0] * cv[0];
+            for (int t = 0; t < NT; ++t) {
+                double x[L];
 #pragma unroll
-            for (int q = 1; q < L; ++q) pcol = pcol + x[q] * cv[q];
-            if (col == 0) {
-                d11[k] = pcol * x[0];
-                d01[k] = pc * x[0];
-                d10[k] = pcol * ci;
-            } else {
-                d11[k] = d11[k] + pcol * x[col];
-                d01[k] = d01[k] + pc * x[col];
-                d10[k] = d10[k] + pcol * ci;
+                for (int a = 0; a < L - 1; ++a) x[a] = cp[t][a];
+                x[L - 1] = cur[t][k];
+                double pcol = x[0] * cv[0];
+#pragma unroll
+                for (int q = 1; q < L; ++q) pcol = pcol + x[q] * cv[q];
+                if (col == 0) {
+                    d11[t][k] = pcol * x[0];
+                    d01[t][k] = pc * x[0];
+                    d10[t][k] = pcol * ci;
+                } else {
+                    d11[t][k] = d11[t][k] + pcol * x[col];
+                    d01[t][k] = d01[t][k] + pc * x[col];
+                    d10[t][k] = d10[t][k] + pcol * ci;
+                }
             }
         }
     }
 #pragma unroll
     for (int k = 0; k < SP; ++k) {
-        const double h11 = 1.0 - d11[k];
-        s01[k] = d01[k] + d10[k];
-        h2[k] = cij2 - s01[k];
-        den[k] = sl[k]->h00 * h11;
+        const double h00 = sl[k]->h00;
+#pragma unroll
+        for (int t = 0; t < NT; ++t) {
+            const double h11 = 1.0 - d11[t][k];
+            s01[t][k] = d01[t][k] + d10[t][k];
+            h2[t][k] = cij2[t] - s01[t][k];
+            den[t][k] = h00 * h11;
+        }
     }
 }
 
-// Phase 2 for a batch of at most 32 targets (one per lane): a one-target step would be a single
-// dependent FP64 chain per lane (latency-bound), so each step tests the lane's target against SP
-// consecutive live sets of the current run instead (SP independent chains).  Sets are still settled
-// in rank order: the first separating set among the SP wins and later ones are discarded.  Same
-// results and counters as set_sweep<L, 1>.
-template <int L, int SP>
-__device__ __forceinline__ void set_sweep_sp(const LevelArgs& A, SetWarpSmem<L>& S, int lane, int oi, int lc,
-                                             int nlive, int nvalid, unsigned segmask, unsigned livemask,
-                                             unsigned long long K0, unsigned long long& tests,
-                                             unsigned long long& degen, int& nan) {
+// Phase 2 for a partially filled batch (NT targets per lane, NT below the kernel's full NT): a step
+// tests the lane's NT targets against SP consecutive live sets of the current run (NT x SP independent
+// chains instead of NT, and one step's bookkeeping for SP sets).  Sets are still settled in rank
+// order per target: the first separating set among a step's SP wins and later ones are discarded.
+// Same results and counters as set_sweep<L, NT>.
+template <int L, int NT, int SP>
+__device__ __forceinline__ void set_sweep_tsp(const LevelArgs& A, SetWarpSmem<L>& S, int lane, int oi, int lc,
+                                              int nlive, int nvalid, unsigned segmask, unsigned livemask,
+                                              unsigned long long K0, unsigned long long& tests,
+                                              unsigned long long& degen, int& nan) {
     const double* __restrict__ C = A.C;
     const double hi2x4 = 4.0 * A.th.hi2;
-    const bool have = lane < nlive;
-    int rel = -1;
-    const double* Cj = C;
-    double cij2 = 0.0;
-    const int q = have ? S.tq[lane] : -1;
-    const bool dir1 = q >= 0 && q < lc;
-    const unsigned long long kb = dir1 ? (K0 | (1ull << kDirShift)) : K0;  // this target's key base
-    if (have) {
-        const unsigned long long d = S.tkey[lane] - kb;
-        rel = d > 0x3fffffffull ? 0x3fffffff : (int)d;
-        Cj = C + S.tj[lane];
-        const double c = S.tcij[lane];
-        cij2 = c + c;
+    int rel[NT], q[NT];
+    const double* Cj[NT];
+    double cij2[NT];
+#pragma unroll
+    for (int t = 0; t < NT; ++t) {
+        const int kk = t * 32 + lane;
+        rel[t] = -1;
+        Cj[t] = C;
+        cij2[t] = 0.0;
+        q[t] = -1;
+        if (kk < nlive) {
+            q[t] = S.tq[kk];
+            const unsigned long long kb = q[t] < lc ? (K0 | (1ull << kDirShift)) : K0;
+            const unsigned long long d = S.tkey[kk] - kb;
+            rel[t] = d > 0x3fffffffull ? 0x3fffffff : (int)d;
+            Cj[t] = C + S.tj[kk];
+            const double c = S.tcij[kk];
+            cij2[t] = c + c;
+        }
     }
     constexpr int LP = L > 1 ? L - 1 : 1;
     const unsigned valid_mask = nvalid >= 32 ? 0xffffffffu : ((1u << nvalid) - 1u);
@@ -709,21 +735,23 @@ __device__ __forceinline__ void set_sweep_sp(const LevelArgs& A, SetWarpSmem<L>&
     };
     // a group: up to SP consecutive live sets of one run (g[k] = nvalid: empty item); returns the
     // first live set after the group
-    auto gather_group = [&](int first, int (&g)[SP], double (&buf)[SP]) -> int {
+    auto gather_group = [&](int first, int (&g)[SP], double (&buf)[NT][SP]) -> int {
         const int re = first < nvalid ? run_end(first) : nvalid;
         int x = first;
 #pragma unroll
         for (int k = 0; k < SP; ++k) {
             const bool ok = x < re;
             g[k] = ok ? x : nvalid;
-            buf[k] = __ldg(Cj + S.slot[ok ? x : (first < nvalid ? first : nvalid - 1)].roff[L - 1]);
+            const int ro = S.slot[ok ? x : (first < nvalid ? first : nvalid - 1)].roff[L - 1];
+#pragma unroll
+            for (int t = 0; t < NT; ++t) buf[t][k] = __ldg(Cj[t] + ro);
             if (ok) x = next_live(x);
         }
         return x;
     };
-    double cp[LP];
+    double cp[NT][LP];
     int g[SP];
-    double nxt[SP];
+    double nxt[NT][SP];
     int after = gather_group(live ? __ffs(live) - 1 : nvalid, g, nxt);
     int sg = 0;
     while (sg < nvalid) {
@@ -733,40 +761,54 @@ __device__ __forceinline__ void set_sweep_sp(const LevelArgs& A, SetWarpSmem<L>&
         const int base = sl0.pos[L - 1];
         if (g[0] < seg_end) {
 #pragma unroll
-            for (int a = 0; a < L - 1; ++a) cp[a] = __ldg(Cj + sl0.roff[a]);
-        }
-        bool pm = false;
+            for (int a = 0; a < L - 1; ++a)
 #pragma unroll
-        for (int a = 0; a < L - 1; ++a) pm |= sl0.pos[a] == q;
-        int lim = pm ? -1 : rel;
-        const int dm = sg0 + q - base;
-        bool hit = false;
+                for (int t = 0; t < NT; ++t) cp[t][a] = __ldg(Cj[t] + sl0.roff[a]);
+        }
+        int lim[NT], dm[NT];
+        unsigned hit = 0;
+#pragma unroll
+        for (int t = 0; t < NT; ++t) {
+            bool pm = false;
+#pragma unroll
+            for (int a = 0; a < L - 1; ++a) pm |= sl0.pos[a] == q[t];
+            lim[t] = pm ? -1 : rel[t];
+            dm[t] = sg0 + q[t] - base;
+        }
         while (g[0] < seg_end) {
             int gn[SP];
-            double alt[SP];
+            double alt[NT][SP];
             const int after2 = gather_group(after, gn, alt);
             const SetSlot<L>* sls[SP];
 #pragma unroll
             for (int k = 0; k < SP; ++k) sls[k] = &S.slot[g[k] < nvalid ? g[k] : g[0]];
-            double s01[SP], h2[SP], den[SP];
-            h_terms_sp<L, SP, LP>(sls, cp, nxt, cij2, s01, h2, den);
+            double s01[NT][SP], h2[NT][SP], den[NT][SP];
+            h_terms_tsp<L, NT, SP, LP>(sls, cp, nxt, cij2, s01, h2, den);
             unsigned cand = 0;
 #pragma unroll
-            for (int k = 0; k < SP; ++k)
-                cand |= (unsigned)((g[k] < seg_end) & (g[k] < lim) & (g[k] != dm) &
-                                   !surely_dependent2(h2[k], den[k], hi2x4)) << k;
+            for (int t = 0; t < NT; ++t)
+#pragma unroll
+                for (int k = 0; k < SP; ++k)
+                    cand |= (unsigned)((g[k] < seg_end) & (g[k] < lim[t]) & (g[k] != dm[t]) &
+                                       !surely_dependent2(h2[t][k], den[t][k], hi2x4)) << (t * SP + k);
             if (__any_sync(0xffffffffu, cand)) {
 #pragma unroll
-                for (int k = 0; k < SP; ++k) {
-                    if (((cand >> k) & 1u) && g[k] < lim) {
-                        const double h01 = 0.5 * cij2 - 0.5 * s01[k];
-                        const int d = decide_slow(h01, den[k], A.th);
-                        if (d != kDependent) {
-                            if (d == kNanError) nan = 1;
-                            else record_find(A, oi, q, S.te[lane], S.tj[lane], dir1, kb + (unsigned long long)g[k]);
-                            rel = g[k];
-                            lim = g[k];
-                            hit = true;
+                for (int t = 0; t < NT; ++t) {
+#pragma unroll
+                    for (int k = 0; k < SP; ++k) {
+                        if (((cand >> (t * SP + k)) & 1u) && g[k] < lim[t]) {
+                            const double h01 = 0.5 * cij2[t] - 0.5 * s01[t][k];
+                            const int d = decide_slow(h01, den[t][k], A.th);
+                            if (d != kDependent) {
+                                const int kk = t * 32 + lane;
+                                const bool dir1 = q[t] < lc;
+                                if (d == kNanError) nan = 1;
+                                else record_find(A, oi, q[t], S.te[kk], S.tj[kk], dir1,
+                                                 (dir1 ? (K0 | (1ull << kDirShift)) : K0) + (unsigned long long)g[k]);
+                                rel[t] = g[k];
+                                lim[t] = g[k];
+                                hit |= 1u << t;
+                            }
                         }
                     }
                 }
@@ -774,16 +816,20 @@ __device__ __forceinline__ void set_sweep_sp(const LevelArgs& A, SetWarpSmem<L>&
 #pragma unroll
             for (int k = 0; k < SP; ++k) {
                 g[k] = gn[k];
-                nxt[k] = alt[k];
+#pragma unroll
+                for (int t = 0; t < NT; ++t) nxt[t][k] = alt[t][k];
             }
             after = after2;
         }
-        const int hi = hit ? lim + 1 : min(seg_end, lim);
-        const int n = max(0, hi - sg0);
-        const bool in = dm >= sg0 && dm < sg0 + n;
-        tests += (unsigned)(n - (in ? 1 : 0));
-        const unsigned rm = n >= 32 ? 0xffffffffu : (((1u << n) - 1u) << sg0);
-        degen += (unsigned)(__popc(dead & rm) - ((in && ((dead >> dm) & 1u)) ? 1 : 0));
+#pragma unroll
+        for (int t = 0; t < NT; ++t) {
+            const int hi = ((hit >> t) & 1u) ? lim[t] + 1 : min(seg_end, lim[t]);
+            const int n = max(0, hi - sg0);
+            const bool in = dm[t] >= sg0 && dm[t] < sg0 + n;
+            tests += (unsigned)(n - (in ? 1 : 0));
+            const unsigned rm = n >= 32 ? 0xffffffffu : (((1u << n) - 1u) << sg0);
+            degen += (unsigned)(__popc(dead & rm) - ((in && ((dead >> dm[t]) & 1u)) ? 1 : 0));
+        }
         sg = seg_end;
     }
 }
@@ -797,15 +843,6 @@ __device__ __forceinline__ void set_sweep_sp(const LevelArgs& A, SetWarpSmem<L>&
 // "dependent" (stats.hpp:301-305) without any arithmetic: those sets are counted, never visited
 // (rank-truncated inputs hit this often: ~29% of C2's level-3 sets), and the last-member
 // prefetch always targets the next LIVE set, so skipped sets cost no L2 round trip either.
-// Key of a find: the target's direction (q < lc: j < i, direction 1 of edge (j, i)) and the set's
-// full-row rank; both directions' mirror entries of the edge are lowered with the key.
-__device__ __forceinline__ void record_find(const LevelArgs& A, int oi, int q, int e, int j, bool dir1,
-                                            unsigned long long key) {
-    atomicMin(A.keys + e, key);
-    atomicMin(A.kdir + oi + q, key);
-    atomicMin(A.kdir + A.off[j] + (dir1 ? A.eu_qa[e] : A.eu_qb[e]), key);
-}
-
 template <int L, int NT>
 __device__ __forceinline__ void set_sweep(const LevelArgs& A, SetWarpSmem<L>& S, int lane, int oi, int lc, int nlive,
                                           int nvalid, unsigned segmask, unsigned livemask, unsigned long long K0,
@@ -1108,11 +1145,15 @@ __global__ void __launch_bounds__(kSetWarps * 32, PCS_SET_MINB) level_set_kernel
                 else set_sweep<L, 1>(A, S, lane, oi, lc, nlive, nvalid, segmask, livemask, K0, tests, degen, nan);
             } else if constexpr (SetCfg<L>::NT == 3) {
                 if (nt == 3) set_sweep<L, 3>(A, S, lane, oi, lc, nlive, nvalid, segmask, livemask, K0, tests, degen, nan);
+#if PCS_NT2_SP > 1
+                else if (nt == 2) set_sweep_tsp<L, 2, PCS_NT2_SP>(A, S, lane, oi, lc, nlive, nvalid, segmask, livemask, K0, tests, degen, nan);
+#else
                 else if (nt == 2) set_sweep<L, 2>(A, S, lane, oi, lc, nlive, nvalid, segmask, livemask, K0, tests, degen, nan);
-                else set_sweep_sp<L, PCS_SET_SP>(A, S, lane, oi, lc, nlive, nvalid, segmask, livemask, K0, tests, degen, nan);
+#endif
+                else set_sweep_tsp<L, 1, PCS_SET_SP>(A, S, lane, oi, lc, nlive, nvalid, segmask, livemask, K0, tests, degen, nan);
             } else {
                 if (nt == 2) set_sweep<L, 2>(A, S, lane, oi, lc, nlive, nvalid, segmask, livemask, K0, tests, degen, nan);
-                else set_sweep_sp<L, 2>(A, S, lane, oi, lc, nlive, nvalid, segmask, livemask, K0, tests, degen, nan);
+                else set_sweep_tsp<L, 1, 2>(A, S, lane, oi, lc, nlive, nvalid, segmask, livemask, K0, tests, degen, nan);
             }
             __syncwarp();
         }

@@ -41,8 +41,8 @@ for s in $STEPS; do
         --no-secondary > $OUT/trace_c3.json 2> $OUT/trace_c3.err
       ;;
     ncufull)
-      timeout 900 ncu --set full --clock-control none --import-source on -k regex:level_set --launch-skip 2 -c 1 -f -o $OUT/top \
-        python tools/profile_target.py 3 32 set > $OUT/ncu_full.log 2>&1
+      timeout 900 ncu --set full --clock-control none --import-source on -k regex:level_set --launch-skip 1 -c 1 -f -o $OUT/top \
+        python tools/profile_target.py 3 16 set > $OUT/ncu_full.log 2>&1
       ;;
     balance)
       timeout 900 python tools/shard_balance.py 8 C2 3 set > $OUT/balance.json 2> $OUT/balance.err
@@ -61,8 +61,8 @@ for s in $STEPS; do
     ncu)
       timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/launches.csv \
         python bench.py --steps 1 --warmup 0 --no-cpu-baseline --no-e2e --no-secondary > $OUT/ncu_bench.log 2>&1
-      timeout 900 ncu --set full --clock-control none --import-source on -k regex:level_set --launch-skip 2 -c 1 -f -o $OUT/top \
-        python tools/profile_target.py 3 32 set > $OUT/ncu_full.log 2>&1
+      timeout 900 ncu --set full --clock-control none --import-source on -k regex:level_set --launch-skip 1 -c 1 -f -o $OUT/top \
+        python tools/profile_target.py 3 16 set > $OUT/ncu_full.log 2>&1
       ;;
   esac
 done

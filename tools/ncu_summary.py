@@ -95,8 +95,8 @@ stalls = sorted(((a.replace("smsp__average_warps_issue_stalled_", "").replace("_
 summary["top_stalls_per_issue"] = stalls
 if summary["dram_read_bytes"] is not None:
     summary["traffic_bytes_per_launch"] = summary["dram_read_bytes"] + (summary["dram_write_bytes"] or 0)
-summary["capture"] = (f"ncu --set full --clock-control none --import-source on -k regex:level_set --launch-skip 2 -c 1 "
-                      f"python tools/profile_target.py 3 32 set  (report gpurun_out/{os.path.basename(rep)})")
+summary["capture"] = (f"ncu --set full --clock-control none --import-source on -k regex:level_set --launch-skip 1 -c 1 "
+                      f"python tools/profile_target.py 3 16 set  (report gpurun_out/{os.path.basename(rep)})")
 if os.path.exists(bench):
     try:
         b = json.loads(open(bench).read().strip().splitlines()[-1])
