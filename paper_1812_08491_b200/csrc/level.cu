@@ -37,6 +37,9 @@ __device__ __noinline__ int decide_slow(double h01, double denom, Thresholds th)
 #ifndef PCS_UNRANK_BSEARCH
 #define PCS_UNRANK_BSEARCH 0  // 1: phase-1 unrank by per-member binary search over the binomial table
 #endif
+#ifndef PCS_FILTER3
+#define PCS_FILTER3 0       // 1: common-path filter without the integer degenerate test (surely_dependent3)
+#endif
 #ifndef PCS_NT2_SP
 #define PCS_NT2_SP 1        // sets per step for two-targets-per-lane batches (L <= 3); 1: plain set_sweep
 #endif
@@ -929,7 +932,11 @@ __device__ __forceinline__ void set_sweep(const LevelArgs& A, SetWarpSmem<L>& S,
             unsigned cand = 0;
 #pragma unroll
             for (int t = 0; t < NT; ++t)
+#if PCS_FILTER3
+                cand |= (unsigned)((sgx < lim[t]) & (sgx != dm[t]) & !surely_dependent3(h2[t], den[t], hi2x4)) << t;
+#else
                 cand |= (unsigned)((sgx < lim[t]) & (sgx != dm[t]) & !surely_dependent2(h2[t], den[t], hi2x4)) << t;
+#endif
             if (__any_sync(0xffffffffu, cand)) {
 #pragma unroll
                 for (int t = 0; t < NT; ++t) {

@@ -323,6 +323,13 @@ __device__ __forceinline__ bool surely_dependent2(double h2, double denom, doubl
     return (h2 * h2 >= fma(denom, hi2x4, kTiny4)) | (__double_as_longlong(denom) <= 0);
 }
 
+// The comparison alone (3 FP64 ops, no integer test): a degenerate denom <= 0 makes the right-hand
+// side <= 4e-240, so it is certified too unless |h2| < 2e-120 (then the exact path decides it).
+__device__ __forceinline__ bool surely_dependent3(double h2, double denom, double hi2x4) {
+    constexpr double kTiny4 = 4.0 * 1e-240;
+    return h2 * h2 >= fma(denom, hi2x4, kTiny4);
+}
+
 // Level-0 decision on rho = clamp(c_ij) (stats.hpp:309-312).
 __device__ __forceinline__ int decide0(double c, const Thresholds& th) {
     const double ac = fabs(c);
