@@ -158,8 +158,12 @@ pcs_status pcs_session_create_device(const double* d_c, int64_t ldc, int32_t p, 
                                      pcs_session** out);
 /* starts the next level; *running = 0 once the loop has stopped (stop reason recorded) */
 pcs_status pcs_session_level_begin(pcs_session* s, int32_t* running, int32_t* ell, int64_t* num_keys);
-/* pass 0: edges tested from their lower endpoint's row; pass 1: from the upper endpoint's row */
+/* pass 0: edges tested from their lower endpoint's row; pass 1: from the upper endpoint's row.
+   cuPC-S levels >= 2 (register-template kernel) test both directions in pass 0 and pass 1 is empty. */
 pcs_status pcs_session_level_pass(pcs_session* s, int32_t pass);
+/* number of passes the current level needs (1 when pass 0 covers both directions, else 2): a
+   multi-GPU caller MIN-reduces the keys after each of them */
+pcs_status pcs_session_level_passes(pcs_session* s, int32_t* passes);
 /* device pointer to the level's int64 key array (num_keys entries; MIN-reduce across ranks) */
 pcs_status pcs_session_keys(pcs_session* s, void** device_ptr, int64_t* count);
 pcs_status pcs_session_level_end(pcs_session* s);

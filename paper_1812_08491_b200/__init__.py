@@ -592,6 +592,14 @@ class Session:
         if rc:
             _raise(rc)
 
+    def level_passes(self) -> int:
+        """1 when pass 0 tests both edge directions (cuPC-S levels >= 2), else 2."""
+        n = ct.c_int32()
+        rc = library().pcs_session_level_passes(self._h, ct.byref(n))
+        if rc:
+            _raise(rc)
+        return n.value
+
     def keys(self) -> tuple[int, int]:
         ptr, n = ct.c_void_p(), ct.c_int64()
         rc = library().pcs_session_keys(self._h, ct.byref(ptr), ct.byref(n))

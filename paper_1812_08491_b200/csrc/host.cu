@@ -580,6 +580,16 @@ pcs_status pcs_session_level_begin(pcs_session* s, int32_t* running, int32_t* el
     return PCS_OK;
 }
 
+static bool merged_level(const pcs_session* s) {
+    return s->cfg.variant == PCS_VARIANT_SET && s->ell >= 2 && s->ell <= kMaxTemplLevel && merge_passes();
+}
+
+pcs_status pcs_session_level_passes(pcs_session* s, int32_t* passes) {
+    if (!s || !passes) return fail(PCS_EINVAL, "null argument");
+    *passes = (s->in_level && merged_level(s)) ? 1 : 2;
+    return PCS_OK;
+}
+
 pcs_status pcs_session_level_pass(pcs_session* s, int32_t pass) {
     if (!s || !s->in_level) return fail(PCS_EINVAL, "no level in progress");
     if (pass != 0 && pass != 1) return fail(PCS_EINVAL, "pass must be 0 or 1");
@@ -588,7 +598,7 @@ pcs_status pcs_session_level_pass(pcs_session* s, int32_t pass) {
     // "pass 2"; pass 1 has nothing left): every set's pseudo-inverse is computed once per level instead
     // of once per direction, at the price of testing direction 1 of edges that direction 0 separates
     // in the same level (their keys stay the direction-0 ones: MIN).  Results are unchanged.
-    const bool merged = s->cfg.variant == PCS_VARIANT_SET && s->ell >= 2 && s->ell <= kMaxTemplLevel && merge_passes();
+    const bool merged = merged_level(s);
     if (merged && pass == 1) return PCS_OK;
     const int kpass = merged ? 2 : pass;
     CUDA_TRY(cudaSetDevice(s->device));
@@ -719,6 +729,9 @@ pcs_status pcs_session_level_end(pcs_session* s) {
         L.kernel_ms = ms;
     }
     L.elapsed_s = now_s() - s->t_level;
+    if (c.dbg[0])
+        trace("level %d filter: %llu steps, %llu candidate tests, %llu steps with a candidate", s->ell,
+              (unsigned long long)c.dbg[0], (unsigned long long)c.dbg[1], (unsigned long long)c.dbg[2]);
     trace("level %d: %.3f ms host (kernels %.3f ms), %llu serial / %llu device tests, %llu removed", L.level,
           L.elapsed_s * 1e3, L.kernel_ms, (unsigned long long)L.ci_tests, (unsigned long long)L.device_ci_tests,
           (unsigned long long)L.edges_removed);

@@ -37,8 +37,8 @@ __device__ __noinline__ int decide_slow(double h01, double denom, Thresholds th)
 #ifndef PCS_UNRANK_BSEARCH
 #define PCS_UNRANK_BSEARCH 0  // 1: phase-1 unrank by per-member binary search over the binomial table
 #endif
-#ifndef PCS_FILTER3
-#define PCS_FILTER3 0       // 1: common-path filter without the integer degenerate test (surely_dependent3)
+#ifndef PCS_COUNT_CAND
+#define PCS_COUNT_CAND 0    // 1: diagnostics counters of the common-path filter (PCS_TRACE prints them)
 #endif
 #ifndef PCS_NT2_SP
 #define PCS_NT2_SP 1        // sets per step for two-targets-per-lane batches (L <= 3); 1: plain set_sweep
@@ -932,10 +932,16 @@ __device__ __forceinline__ void set_sweep(const LevelArgs& A, SetWarpSmem<L>& S,
             unsigned cand = 0;
 #pragma unroll
             for (int t = 0; t < NT; ++t)
-#if PCS_FILTER3
-                cand |= (unsigned)((sgx < lim[t]) & (sgx != dm[t]) & !surely_dependent3(h2[t], den[t], hi2x4)) << t;
-#else
                 cand |= (unsigned)((sgx < lim[t]) & (sgx != dm[t]) & !surely_dependent2(h2[t], den[t], hi2x4)) << t;
+#if PCS_COUNT_CAND  // diagnostics build only: steps, candidate tests, steps whose vote fired
+            {
+                const unsigned nc = __reduce_add_sync(0xffffffffu, (unsigned)__popc(cand));
+                if (lane == 0) {
+                    atomicAdd(&A.cnt->dbg[0], 1ull);
+                    atomicAdd(&A.cnt->dbg[1], (unsigned long long)nc);
+                    if (nc) atomicAdd(&A.cnt->dbg[2], 1ull);
+                }
+            }
 #endif
             if (__any_sync(0xffffffffu, cand)) {
 #pragma unroll

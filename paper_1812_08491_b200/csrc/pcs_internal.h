@@ -25,6 +25,7 @@ struct Counters {
     unsigned long long gpu_exact;   // tests whose statistic was evaluated (not a zero-h00 set)
     unsigned long long rec_count;   // sepset records written
     unsigned long long units[2];    // persistent-grid work cursors (pass A / B)
+    unsigned long long dbg[4];      // diagnostics builds only (PCS_COUNT_CAND)
     int err_nan;                    // fisher_z would throw (NaN statistic)
     int err_other;
 };

@@ -23,9 +23,10 @@ def level_loop(session, allreduce_min: Optional[Callable[[object, int], None]], 
         running, ell, nkeys = session.level_begin()
         if not running:
             break
+        passes = session.level_passes() if hasattr(session, "level_passes") else 2
         for pass_index in (0, 1):
             session.level_pass(pass_index)
-            if world > 1 and nkeys > 0 and allreduce_min is not None:
+            if pass_index < passes and world > 1 and nkeys > 0 and allreduce_min is not None:
                 keys, n = session.keys()
                 allreduce_min(keys, n)
         session.level_end()

@@ -49,6 +49,9 @@ for s in $STEPS; do
       timeout 600 python tools/shard_balance.py 8 C3 -1 set >> $OUT/balance.json 2>> $OUT/balance.err
       timeout 600 python tools/shard_balance.py 8 C2 2 edge >> $OUT/balance.json 2>> $OUT/balance.err
       ;;
+    candtrace)
+      PCS_TRACE=1 timeout 900 python tools/variants.py run cand --workload C2 --max-level 3 --repeats 1 > $OUT/cand.json 2> $OUT/cand.err
+      ;;
     variants)
       timeout 900 python tools/variants.py run --workload C2 --max-level 3 --repeats 2 > $OUT/variants.json 2> $OUT/variants.err
       ;;
