@@ -485,26 +485,44 @@ __global__ void __launch_bounds__(kL1Threads) level1_kernel(LevelArgs A, int pas
         }
         __syncthreads();
         if (active) {
+            const double hi2 = A.th.hi2;
             for (int t = 0; t < n && active; t += kL1Unroll) {
                 double cjk[kL1Unroll];
 #pragma unroll
                 for (int u = 0; u < kL1Unroll; ++u)
                     cjk[u] = (t + u < n) ? __ldg(Cj + (size_t)s_k[t + u] * ldc) : 0.0;
+                // branch-free common path (as in the cuPC-S kernel): h01 = c_ij - c_ik c_jk and
+                // denom = (1 - c_ik^2)(1 - c_jk^2) in the reference's rounding (M2^+ = [1] exactly, the
+                // symmetrised h01 collapses: d01 == d10), certified-dependent filter, exact decision
+                // only for the rare candidates, in set order
+                double h01[kL1Unroll], den[kL1Unroll];
+                unsigned valid = 0, cand = 0;
 #pragma unroll
                 for (int u = 0; u < kL1Unroll; ++u) {
                     const int s = s0 + t + u;
-                    if (!active || t + u >= n || s == q) continue;
+                    const bool ok = t + u < n && s != q;
                     const double h11 = 1.0 - cjk[u] * cjk[u];
-                    const double h01 = cij - s_cik[t + u] * cjk[u];
-                    const double denom = s_h00[t + u] * h11;
-                    const int d = decide_fast(h01, denom, A.th);
-                    ++tests;
-                    if (d != kDependent) {
-                        active = false;
-                        if (d == kNanError) nan = 1;
-                        else atomicMin(A.keys + e, dirbits | (unsigned long long)s);
+                    h01[u] = cij - s_cik[t + u < n ? t + u : 0] * cjk[u];
+                    den[u] = s_h00[t + u < n ? t + u : 0] * h11;
+                    valid |= (unsigned)ok << u;
+                    cand |= (unsigned)(ok & !surely_dependent(h01[u], den[u], hi2)) << u;
+                }
+                unsigned done = valid;
+                if (cand) {
+#pragma unroll
+                    for (int u = 0; u < kL1Unroll; ++u) {
+                        if (!((cand >> u) & 1u)) continue;
+                        const int d = decide_slow(h01[u], den[u], A.th);
+                        if (d != kDependent) {
+                            active = false;
+                            if (d == kNanError) nan = 1;
+                            else atomicMin(A.keys + e, dirbits | (unsigned long long)(s0 + t + u));
+                            done = valid & ((2u << u) - 1u);  // tests up to and including the find
+                            break;
+                        }
                     }
                 }
+                tests += (unsigned)__popc(done);
             }
         }
         __syncthreads();

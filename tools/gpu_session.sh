@@ -52,6 +52,10 @@ for s in $STEPS; do
     candtrace)
       PCS_TRACE=1 timeout 900 python tools/variants.py run cand --workload C2 --max-level 3 --repeats 1 > $OUT/cand.json 2> $OUT/cand.err
       ;;
+    variantsl1)
+      timeout 900 python tools/variants.py run --workload C5 --max-level 1 --repeats 2 > $OUT/variants_c5.json 2> $OUT/variants_c5.err
+      timeout 900 python tools/variants.py run --workload C3 --max-level -1 --repeats 3 > $OUT/variants_c3.json 2> $OUT/variants_c3.err
+      ;;
     variants)
       timeout 900 python tools/variants.py run --workload C2 --max-level 3 --repeats 2 > $OUT/variants.json 2> $OUT/variants.err
       ;;

@@ -15,7 +15,8 @@ import time
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 VDIR = os.path.join(ROOT, "paper_1812_08491_b200", "variants")
-SHAPES = {"C2": (1000, 10000, 0.1, 1), "C3": (1643, 850, 0.01, 2), "C4": (5361, 63, 0.002, 3)}
+SHAPES = {"C2": (1000, 10000, 0.1, 1), "C3": (1643, 850, 0.01, 2), "C4": (5361, 63, 0.002, 3),
+          "C5": (5000, 5000, 0.05, 4)}  # C5: rescaled generator
 
 
 def cmd_build(specs):
@@ -49,12 +50,18 @@ def cmd_run(names, workload, max_level, repeats):
     import paper_1812_08491_b200 as pcs
     p, m, d, case = SHAPES[workload]
     seed = 7919 * case
-    x = pcs.sample_linear_gaussian(pcs.random_dag(p, d, seed), m, seed + 1)
+    w = pcs.random_dag(p, d, seed)
+    x = pcs.sample_linear_gaussian_rescaled(w, m, seed + 1)[0] if workload == "C5" else pcs.sample_linear_gaussian(w, m, seed + 1)
+    del w
     c = pcs.compute_correlation(x)
     names = names or sorted(f[len("libpcstable_b200_"):-3] for f in os.listdir(VDIR) if f.endswith(".so"))
     cfg = pcs.SkeletonConfig(alpha=0.01, max_level=None if max_level < 0 else max_level)
-    base = pcs.run_pc_stable(c, m, cfg)
-    print(json.dumps({"variant": "default", "levels_ms": [round(l.kernel_ms, 3) for l in base.levels]}), flush=True)
+    best = None
+    for _ in range(repeats):  # best of `repeats`, like the variants (the first run pays lazy module loading)
+        base = pcs.run_pc_stable(c, m, cfg)
+        ms = [l.kernel_ms for l in base.levels]
+        best = ms if best is None or sum(ms) < sum(best) else best
+    print(json.dumps({"variant": "default", "levels_ms": [round(v, 3) for v in best]}), flush=True)
     import ctypes as ct
     for name in names:
         lib = os.path.join(VDIR, f"libpcstable_b200_{name}.so")
