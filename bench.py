@@ -241,14 +241,21 @@ def main():
     import torch.distributed as dist
 
     import paper_1812_08491_b200 as pcs
-    from paper_1812_08491_b200.multigpu import run_pc_stable_sharded
+    from paper_1812_08491_b200.multigpu import host_staged_allreduce_min, run_pc_stable_sharded
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # PCS_BENCH_BACKEND=gloo: ranks may share a GPU and keys are MIN-reduced through host memory -- only
+    # for validating the N-rank orchestration on a one-GPU box (its times are not a scaling number)
+    backend = os.environ.get("PCS_BENCH_BACKEND", "nccl")
     if world > 1:
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        local_dev = local % max(1, torch.cuda.device_count())
+        torch.cuda.set_device(local_dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local_dev))
+        else:
+            dist.init_process_group("gloo")
     dev = torch.cuda.current_device()
     p, m = wl["p"], wl["m"]
     seed = 7919 * wl["case"]
@@ -266,7 +273,8 @@ def main():
         if world == 1:
             return pcs.run_pc_stable_data_device(x_dev.data_ptr(), m, p, cfg)
         pcs.correlation_device(x_dev.data_ptr(), m, p, c_dev.data_ptr(), ldc, stream.cuda_stream)
-        return run_pc_stable_sharded(c_dev.data_ptr(), ldc, p, m, cfg, with_sepsets=False)
+        return run_pc_stable_sharded(c_dev.data_ptr(), ldc, p, m, cfg, with_sepsets=False,
+                                     allreduce_min=host_staged_allreduce_min() if backend != "nccl" else None)
 
     with torch.cuda.stream(stream):
         for _ in range(args.warmup):
@@ -291,7 +299,7 @@ def main():
     launches = pcs.kernel_launches() - launches0
     total_ms = sum(times)
     if world > 1:
-        t = torch.tensor([total_ms], dtype=torch.float64, device=f"cuda:{dev}")
+        t = torch.tensor([total_ms], dtype=torch.float64, device=f"cuda:{dev}" if backend == "nccl" else "cpu")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         total_ms = float(t.item())
         dist.barrier()
@@ -395,6 +403,10 @@ def main():
                                "kernel_ms": round(l.kernel_ms, 3)} for l in res.levels],
                 "l2": "flushed between timed steps (256 MiB write outside the events)",
                 "timing": "CUDA events on the library's stream per step, max over ranks",
+                "multi_gpu": (None if world == 1 else
+                              {"ranks": world, "backend": backend, "devices": torch.cuda.device_count(),
+                               "keys_merge": "MIN all-reduce of the level's keys after each pass "
+                                             "(once per level for cuPC-S levels >= 2)"}),
             },
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
             "secondary": secondary,
