@@ -346,6 +346,31 @@ def main():
         e2e = {"value": serial_tests / statistics.mean(et), "unit": "tests/s", "h2d_bytes_per_step": 8 * m * p,
                "d2h_bytes_per_step": 4 * p * ((p + 31) // 32) + 4 * rec_ints + 72 * len(r.levels),
                "s_per_step": statistics.mean(et), "removed_pairs": sep_n}
+    elif not args.no_e2e:
+        # N ranks: every rank copies X from pinned host memory, builds C, runs its shards (keys MIN-merged)
+        # and reads the skeleton back with its sepset records; host wall time, max over ranks
+        x_pin = torch.from_numpy(x_host).pin_memory()
+        et = []
+        for _ in range(max(1, args.steps)):
+            flush.zero_()
+            torch.cuda.synchronize()
+            dist.barrier()
+            t0 = time.perf_counter()
+            with torch.cuda.stream(stream):
+                x_dev.copy_(x_pin, non_blocking=True)
+                pcs.correlation_device(x_dev.data_ptr(), m, p, c_dev.data_ptr(), ldc, stream.cuda_stream)
+                r = run_pc_stable_sharded(c_dev.data_ptr(), ldc, p, m, cfg, with_sepsets=True,
+                                          allreduce_min=host_staged_allreduce_min() if backend != "nccl" else None)
+            sep_n = r.sepsets.stored_count()
+            dt = torch.tensor([time.perf_counter() - t0], dtype=torch.float64,
+                              device=f"cuda:{dev}" if backend == "nccl" else "cpu")
+            dist.all_reduce(dt, op=dist.ReduceOp.MAX)
+            et.append(float(dt.item()))
+        rec_ints = sum((3 + l.level) * l.edges_removed for l in r.levels if l.level >= 1)
+        e2e = {"value": serial_tests / statistics.mean(et), "unit": "tests/s", "h2d_bytes_per_step": 8 * m * p * world,
+               "d2h_bytes_per_step": (4 * p * ((p + 31) // 32) + 4 * rec_ints + 72 * len(r.levels)) * world,
+               "s_per_step": statistics.mean(et), "removed_pairs": sep_n,
+               "timing": "host wall time per step, max over ranks (every rank holds X and the result)"}
 
     # full (uncapped) runs of the other single-GPU BASELINE shapes, same device timing
     secondary = []

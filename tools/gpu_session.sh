@@ -65,7 +65,7 @@ for s in $STEPS; do
     bench2)
       PCS_BENCH_BACKEND=gloo timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 \
         --master-addr 127.0.0.1 --master-port 29517 bench.py --gpus 2 --steps 1 --warmup 1 --no-cpu-baseline \
-        --no-e2e --no-secondary > $OUT/bench2.json 2> $OUT/bench2.err
+        --no-secondary > $OUT/bench2.json 2> $OUT/bench2.err
       ;;
     bench)
       timeout 900 python bench.py > $OUT/bench.json 2> $OUT/bench.err
