@@ -46,6 +46,9 @@ __device__ __noinline__ int decide_slow(double h01, double denom, Thresholds th)
 #ifndef PCS_SET_SP
 #define PCS_SET_SP 2        // sets per step for one-target-per-lane batches (L <= 3)
 #endif
+#ifndef PCS_SET_NT_L2
+#define PCS_SET_NT_L2 3     // targets per lane per set at L = 2 (short tests: per-step overhead dominates)
+#endif
 #ifndef PCS_SET_MINB
 #define PCS_SET_MINB 4      // resident blocks per SM the set kernel is register-budgeted for
 #endif
@@ -578,7 +581,7 @@ constexpr int kSetWarps = 4;
 
 template <int L>
 struct SetCfg {
-    static constexpr int NT = L <= 3 ? PCS_SET_NT_SMALL : 2;  // targets per lane per set
+    static constexpr int NT = L == 2 ? PCS_SET_NT_L2 : (L <= 3 ? PCS_SET_NT_SMALL : 2);  // targets per lane per set
     static constexpr int kStage = 32 * NT;     // live targets staged per pass over the band
 };
 
@@ -1169,8 +1172,9 @@ __global__ void __launch_bounds__(kSetWarps * 32, PCS_SET_MINB) level_set_kernel
             __syncwarp();
             // ---- phase 2: sets in rank order, NT targets per lane
             const int nt = (nlive + 31) >> 5;
-            if constexpr (SetCfg<L>::NT == 4) {
-                if (nt == 4) set_sweep<L, 4>(A, S, lane, oi, lc, nlive, nvalid, segmask, livemask, K0, tests, degen, nan);
+            if constexpr (SetCfg<L>::NT >= 4) {
+                constexpr int NTM = SetCfg<L>::NT;
+                if (nt > 3) set_sweep<L, NTM>(A, S, lane, oi, lc, nlive, nvalid, segmask, livemask, K0, tests, degen, nan);
                 else if (nt == 3) set_sweep<L, 3>(A, S, lane, oi, lc, nlive, nvalid, segmask, livemask, K0, tests, degen, nan);
                 else if (nt == 2) set_sweep<L, 2>(A, S, lane, oi, lc, nlive, nvalid, segmask, livemask, K0, tests, degen, nan);
                 else set_sweep<L, 1>(A, S, lane, oi, lc, nlive, nvalid, segmask, livemask, K0, tests, degen, nan);

@@ -22,7 +22,7 @@ for s in $STEPS; do
     c5)
       timeout 900 python tools/explore.py C5a,C5b,C5c set 2 > $OUT/explore_c5.log 2>&1
       timeout 900 python tools/explore.py C5d set 1 >> $OUT/explore_c5.log 2>&1
-      timeout 900 python tools/explore.py C5e set 0 >> $OUT/explore_c5.log 2>&1
+      timeout 900 python tools/explore.py C5e set 1 >> $OUT/explore_c5.log 2>&1
       ;;
     merge)
       PCS_MERGE_PASSES=0 timeout 600 python tools/explore.py C2 set 3 2 > $OUT/merge_ab.log 2>&1
@@ -51,6 +51,10 @@ for s in $STEPS; do
       ;;
     candtrace)
       PCS_TRACE=1 timeout 900 python tools/variants.py run cand --workload C2 --max-level 3 --repeats 1 > $OUT/cand.json 2> $OUT/cand.err
+      ;;
+    variantsl2)
+      timeout 1500 python tools/variants.py run --workload C5 --max-level 2 --repeats 1 > $OUT/variants_c5l2.json 2> $OUT/variants_c5l2.err
+      timeout 900 python tools/variants.py run --workload C2 --max-level 2 --repeats 3 > $OUT/variants_c2l2.json 2> $OUT/variants_c2l2.err
       ;;
     variantsl1)
       timeout 900 python tools/variants.py run --workload C5 --max-level 1 --repeats 2 > $OUT/variants_c5.json 2> $OUT/variants_c5.err
