@@ -24,6 +24,12 @@ for s in $STEPS; do
       timeout 900 python tools/explore.py C5d set 1 >> $OUT/explore_c5.log 2>&1
       timeout 900 python tools/explore.py C5e set 1 >> $OUT/explore_c5.log 2>&1
       ;;
+    l1dense)
+      for v in 0 1; do
+        PCS_L1_DENSE=$v timeout 900 python tools/explore.py C5b,C5d set 1 2 >> $OUT/l1dense_$v.log 2>&1
+      done
+      PCS_L1_DENSE=1 timeout 900 python tools/explore.py C5e set 1 >> $OUT/l1dense_1.log 2>&1
+      ;;
     merge)
       PCS_MERGE_PASSES=0 timeout 600 python tools/explore.py C2 set 3 2 > $OUT/merge_ab.log 2>&1
       timeout 600 python tools/explore.py C2 set 3 2 >> $OUT/merge_ab.log 2>&1
