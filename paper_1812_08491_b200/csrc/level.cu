@@ -452,9 +452,10 @@ constexpr int kL1Unroll = 8;
 
 __global__ void __launch_bounds__(kL1Threads) level1_kernel(LevelArgs A, int pass, const unsigned long long* prefix,
                                                             unsigned long long tile_base) {
-    __shared__ int s_k[kL1Chunk];
-    __shared__ double s_cik[kL1Chunk];
-    __shared__ double s_h00[kL1Chunk];
+    // per candidate set k of the chunk: the row offset k * ldc of C(k, .) and (c_ik, 1 - c_ik^2), so a
+    // test costs one LDS, one LDS.128, one coalesced gather C(k, j) and its FP64 arithmetic
+    __shared__ int s_koff[kL1Chunk + kL1Unroll];
+    __shared__ double2 s_ch[kL1Chunk + kL1Unroll];
     const unsigned long long tile = tile_base + blockIdx.x;
     const int i = find_row(prefix, A.p, tile);
     const int t_in_row = (int)(tile - prefix[i]);
@@ -473,40 +474,44 @@ __global__ void __launch_bounds__(kL1Threads) level1_kernel(LevelArgs A, int pas
         if (pass == 1 && A.keys[e] != (unsigned long long)kNoneKey) active = false;
     }
     const unsigned long long dirbits = (unsigned long long)pass << kDirShift;
+    const double hi2 = A.th.hi2;
     unsigned long long tests = 0;
     int nan = 0;
     const double* __restrict__ Cj = C + j;
     for (int s0 = 0; s0 < w; s0 += kL1Chunk) {
         if (!__syncthreads_or(active)) break;
         const int n = min(kL1Chunk, w - s0);
-        for (int t = threadIdx.x; t < n; t += kL1Threads) {
-            const int k = A.nbr[oi + s0 + t];
-            const double cik = __ldg(C + (size_t)i * ldc + k);
-            s_k[t] = k;
-            s_cik[t] = cik;
-            s_h00[t] = 1.0 - cik * cik;
+        for (int t = threadIdx.x; t < n + kL1Unroll; t += kL1Threads) {
+            if (t < n) {
+                const int k = A.nbr[oi + s0 + t];
+                const double cik = __ldg(C + (size_t)i * ldc + k);
+                s_koff[t] = k * (int)ldc;  // p * ldc < 2^31 (p <= 46340)
+                s_ch[t] = make_double2(cik, 1.0 - cik * cik);
+            } else {  // padding read by the last unrolled group: a valid address, masked below
+                s_koff[t] = 0;
+                s_ch[t] = make_double2(0.0, 1.0);
+            }
         }
         __syncthreads();
         if (active) {
-            const double hi2 = A.th.hi2;
+            const int qrel = q - s0;  // the target's own position inside this chunk (not a test)
             for (int t = 0; t < n && active; t += kL1Unroll) {
                 double cjk[kL1Unroll];
 #pragma unroll
-                for (int u = 0; u < kL1Unroll; ++u)
-                    cjk[u] = (t + u < n) ? __ldg(Cj + (size_t)s_k[t + u] * ldc) : 0.0;
-                // branch-free common path (as in the cuPC-S kernel): h01 = c_ij - c_ik c_jk and
-                // denom = (1 - c_ik^2)(1 - c_jk^2) in the reference's rounding (M2^+ = [1] exactly, the
-                // symmetrised h01 collapses: d01 == d10), certified-dependent filter, exact decision
-                // only for the rare candidates, in set order
+                for (int u = 0; u < kL1Unroll; ++u) cjk[u] = __ldg(Cj + s_koff[t + u]);
+                // branch-free common path: h01 = c_ij - c_ik c_jk and denom = (1 - c_ik^2)(1 - c_jk^2)
+                // in the reference's rounding (M2^+ = [1] exactly, the symmetrised h01 collapses:
+                // d01 == d10), certified-dependent filter, exact decision only for the rare
+                // candidates, in set order
                 double h01[kL1Unroll], den[kL1Unroll];
                 unsigned valid = 0, cand = 0;
 #pragma unroll
                 for (int u = 0; u < kL1Unroll; ++u) {
-                    const int s = s0 + t + u;
-                    const bool ok = t + u < n && s != q;
+                    const double2 ch = s_ch[t + u];
+                    const bool ok = (t + u < n) & (t + u != qrel);
                     const double h11 = 1.0 - cjk[u] * cjk[u];
-                    h01[u] = cij - s_cik[t + u < n ? t + u : 0] * cjk[u];
-                    den[u] = s_h00[t + u < n ? t + u : 0] * h11;
+                    h01[u] = cij - ch.x * cjk[u];
+                    den[u] = ch.y * h11;
                     valid |= (unsigned)ok << u;
                     cand |= (unsigned)(ok & !surely_dependent(h01[u], den[u], hi2)) << u;
                 }

@@ -46,6 +46,10 @@ for s in $STEPS; do
       PCS_TRACE=1 timeout 600 python bench.py --workload C3 --steps 2 --warmup 2 --no-cpu-baseline --no-e2e \
         --no-secondary > $OUT/trace_c3.json 2> $OUT/trace_c3.err
       ;;
+    ncul1)
+      timeout 900 ncu --set full --clock-control none --import-source on -k regex:level1_kernel -c 1 -f -o $OUT/l1 \
+        python tools/explore.py C5b set 1 > $OUT/ncu_l1.log 2>&1
+      ;;
     ncufull)
       timeout 900 ncu --set full --clock-control none --import-source on -k regex:level_set --launch-skip 1 -c 1 -f -o $OUT/top \
         python tools/profile_target.py 3 16 set > $OUT/ncu_full.log 2>&1
