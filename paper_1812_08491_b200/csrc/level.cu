@@ -17,6 +17,8 @@
 // serial strategy's choice regardless of schedule.
 //
 // Compiled with -fmad=false: decisions are bit-identical to oracle/pcs_oracle.c.
+#include <cstddef>
+
 #include "pcs_internal.h"
 
 namespace pcs {
@@ -36,6 +38,9 @@ __device__ __noinline__ int decide_slow(double h01, double denom, Thresholds th)
 #endif
 #ifndef PCS_UNRANK_BSEARCH
 #define PCS_UNRANK_BSEARCH 0  // 1: phase-1 unrank by per-member binary search over the binomial table
+#endif
+#ifndef PCS_SMEM_PTX
+#define PCS_SMEM_PTX 1      // 1: the step loop reads the set slots by 32-bit shared addresses (inline PTX)
 #endif
 #ifndef PCS_COUNT_CAND
 #define PCS_COUNT_CAND 0    // 1: diagnostics counters of the common-path filter (PCS_TRACE prints them)
@@ -863,6 +868,71 @@ __device__ __forceinline__ void set_sweep_tsp(const LevelArgs& A, SetWarpSmem<L>
     }
 }
 
+// Shared-state-space loads by 32-bit address (PCS_SMEM_PTX): the step loop then carries one 32-bit
+// slot base instead of rematerialising a generic (cluster-window) pointer every step.
+__device__ __forceinline__ double2 lds_f64x2(uint32_t a) {
+    double2 v;
+    asm("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ double lds_f64(uint32_t a) {
+    double v;
+    asm("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ int lds_s32(uint32_t a) {
+    int v;
+    asm("ld.shared.s32 %0, [%1];" : "=r"(v) : "r"(a));
+    return v;
+}
+
+template <int L, int NT, int LP>
+__device__ __forceinline__ void h_terms_stream_sa(uint32_t sla, const double (&cp)[NT][LP],
+                                                  const double (&cur)[NT], const double (&cij2)[NT],
+                                                  double (&s01)[NT], double (&h2)[NT], double (&den)[NT]) {
+    double d11[NT], d01[NT], d10[NT];
+#pragma unroll
+    for (int col = 0; col < L; ++col) {
+        double cv[SetSlot<L>::CW];
+#pragma unroll
+        for (int k = 0; k < SetSlot<L>::CW; k += 2) {
+            const double2 v = lds_f64x2(sla + (uint32_t)offsetof(SetSlot<L>, col) +
+                                        (uint32_t)((col * SetSlot<L>::CW + k) * sizeof(double)));
+            cv[k] = v.x;
+            cv[k + 1] = v.y;
+        }
+        const double* mc = cv;
+        const double ci = cv[L], pc = cv[L + 1];
+#pragma unroll
+        for (int t = 0; t < NT; ++t) {
+            double x[L];
+#pragma unroll
+            for (int a = 0; a < L - 1; ++a) x[a] = cp[t][a];
+            x[L - 1] = cur[t];
+            double pcol = x[0] * mc[0];
+#pragma unroll
+            for (int k = 1; k < L; ++k) pcol = pcol + x[k] * mc[k];
+            if (col == 0) {
+                d11[t] = pcol * x[0];
+                d01[t] = pc * x[0];
+                d10[t] = pcol * ci;
+            } else {
+                d11[t] = d11[t] + pcol * x[col];
+                d01[t] = d01[t] + pc * x[col];
+                d10[t] = d10[t] + pcol * ci;
+            }
+        }
+    }
+    const double h00 = lds_f64(sla + (uint32_t)offsetof(SetSlot<L>, h00));
+#pragma unroll
+    for (int t = 0; t < NT; ++t) {
+        const double h11 = 1.0 - d11[t];
+        s01[t] = d01[t] + d10[t];
+        h2[t] = cij2[t] - s01[t];
+        den[t] = h00 * h11;
+    }
+}
+
 // Phase 2 for one staged batch of targets, NT (<= SetCfg<L>::NT) per lane.
 // segmask: bit s set when set s starts a new run of equal leading L-1 members.  Inside a
 // run (lexicographic order) the last member's position advances by one per set: set
@@ -877,6 +947,9 @@ __device__ __forceinline__ void set_sweep(const LevelArgs& A, SetWarpSmem<L>& S,
                                           int nvalid, unsigned segmask, unsigned livemask, unsigned long long K0,
                                           unsigned long long& tests, unsigned long long& degen, int& nan) {
     const double* __restrict__ C = A.C;
+#if PCS_SMEM_PTX
+    const uint32_t slot0 = (uint32_t)__cvta_generic_to_shared(&S.slot[0]);
+#endif
     const double hi2x4 = 4.0 * A.th.hi2;  // exact (power-of-two scaling)
     int rel[NT];           // tested while the set index is below rel (relative key)
     const double* Cj[NT];  // C + j: gathers C(mem, j) = Cj[t][mem * ldc] (one IMAD.WIDE each)
@@ -946,6 +1019,17 @@ __device__ __forceinline__ void set_sweep(const LevelArgs& A, SetWarpSmem<L>& S,
         // double-buffered last-member gathers: step(s, n, cur, pre) tests live set s with `cur` while
         // prefetching live set n (the next one, possibly in a later run) into `pre`
         auto step = [&](int sgx, int nxs, const double (&cur)[NT], double (&pre)[NT]) {
+#if PCS_SMEM_PTX
+            {  // clamped: always a valid slot
+                const int ro = lds_s32(slot0 + (uint32_t)(min(nxs, nvalid - 1) * (int)sizeof(SetSlot<L>)) +
+                                       (uint32_t)(offsetof(SetSlot<L>, roff) + (L - 1) * sizeof(int)));
+#pragma unroll
+                for (int t = 0; t < NT; ++t) pre[t] = __ldg(Cj[t] + ro);
+            }
+            double s01[NT], h2[NT], den[NT];
+            h_terms_stream_sa<L, NT, LP>(slot0 + (uint32_t)(sgx * (int)sizeof(SetSlot<L>)), cp, cur, cij2, s01, h2,
+                                         den);
+#else
             const SetSlot<L>& sl = S.slot[sgx];
             {  // clamped: always a valid slot
                 const int ro = S.slot[min(nxs, nvalid - 1)].roff[L - 1];
@@ -954,6 +1038,7 @@ __device__ __forceinline__ void set_sweep(const LevelArgs& A, SetWarpSmem<L>& S,
             }
             double s01[NT], h2[NT], den[NT];
             h_terms_stream<L, NT, LP>(sl, cp, cur, cij2, s01, h2, den);
+#endif
             // branch-free common path: flag the (rare) tests not certainly dependent
             unsigned cand = 0;
 #pragma unroll
