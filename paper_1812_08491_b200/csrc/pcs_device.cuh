@@ -318,9 +318,11 @@ __device__ __forceinline__ bool surely_dependent(double h01, double denom, doubl
 // 2 RN(c - s/2) = 2 h01 exactly (if s/2 is inexact, s is subnormal and both sides round to c),
 // h2^2 = 4 RN(h01^2) and RN(denom * 4hi2 + 4e-240) = 4 RN(denom * hi2 + 1e-240), so the
 // unscaled filter holds as well.
+// (The integer test only needs the sign bit: a negative / -0 / negative-NaN denom is degenerate; +0
+// falls to the comparison, whose right-hand side is then 4e-240, or to the exact path.)
 __device__ __forceinline__ bool surely_dependent2(double h2, double denom, double hi2x4) {
     constexpr double kTiny4 = 4.0 * 1e-240;
-    return (h2 * h2 >= fma(denom, hi2x4, kTiny4)) | (__double_as_longlong(denom) <= 0);
+    return (h2 * h2 >= fma(denom, hi2x4, kTiny4)) | (__double2hiint(denom) < 0);
 }
 
 // The comparison alone (3 FP64 ops, no integer test): a degenerate denom <= 0 makes the right-hand
