@@ -53,7 +53,6 @@ WORKLOADS = {
     # (level 2 of this shape is 7.4e13 serial CI tests, ~100 s on one B200)
     "C5": dict(p=5000, m=5000, d=0.05, alpha=0.01, case=4, max_level=1, rescaled=True),
 }
-SNAPSHOT_FIXTURE = os.path.join(ROOT, "tests", "golden", "c2_level3_snapshot.npz")
 
 
 def describe(name: str, wl: dict) -> str:
@@ -132,62 +131,137 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------------- CPU side (reference arm / cpu_baseline)
-def cpu_sample(name: str, wl: dict, target_s: float, threads: int):
-    """Times the reference's fastest strategy (SetShared, all host threads) on a bounded sample of the
-    workload with the CPU oracle; returns (tests_per_s, description)."""
-    from oracle import pyoracle as O  # test infrastructure: the reference restated on the CPU
+SNAPSHOTS = {"C2": os.path.join(ROOT, "tests", "golden", "c2_snapshots.npz")}
+GOLDEN = {"C2": os.path.join(ROOT, "tests", "golden", "c2_full.npz")}
+CPU_WHOLE = ("C1", "C3", "C4")  # configs the reference finishes whole in seconds on the host
 
+
+def _cpu_data(O, wl):
     seed = 7919 * wl["case"]
     w = O.random_dag(wl["p"], wl["d"], seed)
-    x = O.sample_linear_gaussian(w, wl["m"], seed + 1)
-    c = O.compute_correlation(x, threads=threads)
-    cfg = O.config(alpha=wl["alpha"], strategy=O.SET, workers=threads, set_groups=max(2, threads),
-                   max_level=wl["max_level"])
-    if name == "C2":
-        if not os.path.exists(SNAPSHOT_FIXTURE):
-            raise FileNotFoundError(SNAPSHOT_FIXTURE)
-        z = np.load(SNAPSHOT_FIXTURE)
-        off, idx = z["offsets"], z["indices"]
-        ell = int(z["level"])
-        tau = O.threshold_tau(wl["alpha"], wl["m"], ell)
-        widths = np.diff(off)
-        cost = np.array([math.comb(int(wd), ell) * max(int(wd) - ell, 0) for wd in widths], dtype=float)
-        nz = np.nonzero(cost > 0)[0]
-        nz = nz[np.argsort(cost[nz], kind="stable")]
-        budget = target_s * threads * 7e6  # ~7e6 level-3 tests/s per core (measured on this oracle)
-        rows, acc = [], 0.0
-        for r in nz[int(0.4 * len(nz)):]:  # from the 40th cost percentile up: representative rows
-            if acc >= budget:
-                break
-            rows.append(int(r))
-            acc += cost[r]
-        t0 = time.time()
-        st = run_rows(O, c, off, idx, ell, tau, cfg, rows)
-        dt = time.time() - t0
-        desc = (f"level {ell} of {name} (reference SetShared strategy, {threads} threads, set_groups={cfg.set_groups})"
-                f" on {len(rows)} of {int((widths > ell).sum())} rows of the level-{ell} snapshot "
-                f"(tests/golden/c2_level3_snapshot.npz): {st.ci_tests:.3e} CI tests in {dt:.2f} s")
-        return st.ci_tests / dt, desc
-    # whole workload on the CPU (small configs)
-    t0 = time.time()
-    r = O.run_pc_stable(c, wl["m"], cfg)
-    dt = time.time() - t0
-    tests = sum(l.ci_tests for l in r.levels)
-    return tests / dt, (f"full {name} run (reference SetShared strategy, {threads} threads): {tests:.3e} CI tests "
-                        f"in {dt:.2f} s")
+    return O.sample_linear_gaussian(w, wl["m"], seed + 1)  # (p, m): row j = variable j
 
 
-def run_rows(O, c, off, idx, ell, tau, cfg, rows):
-    """The reference's level on a snapshot restricted to `rows` (rows are independent units)."""
+def _snapshot_csr(packed: np.ndarray, p: int):
+    iu, ju = np.triu_indices(p, 1)
+    bits = np.unpackbits(packed)[:len(iu)].astype(bool)
+    adj = np.zeros((p, p), bool)
+    adj[iu[bits], ju[bits]] = True
+    adj |= adj.T
+    off = np.concatenate([[0], np.cumsum(adj.sum(1))]).astype(np.int32)
+    idx = np.nonzero(adj)[1].astype(np.int32)
+    return off, idx
+
+
+def _rows_sub(off, idx, rows):
+    """The snapshot restricted to `rows` (the others empty: their units skip, skeleton.hpp:54-70)."""
     keep = np.zeros(len(off) - 1, bool)
     keep[np.asarray(rows, int)] = True
-    off2 = [0]
-    idx2 = []
-    for i in range(len(off) - 1):
-        if keep[i]:
-            idx2.extend(idx[off[i]:off[i + 1]].tolist())
-        off2.append(len(idx2))
-    return O.run_level(c, np.asarray(off2, np.int32), np.asarray(idx2, np.int32), ell, tau, cfg)
+    w = np.diff(off)
+    w2 = np.where(keep, w, 0)
+    off2 = np.concatenate([[0], np.cumsum(w2)]).astype(np.int32)
+    sel = np.repeat(keep, w)
+    return off2, np.ascontiguousarray(idx[sel], np.int32)
+
+
+def _level_estimate(O, c, off, idx, ell, tau, cfg, budget_s, strata=8):
+    """Whole-level CPU time of the reference's SetShared level (skeleton.hpp:325-333) estimated from a
+    stratified row sample: rows sorted by modelled cost C(w, l) (w - l) (sets x targets), cut into
+    `strata` bands of equal total cost; every band gets budget_s / strata of measured work (rows taken
+    spread across the band, cheapest-first only where one row would exceed the band's budget) and its
+    measured rate (modelled cost per second) extrapolates the band.  Rows are independent units of
+    the level, so a row's time does not depend on which other rows run."""
+    w = np.diff(off).astype(np.int64)
+    cost = np.array([math.comb(int(x), ell) * max(int(x) - ell, 0) for x in w], dtype=float)
+    rows = np.nonzero(cost > 0)[0]
+    rows = rows[np.argsort(cost[rows], kind="stable")]
+    if len(rows) == 0:
+        return 0.0, "no work"
+    cum = np.cumsum(cost[rows])
+    total = cum[-1]
+    edges = np.searchsorted(cum, total * np.arange(1, strata) / strata)
+    bands = [b for b in np.split(rows, edges) if len(b)]
+    est, sampled, nrows = 0.0, 0.0, 0
+    for band in bands:
+        bcost = float(cost[band].sum())
+        order = [band[k] for k in _spread(len(band))]
+        picked, pc, t_used = [], 0.0, 0.0
+        rate = None
+        while order and t_used < budget_s / len(bands):
+            # next batch: double the sample (bounded by what is left)
+            take = max(1, len(picked))
+            batch = order[:take]
+            order = order[take:]
+            o2, i2 = _rows_sub(off, idx, batch)
+            t0 = time.perf_counter()
+            O.run_level(c, o2, i2, ell, tau, cfg)
+            t_used += time.perf_counter() - t0
+            picked += batch
+            pc += float(cost[batch].sum())
+            rate = pc / max(t_used, 1e-9)
+        est += bcost / rate
+        sampled += pc
+        nrows += len(picked)
+    return est, f"L{ell}: {nrows}/{len(rows)} rows, {100 * sampled / total:.2f}% of modelled cost, est {est:.1f}s"
+
+
+def _spread(n):
+    """0..n-1 in an order that covers the range evenly early (bit-reversal-like interleave)."""
+    out, seen, step = [], set(), 1
+    while len(out) < n:
+        for k in range(0, step):
+            x = min(n - 1, int((k + 0.5) * n / step))
+            if x not in seen:
+                seen.add(x)
+                out.append(x)
+        step *= 2
+    return out
+
+
+def cpu_reference_step(name: str, wl: dict, threads: int, budget_s: float):
+    """One step of the reference arm: compute_correlation + run_pc_stable of the workload (the pair
+    bench.hpp:107-113 times), with the reference's fastest strategy (Strategy::SetShared, all host
+    threads) restated by the CPU oracle.  Small configs run whole; C2 (whose level 3 alone is ~8e11
+    tests) is the correlation and level 0 run whole plus a stratified row sample of levels 1-3 on the
+    exact per-level snapshots (tests/golden/c2_snapshots.npz), extrapolated per stratum.
+    Returns (seconds for the whole config, serial CI tests, description, per-level detail)."""
+    from oracle import pyoracle as O  # test infrastructure: the reference restated on the CPU
+
+    x = _cpu_data(O, wl)
+    t0 = time.perf_counter()
+    c_ref = O.compute_correlation(x, threads=threads)  # the reference's (naive-order) correlation
+    t_corr = time.perf_counter() - t0
+    cfg = O.config(alpha=wl["alpha"], strategy=O.SET, workers=threads, set_groups=max(2, threads),
+                   max_level=wl["max_level"])
+    if name in SNAPSHOTS:
+        # the levels run on the device's correlation bits (the oracle's FMA-order restatement), so
+        # that the sampled snapshots are exactly the ones the GPU arm processes
+        c = O.compute_correlation_fma(x, threads=threads)
+        z, g = np.load(SNAPSHOTS[name]), np.load(GOLDEN[name])
+        t0 = time.perf_counter()
+        r0 = O.run_pc_stable(c, wl["m"], O.config(alpha=wl["alpha"], strategy=O.SET, workers=threads,
+                                                  max_level=0))
+        t_l0 = time.perf_counter() - t0
+        parts, detail, total = [f"corr {t_corr:.2f}s", f"L0 {t_l0:.2f}s whole"], [], t_corr + t_l0
+        budgets = {1: 0.15, 2: 0.25, 3: 0.6}
+        for ell in [int(v) for v in z["levels"]]:
+            off, idx = _snapshot_csr(z[f"adj_{ell}"], wl["p"])
+            tau = O.threshold_tau(wl["alpha"], wl["m"], ell)
+            est, desc = _level_estimate(O, c, off, idx, ell, tau, cfg, budget_s * budgets.get(ell, 0.2))
+            total += est
+            parts.append(desc)
+            detail.append({"level": ell, "est_s": est})
+        tests = int(sum(int(row[1]) for row in g["counters"]))
+        del r0
+        return total, tests, (f"{name} (reference SetShared, {threads} threads): " + "; ".join(parts) +
+                              "; levels 1-3 extrapolated from stratified row samples of the exact snapshots"), detail
+    t0 = time.perf_counter()
+    r = O.run_pc_stable(c_ref, wl["m"], cfg)
+    t_skel = time.perf_counter() - t0
+    tests = sum(l.ci_tests for l in r.levels)
+    return t_corr + t_skel, tests, (f"whole {name} (reference SetShared, {threads} threads): correlation "
+                                    f"{t_corr:.2f}s + run_pc_stable {t_skel:.2f}s, {tests:.3e} serial CI tests"), \
+        [{"level": l.level, "s": l.elapsed_s} for l in r.levels]
 
 
 def reference_arm(args, name, wl):
@@ -195,20 +269,33 @@ def reference_arm(args, name, wl):
     if rank != 0:
         return 0
     threads = os.cpu_count() or 1
-    rates, desc = [], ""
+    secs, desc, tests = [], "", 0
     for k in range(args.warmup + args.steps):
-        rate, desc = cpu_sample(name, wl, args.cpu_seconds, threads)
+        # warm-up steps are the same work (page cache, thread pools); only the last K are reported
+        s, tests, desc, _ = cpu_reference_step(name, wl, threads, args.cpu_seconds if k >= args.warmup else
+                                               args.cpu_seconds / 4)
         if k >= args.warmup:
-            rates.append(rate)
-    value = statistics.mean(rates)
+            secs.append(s)
+    sec = statistics.mean(secs)
+    value = tests / sec
+    secondary = []
+    if not args.no_secondary:
+        for sname in CPU_WHOLE:
+            if sname == name:
+                continue
+            swl = WORKLOADS[sname]
+            ss, st, sd, _ = cpu_reference_step(sname, swl, threads, args.cpu_seconds)
+            secondary.append({"workload": describe(sname, swl), "ms_per_step": ss * 1e3, "value": st / ss,
+                              "unit": "tests/s", "serial_ci_tests": st, "sample": sd})
     line = {
         "metric": "CI tests/sec (serial-equivalent)", "value": value, "unit": "tests/s", "n_gpus": args.gpus,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": None, "higher_is_better": True,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": sec * 1e3, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "impl": "reference",
         "data": "synthetic (reference generator random_dag + sample_linear_gaussian)",
-        "config": {"workload": describe(name, wl), "variant": "reference SetShared (CPU)"},
+        "config": {"workload": describe(name, wl)},
         "cpu_baseline": {"value": value, "unit": "tests/s", "cores": threads, "kind": "port", "sample": desc},
         "e2e": {"value": value, "unit": "tests/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "secondary": secondary,
     }
     print(json.dumps(line), flush=True)
     return 0
@@ -372,8 +459,11 @@ def main():
                "s_per_step": statistics.mean(et), "removed_pairs": sep_n,
                "timing": "host wall time per step, max over ranks (every rank holds X and the result)"}
 
-    # full (uncapped) runs of the other single-GPU BASELINE shapes, same device timing
+    # full (uncapped) runs of the other single-GPU BASELINE shapes, same device timing, each with its
+    # end-to-end time (host data in, result out) and, where the reference finishes the whole config on
+    # the host, the reference arm's whole-config time beside it
     secondary = []
+    threads = os.cpu_count() or 1
     if world == 1 and not args.no_secondary:
         for sname in ("C3", "C4", "C5"):
             if sname == name:
@@ -397,17 +487,43 @@ def main():
                         st.append(e0.elapsed_time(e1))
             sms = statistics.mean(st)
             stests = sum(l.ci_tests for l in sr.levels)
-            secondary.append({"workload": describe(sname, swl), "skeleton_wall_s": sms * 1e-3,
-                              "value": stests / (sms * 1e-3), "unit": "tests/s", "serial_ci_tests": stests,
-                              "levels_run": sr.levels_run(), "stop_reason": sr.stop_reason.value,
-                              "edges_left": sr.skeleton.edge_count(), "steps": args.steps, "warmup": 2})
+            ent = {"workload": describe(sname, swl), "ms_per_step": sms, "skeleton_wall_s": sms * 1e-3,
+                   "value": stests / (sms * 1e-3), "unit": "tests/s", "serial_ci_tests": stests,
+                   "levels_run": sr.levels_run(), "stop_reason": sr.stop_reason.value,
+                   "edges_left": sr.skeleton.edge_count(), "steps": args.steps, "warmup": 2}
+            if not args.no_e2e:
+                sx_pin = torch.from_numpy(np.ascontiguousarray(sx.T)).pin_memory().numpy().T
+                cfg_e = pcs.SkeletonConfig(alpha=swl["alpha"], max_level=swl["max_level"], strategy=cfg.strategy,
+                                           device=dev)
+                et = []
+                for _ in range(max(1, args.steps)):
+                    flush.zero_()
+                    torch.cuda.synchronize()
+                    t0 = time.perf_counter()
+                    r2 = pcs.run_pc_stable_data(sx_pin, cfg_e)
+                    r2.sepsets.stored_count()
+                    et.append(time.perf_counter() - t0)
+                rec = sum((3 + l.level) * l.edges_removed for l in r2.levels if l.level >= 1)
+                ent["e2e"] = {"value": stests / statistics.mean(et), "unit": "tests/s",
+                              "h2d_bytes_per_step": 8 * swl["m"] * swl["p"],
+                              "d2h_bytes_per_step": 4 * swl["p"] * ((swl["p"] + 31) // 32) + 4 * rec + 72 * len(r2.levels),
+                              "s_per_step": statistics.mean(et)}
+            if sname in CPU_WHOLE and not args.no_cpu_baseline:
+                try:
+                    cs, ctests, cdesc, _ = cpu_reference_step(sname, swl, threads, args.cpu_seconds)
+                    ent["cpu_baseline"] = {"value": ctests / cs, "unit": "tests/s", "cores": threads, "kind": "port",
+                                           "ms_per_step": cs * 1e3, "sample": cdesc}
+                except Exception as exc:
+                    ent["cpu_baseline"] = {"value": None, "sample": f"failed: {exc}"}
+            secondary.append(ent)
+            del sx_dev
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        threads = os.cpu_count() or 1
         try:
-            rate, desc = cpu_sample(name, wl, args.cpu_seconds, threads)
-            cpu = {"value": rate, "unit": "tests/s", "cores": threads, "kind": "port", "sample": desc}
+            cs, ctests, desc, _ = cpu_reference_step(name, wl, threads, args.cpu_seconds)
+            cpu = {"value": ctests / cs, "unit": "tests/s", "cores": threads, "kind": "port", "ms_per_step": cs * 1e3,
+                   "sample": desc}
         except Exception as exc:  # the oracle is a checker; never let it sink the GPU line
             cpu = {"value": None, "unit": "tests/s", "cores": threads, "kind": "port", "sample": f"failed: {exc}"}
 
@@ -417,8 +533,10 @@ def main():
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": f"synthetic (reference generator random_dag + sample_linear_gaussian, seeds {seed}/{seed + 1})",
-            "config": {
-                "workload": describe(name, wl), "variant": "cuPC-S" if args.variant == "set" else "cuPC-E",
+            "config": {"workload": describe(name, wl),
+                       "l2": "flushed between timed steps (256 MiB write outside the events)"},
+            "detail": {
+                "variant": "cuPC-S" if args.variant == "set" else "cuPC-E",
                 "skeleton_wall_s": ms_per_step * 1e-3, "serial_ci_tests": serial_tests,
                 "levels_run": res.levels_run(), "stop_reason": res.stop_reason.value,
                 "edges_left": res.skeleton.edge_count(),
@@ -426,7 +544,6 @@ def main():
                                "device_pinv": l.device_pseudo_inverses,
                                "device_evaluated_tests": l.device_exact_tests, "removed": l.edges_removed,
                                "kernel_ms": round(l.kernel_ms, 3)} for l in res.levels],
-                "l2": "flushed between timed steps (256 MiB write outside the events)",
                 "timing": "CUDA events on the library's stream per step, max over ranks",
                 "multi_gpu": (None if world == 1 else
                               {"ranks": world, "backend": backend, "devices": torch.cuda.device_count(),

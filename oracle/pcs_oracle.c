@@ -351,6 +351,113 @@ int orc_compute_correlation(const double* x, int m, int p, double* c, int* zero_
     return orc_correlation_normalize(c, p); /* CorrelationMatrix ctor (:155) */
 }
 
+/* ---- compute_correlation in the device's pinned order (FMA Gram) --------------------------
+ * stats.hpp:132-156 leaves the Gram's summation order to Eigen (unpinned by the reference's
+ * tests, which are all tolerance-based).  The device fixes it, and this restates it exactly:
+ *   mean_j : 256 strided partial sums (lane t adds rows t, t+256, ... in order, from +0.0), then a
+ *            halving tree (lane t += lane t+d, d = 128 .. 1); mean = sum / m        (:135)
+ *   xc     : x - mean                                                              (:136)
+ *   G(i,j) : i <= j, g = +0.0; for r = 0 .. m-1: g = fma(xc_i[r], xc_j[r], g); then, if the
+ *            device pads the k extent (m not a multiple of kpad), g = g + 0.0     (:137)
+ *            (the FP64 tensor-core MMA is a correctly rounded FMA chain over k: measured,
+ *            tools/micro/dmma_semantics.cu, 12.8M/12.8M outputs)
+ *   sd, c  : as compute_correlation below (:139-154)
+ * G rows are computed lane-parallel over j (independent FMA chains; bit-identical to scalar). */
+typedef struct {
+    const double* xc;   /* p x m, variable-major */
+    const double* xt;   /* m x p, sample-major (xt[r*p + j]) */
+    int m, p, pad;
+    double* gram;
+    atomic_int next;
+} fcorr_job;
+
+__attribute__((target_clones("avx512f", "fma", "default")))
+static void fcorr_row(const fcorr_job* J, int i) {
+    const int m = J->m, p = J->p;
+    const double* a = J->xc + (size_t)i * m;
+    double acc[64];
+    for (int j0 = i; j0 < p; j0 += 64) {
+        const int nj = p - j0 < 64 ? p - j0 : 64;
+        for (int jj = 0; jj < 64; ++jj) acc[jj] = 0.0;
+        for (int r = 0; r < m; ++r) {
+            const double ar = a[r];
+            const double* b = J->xt + (size_t)r * p + j0;
+            if (nj == 64) {
+                for (int jj = 0; jj < 64; ++jj) acc[jj] = __builtin_fma(ar, b[jj], acc[jj]);
+            } else {
+                for (int jj = 0; jj < nj; ++jj) acc[jj] = __builtin_fma(ar, b[jj], acc[jj]);
+            }
+        }
+        for (int jj = 0; jj < nj; ++jj) J->gram[(size_t)i * p + j0 + jj] = J->pad ? acc[jj] + 0.0 : acc[jj];
+    }
+}
+static void* fcorr_worker(void* arg) {
+    fcorr_job* J = (fcorr_job*)arg;
+    for (;;) {
+        const int i = atomic_fetch_add(&J->next, 1);
+        if (i >= J->p) break;
+        fcorr_row(J, i);
+    }
+    return NULL;
+}
+
+int orc_compute_correlation_fma(const double* x, int m, int p, int kpad, double* c, int* zero_col, int threads) {
+    if (m < 4 || p < 2) { set_err("DataMatrix: need m >= 4 samples and n >= 2 variables"); return ORC_EINVAL; }
+    for (size_t k = 0; k < (size_t)m * p; ++k)
+        if (!isfinite(x[k])) { set_err("DataMatrix: values must be finite"); return ORC_EINVAL; }
+    double* xc = (double*)malloc(sizeof(double) * (size_t)m * p);
+    double* xt = (double*)malloc(sizeof(double) * (size_t)m * p);
+    double* gram = (double*)malloc(sizeof(double) * (size_t)p * p);
+    if (!xc || !xt || !gram) { free(xc); free(xt); free(gram); set_err("oom"); return ORC_ENOMEM; }
+    for (int j = 0; j < p; ++j) {
+        const double* col = x + (size_t)j * m;
+        double red[256];
+        for (int t = 0; t < 256; ++t) {
+            double s = 0.0;
+            for (int r = t; r < m; r += 256) s += col[r];
+            red[t] = s;
+        }
+        for (int d = 128; d > 0; d >>= 1)
+            for (int t = 0; t < d; ++t) red[t] += red[t + d];
+        const double mean = red[0] / m;
+        for (int r = 0; r < m; ++r) {
+            const double v = col[r] - mean;
+            xc[(size_t)j * m + r] = v;
+            xt[(size_t)r * p + j] = v;
+        }
+    }
+    fcorr_job J = {xc, xt, m, p, kpad > 0 && m % kpad != 0, gram, 0};
+    if (threads < 1) threads = 1;
+    pthread_t th[256];
+    if (threads > 256) threads = 256;
+    for (int t = 1; t < threads; ++t) pthread_create(&th[t], NULL, fcorr_worker, &J);
+    fcorr_worker(&J);
+    for (int t = 1; t < threads; ++t) pthread_join(th[t], NULL);
+    free(xc); free(xt);
+    double* sd = (double*)malloc(sizeof(double) * (size_t)p);
+    for (int i = 0; i < p; ++i) {
+        const double ss = gram[(size_t)i * p + i];
+        if (!(ss > 0.0)) {
+            if (zero_col) *zero_col = i;
+            free(gram); free(sd);
+            set_err("compute_correlation: column has zero variance");
+            return ORC_EZEROVAR;
+        }
+        sd[i] = sqrt(ss);
+    }
+    for (int i = 0; i < p; ++i) {
+        c[(size_t)i * p + i] = 1.0;
+        for (int j = i + 1; j < p; ++j) {
+            double v = gram[(size_t)i * p + j] / (sd[i] * sd[j]);
+            v = v < -1.0 ? -1.0 : (v > 1.0 ? 1.0 : v);
+            c[(size_t)i * p + j] = v;
+            c[(size_t)j * p + i] = v;
+        }
+    }
+    free(gram); free(sd);
+    return orc_correlation_normalize(c, p);
+}
+
 int orc_correlation_normalize(double* c, int p) { /* core.hpp:73-95 */
     const double tol = 1e-12;
     if (p < 2) { set_err("CorrelationMatrix: need a square matrix, n >= 2"); return ORC_EINVAL; }
@@ -1137,6 +1244,457 @@ int orc_level_keys(const double* c, int p, const int32_t* offsets, const int32_t
     return level_keys_impl(c, p, offsets, indices, ell, tau, e_begin, e_end, keys, threads);
 }
 
+/* ---- fast serial-rule keys: set-shared evaluation, one pseudo-inverse per (row, set) ----
+ *
+ * Result-identical to run_level_serial (skeleton.hpp:292-307): for every row r and target
+ * position q the first set, in the order test_edge_over_sets walks (lexicographic over the
+ * positions of row r minus q, skeleton.hpp:140-160), whose CI test is independent -- or whose
+ * statistic is NaN, where the serial strategy throws (stats.hpp:112).  The sets of row r are
+ * walked ONCE in lexicographic order of full-row positions (the run_set_shared_unit order,
+ * skeleton.hpp:175-222): the sets that avoid q appear in the same relative order, so the first
+ * hit per target is the serial one.  Each test runs pcor_with_inverse's exact operation
+ * sequence (stats.hpp:292-307), lane-parallel over the row's live targets with IEEE
+ * elementwise operations only (no FMA: -ffp-contract=off; correctly rounded div/sqrt), so every
+ * statistic is bit-identical to the scalar path.  The decision z <= tau is taken on |rho|
+ * against tanh(tau) widened by 1e-9 relative; tests inside that band call decide() exactly.
+ */
+#define FAST_FIRST_NONE INT64_C(-1)
+#define FAST_FIRST_NAN INT64_C(-2)
+
+typedef struct {
+    int cap;
+    int32_t *lst, *tcol, *where;
+    double *cij, *cjs, *rho;
+    uint8_t *live, *indm, *exm;
+} fast_ws;
+
+static void fast_ws_free(fast_ws* W) {
+    free(W->lst); free(W->tcol); free(W->where); free(W->cij); free(W->cjs); free(W->rho);
+    free(W->live); free(W->indm); free(W->exm);
+    memset(W, 0, sizeof *W);
+}
+static int fast_ws_reserve(fast_ws* W, int w, int ell) {
+    if (w <= W->cap) return 0;
+    fast_ws_free(W);
+    const size_t n = (size_t)w + 16;
+    W->lst = malloc(sizeof(int32_t) * n);
+    W->tcol = malloc(sizeof(int32_t) * n);
+    W->where = malloc(sizeof(int32_t) * n);
+    W->cij = calloc(n, sizeof(double));
+    W->cjs = calloc(n * (size_t)(ell > 4 ? 4 : ell), sizeof(double));
+    W->rho = calloc(n, sizeof(double));
+    W->live = calloc(n, 1);
+    W->indm = calloc(n / 8 + 2, 1);
+    W->exm = calloc(n / 8 + 2, 1);
+    W->cap = w;
+    return (W->lst && W->tcol && W->where && W->cij && W->cjs && W->rho && W->live && W->indm && W->exm) ? 0 : -1;
+}
+
+/* Per block of 8 lanes: indm bit = live, non-degenerate and surely independent; exm bit = live,
+ * non-degenerate and inside the decision band (or NaN): decide() exactly.  Everything else is
+ * dependent (degenerate H, stats.hpp:302-305, or |rho| above the band).  n is a multiple of 8;
+ * lanes past the live targets have live = 0.  Returns nonzero if any bit is set.
+ * Portable version: the per-test body of pcor_with_inverse (stats.hpp:292-307) verbatim. */
+static int fast_lanes_c(const int L, const int n, const double* cjs, const double* cij, const uint8_t* live,
+                        const double* minv, const double* P0, const double* ciS, const double h00,
+                        const double rlo, const double rhi, uint8_t* indm, uint8_t* exm, double* rho_out) {
+    int any = 0;
+    for (int blk = 0; blk < n / 8; ++blk) {
+        unsigned im = 0, em = 0;
+        for (int l8 = 0; l8 < 8; ++l8) {
+            const int t = blk * 8 + l8;
+            if (!live[t]) continue;
+            double cj[64], P1[64];
+            for (int k = 0; k < L; ++k) cj[k] = cjs[(size_t)k * n + t];
+            for (int col = 0; col < L; ++col) {
+                double s1 = cj[0] * minv[0 * L + col];
+                for (int k = 1; k < L; ++k) s1 += cj[k] * minv[k * L + col];
+                P1[col] = s1;
+            }
+            double d11 = P1[0] * cj[0], d01 = P0[0] * cj[0], d10 = P1[0] * ciS[0];
+            for (int k = 1; k < L; ++k) {
+                d11 += P1[k] * cj[k];
+                d01 += P0[k] * cj[k];
+                d10 += P1[k] * ciS[k];
+            }
+            const double h11 = 1.0 - d11;
+            const double h01 = cij[t] - 0.5 * (d01 + d10);
+            const double denom = h00 * h11;
+            if (!(denom > 0.0)) continue;
+            const double v = h01 / sqrt(denom);
+            const double rho = v < -RHO_CLAMP ? -RHO_CLAMP : (v > RHO_CLAMP ? RHO_CLAMP : v);
+            const double a = fabs(rho);
+            rho_out[t] = rho;
+            if (a < rlo) im |= 1u << l8;
+            else if (!(a > rhi)) em |= 1u << l8;
+        }
+        indm[blk] = (uint8_t)im;
+        exm[blk] = (uint8_t)em;
+        any |= (int)(im | em);
+    }
+    return any;
+}
+
+#if defined(__x86_64__)
+#include <immintrin.h>
+/* The same operation sequence, 8 lanes per AVX-512 instruction (IEEE mul/add/sub/div/sqrt,
+ * correctly rounded, no FMA): bit-identical to fast_lanes_c. */
+static inline __attribute__((always_inline, target("avx512f"))) int fast_lanes_avx512(
+    const int L, const int n, const double* cjs, const double* cij, const uint8_t* live, const double* minv,
+    const double* P0, const double* ciS, const double h00, const double rlo, const double rhi, uint8_t* indm,
+    uint8_t* exm, double* rho_out) {
+    __m512d mv[16], p0[4], cs[4];
+    for (int q = 0; q < L * L; ++q) mv[q] = _mm512_set1_pd(minv[q]);
+    for (int k = 0; k < L; ++k) { p0[k] = _mm512_set1_pd(P0[k]); cs[k] = _mm512_set1_pd(ciS[k]); }
+    const __m512d one = _mm512_set1_pd(1.0), half = _mm512_set1_pd(0.5), zero = _mm512_setzero_pd();
+    const __m512d pcl = _mm512_set1_pd(RHO_CLAMP), ncl = _mm512_set1_pd(-RHO_CLAMP);
+    const __m512d vlo = _mm512_set1_pd(rlo), vhi = _mm512_set1_pd(rhi), vh00 = _mm512_set1_pd(h00);
+    int any = 0;
+    for (int t = 0; t < n; t += 8) {
+        const __mmask8 lm = _mm512_cmpneq_epi64_mask(
+            _mm512_cvtepu8_epi64(_mm_loadl_epi64((const __m128i*)(live + t))), _mm512_setzero_si512());
+        if (!lm) { indm[t / 8] = 0; exm[t / 8] = 0; continue; }
+        __m512d cj[4], P1[4];
+        for (int k = 0; k < L; ++k) cj[k] = _mm512_loadu_pd(cjs + (size_t)k * n + t);
+        for (int col = 0; col < L; ++col) {
+            __m512d s1 = _mm512_mul_pd(cj[0], mv[0 * L + col]);
+            for (int k = 1; k < L; ++k) s1 = _mm512_add_pd(s1, _mm512_mul_pd(cj[k], mv[k * L + col]));
+            P1[col] = s1;
+        }
+        __m512d d11 = _mm512_mul_pd(P1[0], cj[0]), d01 = _mm512_mul_pd(p0[0], cj[0]), d10 = _mm512_mul_pd(P1[0], cs[0]);
+        for (int k = 1; k < L; ++k) {
+            d11 = _mm512_add_pd(d11, _mm512_mul_pd(P1[k], cj[k]));
+            d01 = _mm512_add_pd(d01, _mm512_mul_pd(p0[k], cj[k]));
+            d10 = _mm512_add_pd(d10, _mm512_mul_pd(P1[k], cs[k]));
+        }
+        const __m512d h11 = _mm512_sub_pd(one, d11);
+        const __m512d h01 = _mm512_sub_pd(_mm512_loadu_pd(cij + t), _mm512_mul_pd(half, _mm512_add_pd(d01, d10)));
+        const __m512d denom = _mm512_mul_pd(vh00, h11);
+        const __mmask8 ok = _mm512_cmp_pd_mask(denom, zero, _CMP_GT_OQ) & lm;
+        const __m512d v = _mm512_div_pd(h01, _mm512_sqrt_pd(_mm512_mask_blend_pd(ok, one, denom)));
+        __m512d rho = _mm512_mask_blend_pd(_mm512_cmp_pd_mask(v, ncl, _CMP_LT_OQ), v, ncl);
+        rho = _mm512_mask_blend_pd(_mm512_cmp_pd_mask(rho, pcl, _CMP_GT_OQ), rho, pcl);
+        const __m512d a = _mm512_abs_pd(rho);
+        const __mmask8 im = _mm512_cmp_pd_mask(a, vlo, _CMP_LT_OQ) & ok;
+        const __mmask8 em = (__mmask8)(ok & ~im & ~_mm512_cmp_pd_mask(a, vhi, _CMP_GT_OQ));
+        _mm512_storeu_pd(rho_out + t, rho);
+        indm[t / 8] = (uint8_t)im;
+        exm[t / 8] = (uint8_t)em;
+        any |= (int)(im | em);
+    }
+    return any;
+}
+#define FAST_AVX(LL)                                                                                        \
+    static __attribute__((target("avx512f"))) int fast_lanes_avx512_##LL(                                  \
+        int n, const double* cjs, const double* cij, const uint8_t* live, const double* minv, const double* P0, \
+        const double* ciS, double h00, double rlo, double rhi, uint8_t* indm, uint8_t* exm, double* rho) {     \
+        return fast_lanes_avx512(LL, n, cjs, cij, live, minv, P0, ciS, h00, rlo, rhi, indm, exm, rho);        \
+    }
+FAST_AVX(1)
+FAST_AVX(2)
+FAST_AVX(3)
+FAST_AVX(4)
+static int g_have_avx512 = -1;
+#endif
+
+static int fast_lanes(int L, int n, const double* cjs, const double* cij, const uint8_t* live, const double* minv,
+                      const double* P0, const double* ciS, double h00, double rlo, double rhi, uint8_t* indm,
+                      uint8_t* exm, double* rho) {
+#if defined(__x86_64__)
+    if (g_have_avx512 < 0) g_have_avx512 = __builtin_cpu_supports("avx512f") ? 1 : 0;
+    if (g_have_avx512 && !getenv("ORC_NO_AVX512")) {
+        switch (L) {
+            case 1: return fast_lanes_avx512_1(n, cjs, cij, live, minv, P0, ciS, h00, rlo, rhi, indm, exm, rho);
+            case 2: return fast_lanes_avx512_2(n, cjs, cij, live, minv, P0, ciS, h00, rlo, rhi, indm, exm, rho);
+            case 3: return fast_lanes_avx512_3(n, cjs, cij, live, minv, P0, ciS, h00, rlo, rhi, indm, exm, rho);
+            case 4: return fast_lanes_avx512_4(n, cjs, cij, live, minv, P0, ciS, h00, rlo, rhi, indm, exm, rho);
+            default: break;
+        }
+    }
+#endif
+    return fast_lanes_c(L, n, cjs, cij, live, minv, P0, ciS, h00, rlo, rhi, indm, exm, rho);
+}
+
+typedef struct {
+    const double* c;
+    int p;
+    const int32_t* off;
+    const int32_t* idx;
+    int ell;
+    double tau, rlo, rhi;
+    int64_t* first;          /* per directed CSR entry: full-row rank of the first event */
+    const int32_t* order;    /* rows, widest first */
+    atomic_int next;
+    atomic_int err;
+    char msg[256];
+    pthread_mutex_t mu;
+} fast_job;
+
+static int fast_row(fast_job* J, int r, ci_ws* cw, fast_ws* W) {
+    const int ell = J->ell, p = J->p;
+    const int32_t* row = J->idx + J->off[r];
+    const int w = J->off[r + 1] - J->off[r];
+    int64_t* first = J->first + J->off[r];
+    for (int q = 0; q < w; ++q) first[q] = FAST_FIRST_NONE;
+    if (w < ell + 1) return ORC_OK; /* no target of this row has an ell-subset of the others */
+    if (fast_ws_reserve(W, w, ell)) return ORC_ENOMEM;
+    const double* cr = J->c + (size_t)r * p;
+    int n = w; /* live targets, compacted (lst: row position, tcol: vertex) */
+    for (int q = 0; q < w; ++q) {
+        W->lst[q] = q;
+        W->tcol[q] = row[q];
+        W->where[q] = q;
+        W->cij[q] = cr[row[q]];
+        W->live[q] = 1;
+    }
+    for (int t = n; t < n + 8; ++t) { W->live[t] = 0; W->cij[t] = 0.0; }
+    int alive = w;
+    int32_t* pos = cw->pos;
+    int32_t* set = cw->set;
+    for (int k = 0; k < ell; ++k) pos[k] = k;
+    double P0[64], ciS[64];
+    for (int64_t rank = 0;; ++rank) {
+        int members_alive = 0;
+        for (int k = 0; k < ell; ++k) {
+            const int li = W->where[pos[k]];
+            members_alive += li >= 0 && W->live[li];
+        }
+        if (alive - members_alive > 0) { /* some live target outside this set */
+            for (int k = 0; k < ell; ++k) set[k] = row[pos[k]];
+            fill_m2(J->c, p, set, ell, cw->m2);
+            int rc = pinv_core(cw->m2, ell, cw->m2inv, &cw->pw);
+            if (rc) return rc;
+            const double* minv = cw->m2inv;
+            for (int k = 0; k < ell; ++k) ciS[k] = cr[set[k]];
+            for (int col = 0; col < ell; ++col) { /* P0 = m1 row i times m2_inv, pcor_with_inverse order */
+                double s0 = ciS[0] * minv[0 * ell + col];
+                for (int k = 1; k < ell; ++k) s0 += ciS[k] * minv[k * ell + col];
+                P0[col] = s0;
+            }
+            double d00 = P0[0] * ciS[0];
+            for (int k = 1; k < ell; ++k) d00 += P0[k] * ciS[k];
+            const double h00 = 1.0 - d00;
+            uint8_t saved[64];
+            for (int k = 0; k < ell; ++k) { /* members are not targets of this set */
+                const int li = W->where[pos[k]];
+                saved[k] = li >= 0 ? W->live[li] : 0;
+                if (li >= 0) W->live[li] = 0;
+            }
+            const int np = (n + 7) & ~7;
+            int any;
+            if (ell <= 4) {
+                for (int k = 0; k < ell; ++k) {
+                    const double* csk = J->c + (size_t)set[k] * p; /* C symmetric: C(j, s) = C(s, j) */
+                    double* dst = W->cjs + (size_t)k * np;
+                    for (int t = 0; t < n; ++t) dst[t] = csk[W->tcol[t]];
+                    for (int t = n; t < np; ++t) dst[t] = 0.0;
+                }
+                any = fast_lanes(ell, np, W->cjs, W->cij, W->live, minv, P0, ciS, h00, J->rlo, J->rhi, W->indm,
+                                 W->exm, W->rho);
+            } else { /* deep levels: few tests, scalar pcor_with_inverse per live target */
+                any = 0;
+                for (int blk = 0; blk < np / 8; ++blk) { W->indm[blk] = 0; W->exm[blk] = 0; }
+                for (int t = 0; t < n; ++t) {
+                    if (!W->live[t]) continue;
+                    double rho;
+                    if (pcor_with_inverse(J->c, p, r, W->tcol[t], set, ell, minv, &rho)) continue;
+                    W->rho[t] = rho;
+                    W->exm[t / 8] |= (uint8_t)(1u << (t % 8));
+                    any = 1;
+                }
+            }
+            for (int k = 0; k < ell; ++k) {
+                const int li = W->where[pos[k]];
+                if (li >= 0) W->live[li] = saved[k];
+            }
+            if (any) {
+                for (int blk = 0; blk < np / 8; ++blk) {
+                    unsigned bits = (unsigned)W->indm[blk] | (unsigned)W->exm[blk];
+                    while (bits) {
+                        const int l8 = __builtin_ctz(bits);
+                        bits &= bits - 1;
+                        const int t = blk * 8 + l8;
+                        int64_t ev = rank;
+                        if ((W->exm[blk] >> l8) & 1) {
+                            int indep;
+                            double z;
+                            const int rc2 = decide(W->rho[t], J->tau, &indep, &z);
+                            if (rc2 == ORC_ENAN) ev = FAST_FIRST_NAN - rank; /* the serial run throws here */
+                            else if (rc2) return rc2;
+                            else if (!indep) continue;
+                        }
+                        first[W->lst[t]] = ev;
+                        W->live[t] = 0;
+                        --alive;
+                    }
+                }
+                if (alive == 0) break;
+                if (alive * 4 < n * 3 && n > 32) { /* re-compact the live targets */
+                    int m2 = 0;
+                    for (int t = 0; t < n; ++t) {
+                        if (!W->live[t]) { W->where[W->lst[t]] = -1; continue; }
+                        W->lst[m2] = W->lst[t];
+                        W->tcol[m2] = W->tcol[t];
+                        W->cij[m2] = W->cij[t];
+                        W->live[m2] = 1;
+                        W->where[W->lst[m2]] = m2;
+                        ++m2;
+                    }
+                    for (int t = m2; t < n + 8; ++t) { W->live[t] = 0; W->cij[t] = 0.0; }
+                    n = m2;
+                }
+            }
+        }
+        if (!orc_next_combination(pos, ell, w)) break;
+    }
+    return ORC_OK;
+}
+
+static void* fast_worker(void* arg) {
+    fast_job* J = (fast_job*)arg;
+    ci_ws cw = {0};
+    fast_ws W = {0};
+    if (ci_reserve(&cw, J->ell)) { atomic_store(&J->err, ORC_ENOMEM); ci_free(&cw); return NULL; }
+    for (;;) {
+        if (atomic_load_explicit(&J->err, memory_order_relaxed)) break;
+        const int k = atomic_fetch_add(&J->next, 1);
+        if (k >= J->p) break;
+        int rc = fast_row(J, J->order[k], &cw, &W);
+        if (rc) {
+            pthread_mutex_lock(&J->mu);
+            if (!atomic_load(&J->err)) { strcpy(J->msg, rc == ORC_ENOMEM ? "oom" : g_err); atomic_store(&J->err, rc); }
+            pthread_mutex_unlock(&J->mu);
+            break;
+        }
+    }
+    fast_ws_free(&W);
+    ci_free(&cw);
+    return NULL;
+}
+
+/* Binomials C(n, k) for n < nmax, k <= ell (values checked against orc_binomial's overflow rule
+ * by the caller's run_level_keys; saturate otherwise). */
+typedef struct { int nmax, ell; uint64_t* v; } bin_tab;
+static uint64_t bt(const bin_tab* T, int n, int k) {
+    if (n < 0 || k < 0 || k > n) return 0;
+    return T->v[(size_t)n * (T->ell + 1) + k];
+}
+static int bin_tab_init(bin_tab* T, int nmax, int ell) {
+    T->nmax = nmax; T->ell = ell;
+    T->v = (uint64_t*)malloc(sizeof(uint64_t) * (size_t)(nmax + 1) * (ell + 1));
+    if (!T->v) return ORC_ENOMEM;
+    for (int n = 0; n <= nmax; ++n)
+        for (int k = 0; k <= ell; ++k) {
+            uint64_t b = 0;
+            if (k <= n && orc_binomial(n, k, &b)) b = UINT64_MAX;
+            T->v[(size_t)n * (ell + 1) + k] = b;
+        }
+    return ORC_OK;
+}
+
+/* unrank (comb.hpp:50-67) with a binary search per position: the number of ell-subsets of
+ * [0, width) whose c-th element precedes x (given the earlier elements) is
+ * C(width - start, ell - c) - C(width - x, ell - c). */
+static void unrank_fast(const bin_tab* T, int width, int ell, uint64_t t, int32_t* pos) {
+    int start = 0;
+    for (int c = 0; c < ell; ++c) {
+        const uint64_t all = bt(T, width - start, ell - c);
+        int lo = start, hi = width - (ell - c); /* largest x in [lo, hi] with covered(x) <= t */
+        while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if (all - bt(T, width - mid, ell - c) <= t) lo = mid; else hi = mid - 1;
+        }
+        t -= all - bt(T, width - lo, ell - c);
+        pos[c] = lo;
+        start = lo + 1;
+    }
+}
+
+/* rank of ascending positions among the ell-subsets of [0, width), lexicographic */
+static uint64_t rank_fast(const bin_tab* T, int width, int ell, const int32_t* pos) {
+    uint64_t rk = 0;
+    int start = 0;
+    for (int c = 0; c < ell; ++c) {
+        rk += bt(T, width - start, ell - c) - bt(T, width - pos[c], ell - c);
+        start = pos[c] + 1;
+    }
+    return rk;
+}
+
+/* full-row rank of row r's set -> rank among the sets of row r minus position q */
+static int64_t reduced_rank(const bin_tab* T, int w, int ell, int64_t full, int q, int32_t* pos) {
+    unrank_fast(T, w, ell, (uint64_t)full, pos);
+    for (int k = 0; k < ell; ++k) pos[k] -= pos[k] > q;
+    return (int64_t)rank_fast(T, w - 1, ell, pos);
+}
+
+static int level_keys_fast(const double* c, int p, const int32_t* off, const int32_t* idx, int ell, double tau,
+                           int64_t* keys, int threads) {
+    fast_job J;
+    memset(&J, 0, sizeof J);
+    J.c = c; J.p = p; J.off = off; J.idx = idx; J.ell = ell; J.tau = tau;
+    const long double rt = tanhl((long double)tau);
+    J.rlo = (double)(rt * (1.0L - 1e-9L));
+    J.rhi = (double)(rt * (1.0L + 1e-9L));
+    J.first = (int64_t*)malloc(sizeof(int64_t) * (size_t)(off[p] + 1));
+    int32_t* order = (int32_t*)malloc(sizeof(int32_t) * (size_t)p);
+    if (!J.first || !order) { free(J.first); free(order); return ORC_ENOMEM; }
+    /* widest rows first (counting sort on width) */
+    int maxw = 0;
+    for (int r = 0; r < p; ++r) if (off[r + 1] - off[r] > maxw) maxw = off[r + 1] - off[r];
+    int n = 0;
+    for (int wd = maxw; wd >= 0; --wd)
+        for (int r = 0; r < p; ++r) if (off[r + 1] - off[r] == wd) order[n++] = r;
+    J.order = order;
+    atomic_init(&J.next, 0);
+    atomic_init(&J.err, 0);
+    pthread_mutex_init(&J.mu, NULL);
+    if (threads < 1) threads = 1;
+    if (threads > 512) threads = 512;
+    pthread_t th[512];
+    for (int t = 1; t < threads; ++t) pthread_create(&th[t], NULL, fast_worker, &J);
+    fast_worker(&J);
+    for (int t = 1; t < threads; ++t) pthread_join(th[t], NULL);
+    pthread_mutex_destroy(&J.mu);
+    free(order);
+    int rc = atomic_load(&J.err);
+    if (rc) { set_err(J.msg); free(J.first); return rc; }
+    /* per undirected edge (a < b, CSR order): direction 0 = row a, then row b (Appendix B) */
+    int32_t pos[65];
+    bin_tab T;
+    if (bin_tab_init(&T, maxw + 1, ell)) { free(J.first); return ORC_ENOMEM; }
+    int64_t e = 0;
+    for (int a = 0; a < p && !rc; ++a) {
+        const int wa = off[a + 1] - off[a];
+        for (int qa = 0; qa < wa; ++qa) {
+            const int b = idx[off[a] + qa];
+            if (b <= a) continue;
+            int64_t key = NONE_KEY;
+            int64_t ev = J.first[off[a] + qa];
+            int dir = 0, wr = wa, q = qa;
+            if (ev == FAST_FIRST_NONE) {
+                const int wb = off[b + 1] - off[b];
+                q = bsearch_row(idx + off[b], wb, a);
+                ev = J.first[off[b] + q];
+                dir = 1;
+                wr = wb;
+            }
+            if (ev <= FAST_FIRST_NAN) { set_err("fisher_z: rho must lie in (-1, 1)"); rc = ORC_ENAN; break; }
+            if (ev >= 0) key = ((int64_t)dir << 62) | reduced_rank(&T, wr, ell, ev, q, pos);
+            keys[e++] = key;
+        }
+    }
+    free(T.v);
+    free(J.first);
+    return rc;
+}
+
+int orc_level_keys_fast(const double* c, int p, const int32_t* offsets, const int32_t* indices, int ell, double tau,
+                        int64_t* keys, int threads) {
+    if (ell < 1) { set_err("level_keys: need ell >= 1"); return ORC_EINVAL; }
+    return level_keys_fast(c, p, offsets, indices, ell, tau, keys, threads);
+}
+
 /* a whole level in key mode: identical skeleton/sepsets/counters to Serial */
 static int run_level_keys(level_ctx* X, orc_level_stats* st) {
     const snapshot_t* S = X->snap;
@@ -1155,10 +1713,14 @@ static int run_level_keys(level_ctx* X, orc_level_stats* st) {
     }
     int64_t* keys = (int64_t*)malloc(sizeof(int64_t) * (size_t)(ne + 1));
     if (!keys) return ORC_ENOMEM;
-    int rc = level_keys_impl(X->c, p, S->off, S->idx, ell, X->tau, 0, ne, keys, X->cfg->worker_count);
+    int rc = X->cfg->strategy == ORC_FAST
+                 ? level_keys_fast(X->c, p, S->off, S->idx, ell, X->tau, keys, X->cfg->worker_count)
+                 : level_keys_impl(X->c, p, S->off, S->idx, ell, X->tau, 0, ne, keys, X->cfg->worker_count);
     if (rc) { free(keys); return rc; }
     uint64_t tests = 0, removed = 0;
     int64_t e = 0;
+    bin_tab T;
+    if (bin_tab_init(&T, S->max_width + 1, ell)) { free(keys); return ORC_ENOMEM; }
     int32_t* set = (int32_t*)malloc(sizeof(int32_t) * (size_t)(ell + 1));
     int32_t* pos = (int32_t*)malloc(sizeof(int32_t) * (size_t)(ell + 1));
     for (int a = 0; a < p; ++a) {
@@ -1167,9 +1729,8 @@ static int run_level_keys(level_ctx* X, orc_level_stats* st) {
             const int b = S->idx[q];
             if (b <= a) continue;
             const int wb = S->off[b + 1] - S->off[b];
-            uint64_t t0 = 0, t1 = 0;
-            if (wa >= ell + 1) orc_binomial(wa - 1, ell, &t0);
-            if (wb >= ell + 1) orc_binomial(wb - 1, ell, &t1);
+            const uint64_t t0 = wa >= ell + 1 ? bt(&T, wa - 1, ell) : 0;
+            const uint64_t t1 = wb >= ell + 1 ? bt(&T, wb - 1, ell) : 0;
             const int64_t key = keys[e++];
             if (key == NONE_KEY) { tests += t0 + t1; continue; }
             const int dir = (int)(key >> 62);
@@ -1179,14 +1740,14 @@ static int run_level_keys(level_ctx* X, orc_level_stats* st) {
             const int32_t* row = S->idx + S->off[r];
             const int wr = S->off[r + 1] - S->off[r];
             const int qq = dir == 0 ? q - S->off[a] : bsearch_row(row, wr, a);
-            orc_unrank_positions_excluding(wr - 1, ell, rk, qq, pos);
-            for (int k = 0; k < ell; ++k) set[k] = row[pos[k]];
+            unrank_fast(&T, wr - 1, ell, rk, pos); /* comb.hpp:87-94 */
+            for (int k = 0; k < ell; ++k) set[k] = row[pos[k] >= qq ? pos[k] + 1 : pos[k]];
             clear_edge(X->R, a, b);
             sep_store(X->R, a, b, set, ell);
             ++removed;
         }
     }
-    free(set); free(pos); free(keys);
+    free(set); free(pos); free(keys); free(T.v);
     st->ci_tests = tests;
     st->pseudo_inverses = tests;
     st->edges_removed = removed;
@@ -1272,7 +1833,7 @@ static int validate_cfg(const orc_config* cfg) { /* core.hpp:370-383 */
     if (cfg->set_groups < 1) { set_err("SkeletonConfig: set_groups must be >= 1"); return ORC_EINVAL; }
     if (cfg->unit_width < 1) { set_err("SkeletonConfig: unit_width must be >= 1"); return ORC_EINVAL; }
     if (cfg->worker_count < 1) { set_err("SkeletonConfig: worker_count must be >= 1"); return ORC_EINVAL; }
-    if (cfg->strategy < ORC_SERIAL || cfg->strategy > ORC_KEYS) { set_err("SkeletonConfig: bad strategy"); return ORC_EINVAL; }
+    if (cfg->strategy < ORC_SERIAL || cfg->strategy > ORC_FAST) { set_err("SkeletonConfig: bad strategy"); return ORC_EINVAL; }
     return ORC_OK;
 }
 

@@ -35,7 +35,10 @@ enum {
     ORC_ENOMEM = 6
 };
 
-enum { ORC_SERIAL = 0, ORC_EDGE = 1, ORC_SET = 2, ORC_KEYS = 3 };
+/* ORC_KEYS: serial-rule keys, one pseudo-inverse per test (test_edge_over_sets order).
+ * ORC_FAST: the same keys by set-shared evaluation (one pseudo-inverse per (row, set),
+ *           lane-parallel over targets); result-identical to ORC_SERIAL. */
+enum { ORC_SERIAL = 0, ORC_EDGE = 1, ORC_SET = 2, ORC_KEYS = 3, ORC_FAST = 4 };
 enum { ORC_STOP_MAX_DEGREE = 0, ORC_STOP_LEVEL_CAP = 1, ORC_STOP_SAMPLE_SIZE = 2 };
 
 const char* orc_last_error(void);
@@ -71,6 +74,9 @@ int orc_fisher_z(double rho, double* out);
 int orc_threshold_tau(double alpha, int m, int ell, double* out);
 /* x column-major m x p; c_out row-major p x p; *zero_col set on ORC_EZEROVAR */
 int orc_compute_correlation(const double* x, int m, int p, double* c_out, int* zero_col, int threads);
+/* the same in the device's pinned order: tree column means, FMA-chain Gram over k, k extent padded
+ * to a multiple of kpad (0: none) -- see pcs_oracle.c */
+int orc_compute_correlation_fma(const double* x, int m, int p, int kpad, double* c, int* zero_col, int threads);
 /* CorrelationMatrix constructor: validate + symmetrise + clamp in place (core.hpp:73-95) */
 int orc_correlation_normalize(double* c, int p);
 /* a, out row-major n x n */
@@ -124,6 +130,10 @@ void orc_result_free(orc_result* r);
  */
 int orc_level_keys(const double* c, int p, const int32_t* offsets, const int32_t* indices, int ell,
                    double tau, int64_t e_begin, int64_t e_end, int64_t* keys, int threads);
+
+/* the same keys as orc_level_keys over ALL edges of the snapshot, by set-shared evaluation */
+int orc_level_keys_fast(const double* c, int p, const int32_t* offsets, const int32_t* indices, int ell,
+                        double tau, int64_t* keys, int threads);
 
 /* one level on a given snapshot, rows [row_begin, row_end) only (bounded CPU sample) */
 int orc_run_level(const double* c, int p, const int32_t* offsets, const int32_t* indices, int ell, double tau,

@@ -17,7 +17,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libpcs_oracle.so")
 
 OK, EINVAL, EZEROVAR, EOVERFLOW, ENAN, ELEVEL, ENOMEM = range(7)
-SERIAL, EDGE, SET, KEYS = range(4)
+SERIAL, EDGE, SET, KEYS, FAST = range(5)
 STOP_NAMES = {0: "max-degree", 1: "level-cap", 2: "sample-size"}
 NONE_KEY = (1 << 63) - 1
 
@@ -79,6 +79,7 @@ def lib():
         L.orc_fisher_z.argtypes = [ct.c_double, dp]
         L.orc_threshold_tau.argtypes = [ct.c_double, ct.c_int, ct.c_int, dp]
         L.orc_compute_correlation.argtypes = [dp, ct.c_int, ct.c_int, dp, ct.POINTER(ct.c_int), ct.c_int]
+        L.orc_compute_correlation_fma.argtypes = [dp, ct.c_int, ct.c_int, ct.c_int, dp, ct.POINTER(ct.c_int), ct.c_int]
         L.orc_correlation_normalize.argtypes = [dp, ct.c_int]
         L.orc_pseudo_inverse.argtypes = [dp, ct.c_int, dp]
         L.orc_partial_correlation.argtypes = [dp, ct.c_int, ct.c_int, ct.c_int, ip, ct.c_int, dp, ct.POINTER(ct.c_int)]
@@ -99,6 +100,8 @@ def lib():
         L.orc_result_free.argtypes = [ct.c_void_p]
         L.orc_level_keys.argtypes = [dp, ct.c_int, ip, ip, ct.c_int, ct.c_double, ct.c_int64, ct.c_int64,
                                      ct.POINTER(ct.c_int64), ct.c_int]
+        L.orc_level_keys_fast.argtypes = [dp, ct.c_int, ip, ip, ct.c_int, ct.c_double, ct.POINTER(ct.c_int64),
+                                          ct.c_int]
         L.orc_orient.argtypes = [ct.c_int, ct.POINTER(ct.c_uint8), ip, ct.POINTER(ct.c_int64), ip, ct.c_int, ip,
                                  ct.c_int64, ip, ct.POINTER(ct.c_int64), ip, ct.POINTER(ct.c_int64)]
         _lib = L
@@ -168,6 +171,24 @@ def compute_correlation(x_colmajor: np.ndarray, threads: int = 1) -> np.ndarray:
     c = np.empty((p, p), np.float64)
     zc = ct.c_int(-1)
     rc = lib().orc_compute_correlation(_dp(x), m, p, _dp(c), ct.byref(zc), threads)
+    if rc == EZEROVAR:
+        e = OracleError(rc, lib().orc_last_error().decode())
+        e.column = zc.value
+        raise e
+    _check(rc)
+    return c
+
+
+DEVICE_KPAD = 32  # the device Gram's k-chunk (csrc/corr.cu kGK)
+
+
+def compute_correlation_fma(x_colmajor: np.ndarray, threads: int = 1, kpad: int = DEVICE_KPAD) -> np.ndarray:
+    """compute_correlation in the device's pinned order (tree means, FMA-chain Gram); x as above."""
+    x = np.ascontiguousarray(x_colmajor, np.float64)
+    p, m = x.shape
+    c = np.empty((p, p), np.float64)
+    zc = ct.c_int(-1)
+    rc = lib().orc_compute_correlation_fma(_dp(x), m, p, kpad, _dp(c), ct.byref(zc), threads)
     if rc == EZEROVAR:
         e = OracleError(rc, lib().orc_last_error().decode())
         e.column = zc.value
@@ -318,6 +339,44 @@ def run_pc_stable(c: np.ndarray, m: int, cfg: OrcConfig | None = None, **kw) -> 
     return SkeletonResult(p, adj, sep, levels, reason)
 
 
+@dataclass
+class ResultArrays:
+    """A run's result without per-pair Python objects: adjacency (p, p) uint8, per unordered-pair
+    slot (core.hpp:329-335, ascending (i, j), i < j) the sepset length (-1: none) and its members."""
+    p: int
+    adjacency: np.ndarray
+    slot_len: np.ndarray      # int32[p(p-1)/2]
+    slot_off: np.ndarray      # int64[p(p-1)/2]
+    members: np.ndarray       # int32[total]
+    levels: list
+    stop_reason: str
+
+
+def run_pc_stable_arrays(c: np.ndarray, m: int, cfg: OrcConfig | None = None, **kw) -> ResultArrays:
+    c = np.ascontiguousarray(c, np.float64)
+    p = c.shape[0]
+    cfg = cfg or config(**kw)
+    h = ct.c_void_p()
+    _check(lib().orc_run_pc_stable(_dp(c), p, m, ct.byref(cfg), ct.byref(h)))
+    try:
+        lv = (OrcLevel * 128)()
+        n = lib().orc_result_levels(h, lv, 128)
+        levels = [LevelStats(lv[k].level, lv[k].ci_tests, lv[k].pseudo_inverses, lv[k].edges_removed,
+                             lv[k].elapsed_s) for k in range(n)]
+        adj = np.empty((p, p), np.uint8)
+        lib().orc_result_adjacency(h, adj.ctypes.data_as(ct.POINTER(ct.c_uint8)))
+        tot = lib().orc_result_member_total(h)
+        ns = p * (p - 1) // 2
+        lvl = np.empty(ns, np.int32)
+        off = np.empty(ns, np.int64)
+        mem = np.empty(max(tot, 1), np.int32)
+        lib().orc_result_sepsets(h, _ip(lvl), off.ctypes.data_as(ct.POINTER(ct.c_int64)), _ip(mem))
+        reason = STOP_NAMES[lib().orc_result_stop_reason(h)]
+    finally:
+        lib().orc_result_free(h)
+    return ResultArrays(p, adj, lvl, off, mem[:tot], levels, reason)
+
+
 def level_keys(c: np.ndarray, offsets: np.ndarray, indices: np.ndarray, ell: int, tau: float,
                e_begin: int = 0, e_end: int | None = None, threads: int = 1) -> np.ndarray:
     c = np.ascontiguousarray(c, np.float64)
@@ -331,6 +390,21 @@ def level_keys(c: np.ndarray, offsets: np.ndarray, indices: np.ndarray, ell: int
     _check(lib().orc_level_keys(_dp(c), p, _ip(off), _ip(idx), ell, tau, e_begin, e_end,
                                 keys.ctypes.data_as(ct.POINTER(ct.c_int64)), threads))
     return keys[:max(e_end - e_begin, 0)]
+
+
+def level_keys_fast(c: np.ndarray, offsets: np.ndarray, indices: np.ndarray, ell: int, tau: float,
+                    threads: int = 1) -> np.ndarray:
+    """level_keys over every edge of the snapshot by set-shared evaluation (same keys)."""
+    c = np.ascontiguousarray(c, np.float64)
+    p = c.shape[0]
+    off = np.ascontiguousarray(offsets, np.int32)
+    idx = np.ascontiguousarray(indices if len(indices) else np.zeros(1, np.int32), np.int32)
+    rows = np.repeat(np.arange(p, dtype=np.int64), np.diff(off.astype(np.int64)))
+    ne = int((idx[:len(rows)] > rows).sum())
+    keys = np.full(max(ne, 1), NONE_KEY, np.int64)
+    _check(lib().orc_level_keys_fast(_dp(c), p, _ip(off), _ip(idx), ell, tau,
+                                     keys.ctypes.data_as(ct.POINTER(ct.c_int64)), threads))
+    return keys[:ne]
 
 
 def run_level(c: np.ndarray, offsets: np.ndarray, indices: np.ndarray, ell: int, tau: float,

@@ -23,6 +23,7 @@ COMMON = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xptxas", "-
           "--expt-relaxed-constexpr", "-I", CSRC, "-I", os.path.join(ROOT, "include")]
 UNITS = {
     "level.cu": ["-fmad=false"],
+    "level1t.cu": ["-fmad=false"],
     "corr.cu": [],
     "host.cu": [],
     "probe.cu": [],

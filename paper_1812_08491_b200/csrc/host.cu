@@ -580,8 +580,23 @@ pcs_status pcs_session_level_begin(pcs_session* s, int32_t* running, int32_t* el
     return PCS_OK;
 }
 
+// PCS_L1_TILE: 0 never, 1 always, unset/other: when the level-1 snapshot is dense (at least half of all
+// pairs live), where the TMA-tiled sweep (level1t.cu) tests every (i, j, k) of a 32 x 64 x 32 tile from
+// shared memory.  Sparse snapshots keep level1_kernel (a tile would mostly test absent pairs).
+static bool level1_tile(const pcs_session* s) {
+    static const int mode = [] {
+        const char* e = std::getenv("PCS_L1_TILE");
+        return e ? std::atoi(e) : -1;
+    }();
+    if (s->ell != 1 || mode == 0) return false;
+    if (mode == 1) return true;
+    const double pairs = (double)s->p * (double)(s->p - 1);
+    return (double)s->info.e_dir >= 0.5 * pairs;
+}
+
 static bool merged_level(const pcs_session* s) {
-    return s->cfg.variant == PCS_VARIANT_SET && s->ell >= 2 && s->ell <= kMaxTemplLevel && merge_passes();
+    return (s->cfg.variant == PCS_VARIANT_SET && s->ell >= 2 && s->ell <= kMaxTemplLevel && merge_passes()) ||
+           level1_tile(s);
 }
 
 pcs_status pcs_session_level_passes(pcs_session* s, int32_t* passes) {
@@ -618,7 +633,25 @@ pcs_status pcs_session_level_pass(pcs_session* s, int32_t pass) {
         }
         if (!s->dBounds && (st = realloc_dev(s, &s->dBounds, 2))) return st;
     }
-    if (s->cfg.variant == PCS_VARIANT_SET || s->ell == 1 || s->ell > kMaxTemplLevel) {
+    if (level1_tile(s)) {
+        int r0 = 0, r1 = s->p;
+        if (nsh > 1) {  // cost-weighted contiguous row range (the level1_kernel split, mapped to rows)
+            unsigned long long b[2] = {0, 0};
+            launch_row_work_sharded(A, 2, s->cfg.variant, s->dPrefix, s->dShardCost, shard, nsh, s->dBounds, s->st);
+            std::vector<unsigned long long> pre((size_t)s->p + 1);
+            CUDA_TRY(cudaMemcpyAsync(b, s->dBounds, sizeof(b), cudaMemcpyDeviceToHost, s->st));
+            CUDA_TRY(cudaMemcpyAsync(pre.data(), s->dPrefix, sizeof(unsigned long long) * pre.size(),
+                                     cudaMemcpyDeviceToHost, s->st));
+            CUDA_TRY(cudaStreamSynchronize(s->st));
+            auto row_of = [&](unsigned long long u) {  // first row whose units start at or after u
+                return (int)(std::lower_bound(pre.begin(), pre.end() - 1, u) - pre.begin());
+            };
+            r0 = shard == 0 ? 0 : row_of(b[0]);
+            r1 = shard == nsh - 1 ? s->p : row_of(b[1]);
+        }
+        if (launch_level1_tile(A, s->dAdj, s->W, r0, r1, s->st))
+            return fail(PCS_ECUDA, "level-1 tile kernel: tensor map / launch failed");
+    } else if (s->cfg.variant == PCS_VARIANT_SET || s->ell == 1 || s->ell > kMaxTemplLevel) {
         unsigned long long u0 = 0, u1 = 0;
         if (nsh > 1) {
             unsigned long long b[2] = {0, 0};

@@ -92,6 +92,8 @@ void launch_edge_bounds(const LevelArgs& A, int pass, long long E, unsigned long
                         unsigned long long* bounds, cudaStream_t s);
 void launch_level1(const LevelArgs& A, int pass, const unsigned long long* prefix, unsigned long long u_begin,
                    unsigned long long u_end, cudaStream_t s);
+// ---- level1t.cu: ell = 1, both directions, TMA-tiled (dense snapshots); rows [row_begin, row_end)
+int launch_level1_tile(const LevelArgs& A, const uint32_t* adj, int W, int row_begin, int row_end, cudaStream_t s);
 int launch_level_set(const LevelArgs& A, int pass, const unsigned long long* prefix, unsigned long long u_begin,
                      unsigned long long u_end, int num_sms, cudaStream_t s);
 int launch_level_edge(const LevelArgs& A, int pass, long long e_begin, long long e_end, int num_sms,

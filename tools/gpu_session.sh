@@ -81,6 +81,20 @@ for s in $STEPS; do
         --master-addr 127.0.0.1 --master-port 29517 bench.py --gpus 2 --steps 1 --warmup 1 --no-cpu-baseline \
         --no-secondary > $OUT/bench2.json 2> $OUT/bench2.err
       ;;
+    golden)
+      timeout 1500 python -m pytest tests/test_gpu_golden.py -x -q -s > $OUT/pytest_golden.log 2>&1; echo "pytest rc=$?" >> $OUT/pytest_golden.log
+      ;;
+    l1tile)
+      for v in 0 1; do
+        PCS_L1_TILE=$v timeout 900 python tools/explore.py C3,C5b set 1 2 >> $OUT/l1tile_$v.log 2>&1
+      done
+      PCS_L1_TILE=1 timeout 900 python tools/explore.py C5d,C5e set 1 >> $OUT/l1tile_1.log 2>&1
+      PCS_L1_TILE=0 timeout 900 python tools/explore.py C5d set 1 >> $OUT/l1tile_0.log 2>&1
+      ;;
+    ncul1t)
+      PCS_L1_TILE=1 timeout 900 ncu --set full --clock-control none --import-source on -k regex:level1_tile -c 1 -f -o $OUT/l1t \
+        python tools/explore.py C5b set 1 > $OUT/ncu_l1t.log 2>&1
+      ;;
     bench)
       timeout 900 python bench.py > $OUT/bench.json 2> $OUT/bench.err
       ;;
