@@ -62,6 +62,13 @@ def describe(name: str, wl: dict) -> str:
             f"{cap}, seed={7919 * wl['case']}{gen}")
 
 
+def bench_config(name: str, wl: dict) -> dict:
+    """The `config` of both arms' lines (identical: same workload, same metric)."""
+    return {"workload": describe(name, wl),
+            "l2": "GPU arm: L2 flushed between timed steps (256 MiB write outside the events); "
+                  "reference arm: host CPU"}
+
+
 def generate(pcs, wl: dict):
     """(m, p) data of a workload with the reference generator (datagen.hpp:42-82), or its per-column-
     rescaled variant for the scaling shapes."""
@@ -164,45 +171,79 @@ def _rows_sub(off, idx, rows):
     return off2, np.ascontiguousarray(idx[sel], np.int32)
 
 
-def _level_estimate(O, c, off, idx, ell, tau, cfg, budget_s, strata=8):
+def _level_estimate(O, c, off, idx, ell, tau, cfg, budget_s, strata=8, threads=1):
     """Whole-level CPU time of the reference's SetShared level (skeleton.hpp:325-333) estimated from a
     stratified row sample: rows sorted by modelled cost C(w, l) (w - l) (sets x targets), cut into
-    `strata` bands of equal total cost; every band gets budget_s / strata of measured work (rows taken
-    spread across the band, cheapest-first only where one row would exceed the band's budget) and its
-    measured rate (modelled cost per second) extrapolates the band.  Rows are independent units of
-    the level, so a row's time does not depend on which other rows run."""
+    `strata` bands of equal total cost, visited cheapest band first.  Each band gets an equal share of
+    the time budget: rows spread across the band are run (rows are independent units of the level) as
+    long as the rate measured so far predicts they fit; the band's measured rate (modelled cost per
+    second) extrapolates the band.  A band whose cheapest row alone would exceed its share runs a spread
+    1/K of the sets of a few of its rows instead (every K-th SetShared unit chunk, scaled by K; reported
+    as `set-sampled`)."""
     w = np.diff(off).astype(np.int64)
     cost = np.array([math.comb(int(x), ell) * max(int(x) - ell, 0) for x in w], dtype=float)
     rows = np.nonzero(cost > 0)[0]
     rows = rows[np.argsort(cost[rows], kind="stable")]
     if len(rows) == 0:
-        return 0.0, "no work"
+        return 0.0, f"L{ell}: no work"
     cum = np.cumsum(cost[rows])
     total = cum[-1]
-    edges = np.searchsorted(cum, total * np.arange(1, strata) / strata)
-    bands = [b for b in np.split(rows, edges) if len(b)]
-    est, sampled, nrows = 0.0, 0.0, 0
+    cuts = np.searchsorted(cum, total * np.arange(1, strata) / strata)
+    bands = [b for b in np.split(rows, cuts) if len(b)]
+    share = budget_s / len(bands)
+    est, sampled, nrows, rate, extrap = 0.0, 0.0, 0, None, 0
     for band in bands:
         bcost = float(cost[band].sum())
-        order = [band[k] for k in _spread(len(band))]
-        picked, pc, t_used = [], 0.0, 0.0
-        rate = None
-        while order and t_used < budget_s / len(bands):
-            # next batch: double the sample (bounded by what is left)
-            take = max(1, len(picked))
-            batch = order[:take]
-            order = order[take:]
+        if rate is not None and cost[band[0]] / rate > share:
+            # rows too heavy to run whole inside the share: run a spread 1/K of each sampled row's
+            # conditioning sets (every K-th unit chunk, orc_run_level_sampled) and scale by K
+            sel = [int(band[k]) for k in _spread(len(band))][:max(1, min(len(band), threads))]
+            K = 1
+            while float(cost[sel].sum()) / K / rate > 0.5 * share and K < 65536:
+                K *= 2
+            scfg = O.config(alpha=cfg.alpha, strategy=O.SET, workers=threads, set_groups=K * threads,
+                            max_level=None if cfg.max_level < 0 else cfg.max_level)
+            o2, i2 = _rows_sub(off, idx, sel)
+            t0 = time.perf_counter()
+            O.run_level_sampled(c, o2, i2, ell, tau, scfg, K)
+            dt = (time.perf_counter() - t0) * K
+            est += bcost / (float(cost[sel].sum()) / dt)
+            sampled += float(cost[sel].sum()) / K
+            nrows += len(sel)
+            extrap += 1
+            continue
+        order = [int(band[k]) for k in _spread(len(band))]
+        t_used, pc, picked = 0.0, 0.0, 0
+        while order and t_used < share:
+            left = share - t_used
+            batch, bc = [], 0.0
+            for r in order:
+                if rate is None and batch:
+                    break  # first measurement of the level: one row
+                if rate is not None and (bc + cost[r]) / rate > left:
+                    continue  # would not fit: look for a lighter row of the band
+                batch.append(r)
+                bc += cost[r]
+                if rate is not None and bc / rate > 0.5 * left:
+                    break
+            if not batch:
+                if picked:
+                    break
+                batch, bc = [int(band[0])], float(cost[band[0]])  # the band's cheapest row
+            taken = set(batch)
+            order = [r for r in order if r not in taken]
             o2, i2 = _rows_sub(off, idx, batch)
             t0 = time.perf_counter()
             O.run_level(c, o2, i2, ell, tau, cfg)
             t_used += time.perf_counter() - t0
-            picked += batch
-            pc += float(cost[batch].sum())
+            pc += bc
+            picked += len(batch)
             rate = pc / max(t_used, 1e-9)
-        est += bcost / rate
+        est += bcost / (pc / max(t_used, 1e-9))
         sampled += pc
-        nrows += len(picked)
-    return est, f"L{ell}: {nrows}/{len(rows)} rows, {100 * sampled / total:.2f}% of modelled cost, est {est:.1f}s"
+        nrows += picked
+    return est, (f"L{ell}: {nrows}/{len(rows)} rows in {len(bands)} cost strata, {100 * sampled / total:.2f}% of modelled "
+                 f"cost run, {extrap} strata set-sampled, est {est:.1f}s")
 
 
 def _spread(n):
@@ -238,16 +279,16 @@ def cpu_reference_step(name: str, wl: dict, threads: int, budget_s: float):
         # that the sampled snapshots are exactly the ones the GPU arm processes
         c = O.compute_correlation_fma(x, threads=threads)
         z, g = np.load(SNAPSHOTS[name]), np.load(GOLDEN[name])
-        t0 = time.perf_counter()
-        r0 = O.run_pc_stable(c, wl["m"], O.config(alpha=wl["alpha"], strategy=O.SET, workers=threads,
-                                                  max_level=0))
-        t_l0 = time.perf_counter() - t0
+        r0 = O.run_pc_stable_arrays(c, wl["m"], O.config(alpha=wl["alpha"], strategy=O.SET, workers=threads,
+                                                         max_level=0))
+        t_l0 = r0.levels[0].elapsed_s
         parts, detail, total = [f"corr {t_corr:.2f}s", f"L0 {t_l0:.2f}s whole"], [], t_corr + t_l0
         budgets = {1: 0.15, 2: 0.25, 3: 0.6}
         for ell in [int(v) for v in z["levels"]]:
             off, idx = _snapshot_csr(z[f"adj_{ell}"], wl["p"])
             tau = O.threshold_tau(wl["alpha"], wl["m"], ell)
-            est, desc = _level_estimate(O, c, off, idx, ell, tau, cfg, budget_s * budgets.get(ell, 0.2))
+            est, desc = _level_estimate(O, c, off, idx, ell, tau, cfg, budget_s * budgets.get(ell, 0.2),
+                                        threads=threads)
             total += est
             parts.append(desc)
             detail.append({"level": ell, "est_s": est})
@@ -255,12 +296,16 @@ def cpu_reference_step(name: str, wl: dict, threads: int, budget_s: float):
         del r0
         return total, tests, (f"{name} (reference SetShared, {threads} threads): " + "; ".join(parts) +
                               "; levels 1-3 extrapolated from stratified row samples of the exact snapshots"), detail
-    t0 = time.perf_counter()
-    r = O.run_pc_stable(c_ref, wl["m"], cfg)
-    t_skel = time.perf_counter() - t0
-    tests = sum(l.ci_tests for l in r.levels)
+    r = O.run_pc_stable_arrays(c_ref, wl["m"], cfg)
+    t_skel = sum(l.elapsed_s for l in r.levels)  # the levels' own timing (bench.hpp:107-113), no result export
+    # the metric's test count is Strategy::Serial's (SetShared counts its own tests differently,
+    # skeleton.hpp:188-194): the oracle's serial-rule run on the same matrix
+    rs = O.run_pc_stable_arrays(c_ref, wl["m"], alpha=wl["alpha"], max_level=wl["max_level"], strategy=O.FAST,
+                                workers=threads)
+    tests = sum(l.ci_tests for l in rs.levels)
     return t_corr + t_skel, tests, (f"whole {name} (reference SetShared, {threads} threads): correlation "
-                                    f"{t_corr:.2f}s + run_pc_stable {t_skel:.2f}s, {tests:.3e} serial CI tests"), \
+                                    f"{t_corr:.2f}s + run_pc_stable {t_skel:.2f}s (levels {len(r.levels)}), "
+                                    f"{tests:.3e} serial-equivalent CI tests"), \
         [{"level": l.level, "s": l.elapsed_s} for l in r.levels]
 
 
@@ -270,10 +315,11 @@ def reference_arm(args, name, wl):
         return 0
     threads = os.cpu_count() or 1
     secs, desc, tests = [], "", 0
+    # the whole run stays within a few minutes: timed steps share ~120 s, warm-ups are quarter steps
+    budget = min(args.cpu_seconds, 120.0 / max(1, args.steps))
     for k in range(args.warmup + args.steps):
         # warm-up steps are the same work (page cache, thread pools); only the last K are reported
-        s, tests, desc, _ = cpu_reference_step(name, wl, threads, args.cpu_seconds if k >= args.warmup else
-                                               args.cpu_seconds / 4)
+        s, tests, desc, _ = cpu_reference_step(name, wl, threads, budget if k >= args.warmup else budget / 4)
         if k >= args.warmup:
             secs.append(s)
     sec = statistics.mean(secs)
@@ -292,7 +338,7 @@ def reference_arm(args, name, wl):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": sec * 1e3, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "impl": "reference",
         "data": "synthetic (reference generator random_dag + sample_linear_gaussian)",
-        "config": {"workload": describe(name, wl)},
+        "config": bench_config(name, wl),
         "cpu_baseline": {"value": value, "unit": "tests/s", "cores": threads, "kind": "port", "sample": desc},
         "e2e": {"value": value, "unit": "tests/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "secondary": secondary,
@@ -328,7 +374,8 @@ def main():
     import torch.distributed as dist
 
     import paper_1812_08491_b200 as pcs
-    from paper_1812_08491_b200.multigpu import host_staged_allreduce_min, run_pc_stable_sharded
+    from paper_1812_08491_b200.multigpu import (correlation_sharded, host_staged_all_gather, host_staged_allreduce_min,
+                                                row_band, run_pc_stable_sharded)
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -350,7 +397,8 @@ def main():
     x_host = np.ascontiguousarray(x.T)               # row j = variable j
     x_dev = torch.from_numpy(x_host).to(f"cuda:{dev}")
     ldc = (p + 3) // 4 * 4
-    c_dev = torch.empty((p, ldc), dtype=torch.float64, device=f"cuda:{dev}")
+    band = row_band(p, rank, world)[2]
+    c_dev = torch.empty((band * world, ldc), dtype=torch.float64, device=f"cuda:{dev}")  # rows >= p: gather scratch
     stream = torch.cuda.Stream()
     cfg = pcs.SkeletonConfig(alpha=wl["alpha"], max_level=wl["max_level"], strategy=pcs.Strategy(
         "edge" if args.variant == "edge" else "set"), device=dev, stream=stream.cuda_stream)
@@ -359,7 +407,9 @@ def main():
     def step():
         if world == 1:
             return pcs.run_pc_stable_data_device(x_dev.data_ptr(), m, p, cfg)
-        pcs.correlation_device(x_dev.data_ptr(), m, p, c_dev.data_ptr(), ldc, stream.cuda_stream)
+        # each rank builds its row band of C, the bands are all-gathered (NCCL), then the sharded levels
+        correlation_sharded(x_dev.data_ptr(), m, p, c_dev, stream=stream.cuda_stream,
+                            gather=host_staged_all_gather if backend != "nccl" else None)
         return run_pc_stable_sharded(c_dev.data_ptr(), ldc, p, m, cfg, with_sepsets=False,
                                      allreduce_min=host_staged_allreduce_min() if backend != "nccl" else None)
 
@@ -445,7 +495,8 @@ def main():
             t0 = time.perf_counter()
             with torch.cuda.stream(stream):
                 x_dev.copy_(x_pin, non_blocking=True)
-                pcs.correlation_device(x_dev.data_ptr(), m, p, c_dev.data_ptr(), ldc, stream.cuda_stream)
+                correlation_sharded(x_dev.data_ptr(), m, p, c_dev, stream=stream.cuda_stream,
+                                    gather=host_staged_all_gather if backend != "nccl" else None)
                 r = run_pc_stable_sharded(c_dev.data_ptr(), ldc, p, m, cfg, with_sepsets=True,
                                           allreduce_min=host_staged_allreduce_min() if backend != "nccl" else None)
             sep_n = r.sepsets.stored_count()
@@ -533,8 +584,7 @@ def main():
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": f"synthetic (reference generator random_dag + sample_linear_gaussian, seeds {seed}/{seed + 1})",
-            "config": {"workload": describe(name, wl),
-                       "l2": "flushed between timed steps (256 MiB write outside the events)"},
+            "config": bench_config(name, wl),
             "detail": {
                 "variant": "cuPC-S" if args.variant == "set" else "cuPC-E",
                 "skeleton_wall_s": ms_per_step * 1e-3, "serial_ci_tests": serial_tests,
@@ -543,12 +593,14 @@ def main():
                 "per_level": [{"level": l.level, "ci_tests": l.ci_tests, "device_ci_tests": l.device_ci_tests,
                                "device_pinv": l.device_pseudo_inverses,
                                "device_evaluated_tests": l.device_exact_tests, "removed": l.edges_removed,
+                               "near_threshold_tests": l.device_near_threshold,
                                "kernel_ms": round(l.kernel_ms, 3)} for l in res.levels],
                 "timing": "CUDA events on the library's stream per step, max over ranks",
                 "multi_gpu": (None if world == 1 else
                               {"ranks": world, "backend": backend, "devices": torch.cuda.device_count(),
+                               "correlation": "row bands of C per rank (Gram row tiles), all-gathered",
                                "keys_merge": "MIN all-reduce of the level's keys after each pass "
-                                             "(once per level for cuPC-S levels >= 2)"}),
+                                             "(once per level for cuPC-S levels >= 2 and the tiled level 1)"}),
             },
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
             "secondary": secondary,

@@ -78,6 +78,9 @@ typedef struct {
     uint64_t device_exact_tests;      /* tests whose statistic the device evaluated (in the reference's
                                          operation order); the rest of device_ci_tests were decided
                                          without arithmetic (set with h00 == 0: degenerate) */
+    uint64_t device_near_threshold;   /* tests whose statistic fell inside the +-1e-9 band around the
+                                         threshold (or was tiny) and were decided by the exact
+                                         fisher_z comparison (stats.hpp:345-351) -- listed, not hidden */
 } pcs_level_stats;
 
 typedef struct pcs_result pcs_result;
@@ -103,6 +106,11 @@ pcs_status pcs_run_pc_stable(const double* c, int32_t p, int32_t m, const pcs_co
    enqueued on `stream` (0 = legacy default stream); synchronous */
 pcs_status pcs_correlation_device(const double* d_x, int32_t m, int32_t p, double* d_c, int64_t ldc, uint64_t stream,
                                   int32_t* zero_var_col);
+/* rows [row_begin, row_end) of the same matrix only (the other rows of d_c are not written): the
+   multi-GPU split of stats.hpp:132-156 -- each rank builds its row band, the bands are all-gathered;
+   bit-identical to the rows pcs_correlation_device writes */
+pcs_status pcs_correlation_device_rows(const double* d_x, int32_t m, int32_t p, int32_t row_begin, int32_t row_end,
+                                       double* d_c, int64_t ldc, uint64_t stream, int32_t* zero_var_col);
 /* compute_correlation + run_pc_stable from m x p column-major host data (one device pipeline) */
 pcs_status pcs_run_pc_stable_data(const double* x, int32_t m, int32_t p, const pcs_config* cfg, pcs_result** out,
                                   int32_t* zero_var_col);

@@ -339,6 +339,7 @@ struct LevelStats {
     std::uint64_t device_pseudo_inverses = 0;
     double kernel_ms = 0.0;
     std::uint64_t device_exact_tests = 0;
+    std::uint64_t device_near_threshold = 0;  // tests inside the +-1e-9 threshold band (exact comparison)
 };
 
 enum class StopReason { MaxDegreeReached, LevelCapReached, SampleSizeExhausted };
@@ -428,6 +429,7 @@ inline SkeletonResult collect(pcs_result* raw) {
         x.device_pseudo_inverses = L.device_pseudo_inverses;
         x.kernel_ms = L.kernel_ms;
         x.device_exact_tests = L.device_exact_tests;
+        x.device_near_threshold = L.device_near_threshold;
         levels.push_back(x);
     }
     StopReason reason = StopReason::MaxDegreeReached;

@@ -1024,14 +1024,18 @@ static void shuffle_units(unit_t* u, size_t n, uint64_t seed) { /* skeleton.hpp:
 }
 
 /* run_level_units (skeleton.hpp:232-256) */
+/* keep_stride > 1 (bench sampling only): run just the units whose chunk is a multiple of keep_stride */
+static int g_keep_stride = 1;
 static int run_level_units(level_ctx* X, int chunks_per_row, int strategy, orc_level_stats* st) {
     const int p = X->p;
-    const size_t n = (size_t)p * (size_t)chunks_per_row;
+    size_t n = (size_t)p * (size_t)chunks_per_row;
     unit_t* units = (unit_t*)malloc(sizeof(unit_t) * (n ? n : 1));
     if (!units) return ORC_ENOMEM;
     size_t k = 0;
     for (int i = 0; i < p; ++i)
-        for (int ch = 0; ch < chunks_per_row; ++ch) units[k++] = (unit_t){i, ch};
+        for (int ch = 0; ch < chunks_per_row; ++ch)
+            if (ch % g_keep_stride == 0) units[k++] = (unit_t){i, ch};
+    n = k;
     if (X->cfg->has_schedule_seed) shuffle_units(units, n, X->cfg->schedule_seed + (uint64_t)X->ell);
     const int workers = X->cfg->worker_count;
     units_job J;
@@ -1810,6 +1814,19 @@ int orc_run_level(const double* c, int p, const int32_t* offsets, const int32_t*
     snap_free(&S);
     orc_result_free(R);
     if (!rc) *out = st;
+    return rc;
+}
+
+/* A sample of one SetShared level (bench.py's reference arm): rows [row_begin, row_end) of the snapshot,
+ * with set_groups = G units per row of which only chunks 0, keep_stride, 2 keep_stride, ... run -- every
+ * (G)th band of 64 sets from those chunks, i.e. 1/keep_stride of each row's sets, spread over the whole
+ * rank range.  Not thread-safe against concurrent orc_run_level calls (test infrastructure). */
+int orc_run_level_sampled(const double* c, int p, const int32_t* offsets, const int32_t* indices, int ell, double tau,
+                          const orc_config* cfg, int row_begin, int row_end, int keep_stride, orc_level_stats* out) {
+    if (cfg->strategy != ORC_SET || keep_stride < 1) { set_err("run_level_sampled: SET strategy only"); return ORC_EINVAL; }
+    g_keep_stride = keep_stride;
+    const int rc = orc_run_level(c, p, offsets, indices, ell, tau, cfg, row_begin, row_end, out);
+    g_keep_stride = 1;
     return rc;
 }
 

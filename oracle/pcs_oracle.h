@@ -139,6 +139,11 @@ int orc_level_keys_fast(const double* c, int p, const int32_t* offsets, const in
 int orc_run_level(const double* c, int p, const int32_t* offsets, const int32_t* indices, int ell, double tau,
                   const orc_config* cfg, int row_begin, int row_end, orc_level_stats* out);
 
+/* the SET level on rows [row_begin, row_end) running only every keep_stride-th unit chunk (a spread
+ * 1/keep_stride of each row's sets): bench.py's reference-arm sampler of rows too heavy to run whole */
+int orc_run_level_sampled(const double* c, int p, const int32_t* offsets, const int32_t* indices, int ell, double tau,
+                          const orc_config* cfg, int row_begin, int row_end, int keep_stride, orc_level_stats* out);
+
 /* ---- orient.hpp (pcs_orient_oracle.c) ----
  * stage bit 1: find_v_structures, bit 2: apply_meek_rules (3 = orient_skeleton).  With bit 1 clear
  * the input mixed graph is directed_in + every other skeleton edge undirected.  Outputs ascending

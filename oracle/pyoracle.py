@@ -423,6 +423,22 @@ def run_level(c: np.ndarray, offsets: np.ndarray, indices: np.ndarray, ell: int,
     return LevelStats(st.level, st.ci_tests, st.pseudo_inverses, st.edges_removed, st.elapsed_s)
 
 
+def run_level_sampled(c: np.ndarray, offsets: np.ndarray, indices: np.ndarray, ell: int, tau: float,
+                      cfg: OrcConfig, keep_stride: int) -> LevelStats:
+    """run_level with only every keep_stride-th unit chunk of each row (cfg.strategy must be SET)."""
+    c = np.ascontiguousarray(c, np.float64)
+    p = c.shape[0]
+    off = np.ascontiguousarray(offsets, np.int32)
+    idx = np.ascontiguousarray(indices if len(indices) else np.zeros(1, np.int32), np.int32)
+    st = OrcLevel()
+    lib().orc_run_level_sampled.argtypes = [ct.POINTER(ct.c_double), ct.c_int, ct.POINTER(ct.c_int32),
+                                            ct.POINTER(ct.c_int32), ct.c_int, ct.c_double, ct.POINTER(OrcConfig),
+                                            ct.c_int, ct.c_int, ct.c_int, ct.POINTER(OrcLevel)]
+    _check(lib().orc_run_level_sampled(_dp(c), p, _ip(off), _ip(idx), ell, tau, ct.byref(cfg), 0, p, keep_stride,
+                                       ct.byref(st)))
+    return LevelStats(st.level, st.ci_tests, st.pseudo_inverses, st.edges_removed, st.elapsed_s)
+
+
 # ---------------------------------------------------------------- orient.hpp
 class MixedGraph:
     """orient.hpp:15-32: directed (from, to) pairs and undirected (a < b) pairs, ascending."""

@@ -88,6 +88,7 @@ class _Level(ct.Structure):
         ("level", ct.c_int32), ("pad", ct.c_int32), ("ci_tests", ct.c_uint64), ("pseudo_inverses", ct.c_uint64),
         ("edges_removed", ct.c_uint64), ("elapsed_s", ct.c_double), ("device_ci_tests", ct.c_uint64),
         ("device_pseudo_inverses", ct.c_uint64), ("kernel_ms", ct.c_double), ("device_exact_tests", ct.c_uint64),
+        ("device_near_threshold", ct.c_uint64),
     ]
 
 
@@ -134,6 +135,8 @@ def library():
     L.pcs_result_record_ints.restype = ct.c_int64
     L.pcs_result_records.argtypes = [vp, ip]
     L.pcs_correlation_device.argtypes = [vp, ct.c_int32, ct.c_int32, vp, ct.c_int64, ct.c_uint64, ip]
+    L.pcs_correlation_device_rows.argtypes = [vp, ct.c_int32, ct.c_int32, ct.c_int32, ct.c_int32, vp, ct.c_int64,
+                                              ct.c_uint64, ip]
     L.pcs_kernel_launches.restype = ct.c_ulonglong
     L.pcs_probe_fp64_tflops.argtypes = [dp]
     L.pcs_session_snapshot.argtypes = [vp, ip, ip]
@@ -234,6 +237,7 @@ class LevelStats:  # core.hpp:387-393 (+ device counters)
     device_pseudo_inverses: int = 0
     kernel_ms: float = 0.0
     device_exact_tests: int = 0
+    device_near_threshold: int = 0  # tests decided by the exact comparison inside the threshold band
 
 
 class AdjacencyMatrix:
@@ -360,7 +364,7 @@ def _collect(h, with_sepsets: bool = True) -> SkeletonResult:
     n = L.pcs_result_levels(h, lv, 256)
     levels = [LevelStats(lv[k].level, lv[k].ci_tests, lv[k].pseudo_inverses, lv[k].edges_removed, lv[k].elapsed_s,
                          lv[k].device_ci_tests, lv[k].device_pseudo_inverses, lv[k].kernel_ms,
-                         lv[k].device_exact_tests) for k in range(n)]
+                         lv[k].device_exact_tests, lv[k].device_near_threshold) for k in range(n)]
     W = (p + 31) // 32
     bits = np.empty((p, W), np.uint32)
     L.pcs_result_bitmask(h, bits.ctypes.data_as(ct.POINTER(ct.c_uint32)))
@@ -457,6 +461,17 @@ def correlation_device(x_ptr: int, m: int, p: int, c_ptr: int, ldc: int, stream:
     """compute_correlation from device-resident column-major data into a device p x ldc buffer."""
     col = ct.c_int32(-1)
     rc = library().pcs_correlation_device(ct.c_void_p(x_ptr), m, p, ct.c_void_p(c_ptr), ldc, stream, ct.byref(col))
+    if rc:
+        _raise(rc, col.value)
+
+
+def correlation_device_rows(x_ptr: int, m: int, p: int, row_begin: int, row_end: int, c_ptr: int, ldc: int,
+                            stream: int = 0):
+    """Rows [row_begin, row_end) of compute_correlation into the device p x ldc buffer (the multi-GPU
+    split: each rank builds its row band, then the bands are all-gathered; multigpu.correlation_sharded)."""
+    col = ct.c_int32(-1)
+    rc = library().pcs_correlation_device_rows(ct.c_void_p(x_ptr), m, p, row_begin, row_end, ct.c_void_p(c_ptr), ldc,
+                                               stream, ct.byref(col))
     if rc:
         _raise(rc, col.value)
 

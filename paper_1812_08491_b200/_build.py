@@ -25,9 +25,9 @@ UNITS = {
     "level.cu": ["-fmad=false"],
     "level1t.cu": ["-fmad=false"],
     "corr.cu": [],
-    "host.cu": [],
+    "host.cu": ["-Xcompiler", "-ffp-contract=off"],
     "probe.cu": [],
-    "orient.cu": [],
+    "orient.cu": ["-Xcompiler", "-ffp-contract=off"],
 }
 
 
@@ -84,7 +84,7 @@ def build(verbose: bool = False, force: bool = False) -> str:
     # the reference CLI (pcstable_main.cpp) on the device path: host C++20 over the drop-in header
     cli_src = os.path.join(PKG, "cli", "pcstable_b200.cpp")
     if force or _stale(CLI, [cli_src, LIB, os.path.join(ROOT, "include", "pcstable_b200.hpp")]):
-        cmd = ["g++", "-std=c++20", "-O2", "-Wall", "-Wextra", "-I", os.path.join(ROOT, "include"), cli_src, LIB,
+        cmd = ["g++", "-std=c++20", "-O2", "-ffp-contract=off", "-Wall", "-Wextra", "-I", os.path.join(ROOT, "include"), cli_src, LIB,
                "-Wl,-rpath,$ORIGIN", "-o", CLI]
         res = subprocess.run(cmd, capture_output=True, text=True)
         if res.returncode != 0:

@@ -52,6 +52,26 @@ void launch_normalize_corr(double* C, long long ldc, int p, int* err, cudaStream
     set_diag_kernel<<<(p + 255) / 256, 256, 0, s>>>(C, ldc, p);
 }
 
+// exact invariants the kernels rely on (a matrix this library built has them): flag = 1 otherwise
+__global__ void check_corr_kernel(const double* C, long long ldc, int p, int* flag) {
+    const long long n = (long long)p * p;
+    for (long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += (long long)gridDim.x * blockDim.x) {
+        const int i = (int)(k / p), j = (int)(k % p);
+        const double a = C[(size_t)i * ldc + j];
+        bool bad = i == j ? a != 1.0 : !(fabs(a) <= 1.0);  // NaN fails too
+        if (!bad && i < j) bad = __double_as_longlong(a) != __double_as_longlong(C[(size_t)j * ldc + i]);
+        if (bad) atomicOr(flag, 1);
+    }
+}
+
+void launch_check_corr(const double* C, long long ldc, int p, int* flag, cudaStream_t s) {
+    long long n = (long long)p * p;
+    long long blocks = (n + 255) / 256;
+    if (blocks > 148 * 16) blocks = 148 * 16;
+    ++g_kernel_launches;
+    check_corr_kernel<<<(int)blocks, 256, 0, s>>>(C, ldc, p, flag);
+}
+
 // ------------------------------------------------ correlation build
 __global__ void colmean_kernel(const double* __restrict__ X, int m, int p, double* mean, int* err) {
     const int j = blockIdx.x;
@@ -95,10 +115,13 @@ __device__ __forceinline__ void dmma_8x8x4(double (&d)[2], double a, double b) {
 }
 
 // 4 warps (2 x 2), each owning a 32 x 32 sub-tile = 4 x 4 DMMA tiles of 8 x 8.
+// bi0 / full: the row-band variant (multi-GPU correlation split) computes every tile of row tiles
+// bi0 + blockIdx.y, both triangles; G(j, i) = G(i, j) bit for bit (the FMA chain of x_i[k] x_j[k] is
+// commutative per step), so the rows of different ranks assemble into a symmetric matrix.
 __global__ void __launch_bounds__(128) gram_dmma_kernel(const double* __restrict__ Xc, int p, int ldk,
-                                                        double* __restrict__ G, long long ldg) {
-    const int bi = blockIdx.y, bj = blockIdx.x;
-    if (bi > bj) return;  // symmetric: upper tiles only
+                                                        double* __restrict__ G, long long ldg, int bi0, int full) {
+    const int bi = bi0 + blockIdx.y, bj = blockIdx.x;
+    if (!full && bi > bj) return;  // symmetric: upper tiles only
     __shared__ __align__(16) double sA[kGT * kGPad];
     __shared__ __align__(16) double sB[kGT * kGPad];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -173,6 +196,62 @@ __global__ void corr_finalize_kernel(const double* __restrict__ G, long long ldg
     }
 }
 
+// sd_j = sqrt(G(j, j)) for every column from the same FMA chain as the Gram's diagonal (k = 0 .. ldk-1,
+// from +0.0; the DMMA diagonal is that chain, tools/micro/dmma_semantics.cu), ZeroVarianceError check
+__global__ void sumsq_sd_kernel(const double* __restrict__ Xc, int p, int ldk, double* sd, int* zero_col) {
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= p) return;
+    const double* x = Xc + (size_t)j * ldk;
+    double s = 0.0;
+    for (int k = 0; k < ldk; ++k) s = fma(x[k], x[k], s);
+    if (!(s > 0.0)) atomicMin(zero_col, j);
+    sd[j] = sqrt(s);
+}
+
+// rows [r0, r1) of C from row-band Gram tiles (G holds rows (r0 / kGT) * kGT .. of the band at row 0)
+__global__ void corr_finalize_rows_kernel(const double* __restrict__ G, long long ldg, int p, int g_row0, int r0, int r1,
+                                          const double* __restrict__ sd, double* __restrict__ C, long long ldc) {
+    const long long n = (long long)(r1 - r0) * p;
+    for (long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += (long long)gridDim.x * blockDim.x) {
+        const int i = r0 + (int)(k / p), j = (int)(k % p);
+        double v;
+        if (i == j) v = 1.0;
+        else {
+            const int a = i < j ? i : j, b = i < j ? j : i;
+            v = G[(size_t)(i - g_row0) * ldg + j] / (sd[a] * sd[b]);
+            v = v < -1.0 ? -1.0 : (v > 1.0 ? 1.0 : v);
+        }
+        C[(size_t)i * ldc + j] = v;
+    }
+}
+
+// Rows [r0, r1) of the correlation matrix (the others untouched): every rank of a multi-GPU run builds
+// its row band and the bands are all-gathered (bit-identical to launch_correlation's rows).
+// Scratch: Xc (p x ldk), G (band rows x ldg), sd (p), err_flags[2].
+void launch_correlation_rows(const double* X, int m, int p, int r0, int r1, double* Xc, double* G, long long ldg,
+                             double* mean, double* C, long long ldc, int* err_flags, cudaStream_t s) {
+    const int ldk = (m + kGK - 1) / kGK * kGK;
+    ++g_kernel_launches;
+    colmean_kernel<<<p, 256, 0, s>>>(X, m, p, mean, err_flags);
+    long long n = (long long)p * ldk;
+    long long blocks = (n + 255) / 256;
+    if (blocks > 148 * 32) blocks = 148 * 32;
+    ++g_kernel_launches;
+    center_kernel<<<(int)blocks, 256, 0, s>>>(X, m, p, mean, Xc, ldk);
+    if (r1 <= r0) return;
+    const int nb = (p + kGT - 1) / kGT, bi0 = r0 / kGT, bi1 = (r1 + kGT - 1) / kGT;
+    double* sd = mean;  // mean is dead after centring
+    ++g_kernel_launches;
+    sumsq_sd_kernel<<<(p + 255) / 256, 256, 0, s>>>(Xc, p, ldk, sd, err_flags + 1);
+    ++g_kernel_launches;
+    gram_dmma_kernel<<<dim3(nb, bi1 - bi0), 128, 0, s>>>(Xc, p, ldk, G - (size_t)bi0 * kGT * ldg, ldg, bi0, 1);
+    n = (long long)(r1 - r0) * p;
+    blocks = (n + 255) / 256;
+    if (blocks > 148 * 32) blocks = 148 * 32;
+    ++g_kernel_launches;
+    corr_finalize_rows_kernel<<<(int)blocks, 256, 0, s>>>(G, ldg, p, bi0 * kGT, r0, r1, sd, C, ldc);
+}
+
 // X: m x p column-major (device).  Scratch: Xc (p x ldk), G (p x ldg), mean (p), err_flags[2] = {flags, zero_col}
 void launch_correlation(const double* X, int m, int p, double* Xc, double* G, long long ldg, double* mean, double* C,
                         long long ldc, int* err_flags, cudaStream_t s) {
@@ -186,7 +265,7 @@ void launch_correlation(const double* X, int m, int p, double* Xc, double* G, lo
     center_kernel<<<(int)blocks, 256, 0, s>>>(X, m, p, mean, Xc, ldk);
     const int nb = (p + kGT - 1) / kGT;
     ++g_kernel_launches;
-    gram_dmma_kernel<<<dim3(nb, nb), 128, 0, s>>>(Xc, p, ldk, G, ldg);
+    gram_dmma_kernel<<<dim3(nb, nb), 128, 0, s>>>(Xc, p, ldk, G, ldg, 0, 0);
     double* sd = mean;  // mean is dead after centring
     ++g_kernel_launches;
     corr_sd_kernel<<<(p + 255) / 256, 256, 0, s>>>(G, ldg, p, sd, err_flags + 1);

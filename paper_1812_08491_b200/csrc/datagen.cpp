@@ -131,27 +131,44 @@ pcs_status pcs_sample_linear_gaussian_rescaled(const double* weights, int32_t n,
         for (int r = 0; r < m; ++r)
             for (int i = 0; i < n; ++i) x[(size_t)i * m + r] = g.normal();
     }
-    unsigned nt = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+    // Scales are carried as mant * 2^exp (mant in [0.5, 1), frexp) and combined with ldexp and IEEE
+    // mul/div/sqrt only -- no exp/log, whose last bits differ between libm builds -- and the sum of
+    // squares over fixed sample chunks added in chunk order (not per thread), so the output is the same
+    // bits on every host whatever its core count.
+    constexpr int kChunks = 16;
+    std::vector<double> smant((size_t)n);
+    std::vector<long long> sexp((size_t)n);
+    unsigned nt = std::max(1u, std::min((unsigned)kChunks, std::thread::hardware_concurrency()));
     if ((long long)m * (long long)(start[n] / std::max(1, n) + 1) < 200000) nt = 1;
-    std::vector<double> coef, part(nt);
+    std::vector<double> coef, part(kChunks);
     for (int i = 0; i < n; ++i) {
         const int64_t b = start[i], e = start[i + 1];
-        double F = 0.0;  // log of the largest contributing scale (noise: scale 1)
-        for (int64_t k = b; k < e; ++k) F = std::max(F, log_scale[par[k]]);
+        double Fm = 0.5;  // largest contributing scale (noise: 1 = 0.5 * 2^1)
+        long long Fe = 1;
+        for (int64_t k = b; k < e; ++k) {
+            const int j = par[k];
+            if (sexp[j] > Fe || (sexp[j] == Fe && smant[j] > Fm)) { Fm = smant[j]; Fe = sexp[j]; }
+        }
+        auto ratio = [&](double mant, long long ex) {  // (mant * 2^ex) / (Fm * 2^Fe), in (0, 2]
+            const long long d = ex - Fe;
+            return d < -2200 ? 0.0 : std::ldexp(mant / Fm, (int)d);
+        };
         coef.resize((size_t)(e - b));
-        for (int64_t k = b; k < e; ++k) coef[(size_t)(k - b)] = pw[k] * std::exp(log_scale[par[k]] - F);
-        const double nz = std::exp(-F);
+        for (int64_t k = b; k < e; ++k) coef[(size_t)(k - b)] = pw[k] * ratio(smant[par[k]], sexp[par[k]]);
+        const double nz = ratio(0.5, 1);
         double* xi = x + (size_t)i * m;
         auto work = [&](unsigned t) {
-            const int r0 = (int)((long long)m * t / nt), r1 = (int)((long long)m * (t + 1) / nt);
-            double ss = 0.0;
-            for (int r = r0; r < r1; ++r) {
-                double v = xi[r] * nz;
-                for (int64_t k = b; k < e; ++k) v += coef[(size_t)(k - b)] * x[(size_t)par[k] * m + r];
-                xi[r] = v;
-                ss += v * v;
+            for (int c = (int)t; c < kChunks; c += (int)nt) {
+                const int r0 = (int)((long long)m * c / kChunks), r1 = (int)((long long)m * (c + 1) / kChunks);
+                double ss = 0.0;
+                for (int r = r0; r < r1; ++r) {
+                    double v = xi[r] * nz;
+                    for (int64_t k = b; k < e; ++k) v += coef[(size_t)(k - b)] * x[(size_t)par[k] * m + r];
+                    xi[r] = v;
+                    ss += v * v;
+                }
+                part[(size_t)c] = ss;
             }
-            part[t] = ss;
         };
         if (nt == 1) {
             work(0);
@@ -161,12 +178,15 @@ pcs_status pcs_sample_linear_gaussian_rescaled(const double* weights, int32_t n,
             for (auto& t : th) t.join();
         }
         double ss = 0.0;
-        for (unsigned t = 0; t < nt; ++t) ss += part[t];
+        for (int c = 0; c < kChunks; ++c) ss += part[(size_t)c];
         const double rms = std::sqrt(ss / m);
         if (!(rms > 0.0) || !std::isfinite(rms)) return PCS_EINVAL;
         const double inv = 1.0 / rms;
         for (int r = 0; r < m; ++r) xi[r] *= inv;
-        log_scale[i] = F + std::log(rms);
+        int ex = 0;
+        smant[(size_t)i] = std::frexp(Fm * rms, &ex);  // scale_i = F * rms
+        sexp[(size_t)i] = Fe + ex;
+        log_scale[i] = std::log(smant[(size_t)i]) + (double)sexp[(size_t)i] * 0.69314718055994530942;  // output only
     }
     return PCS_OK;
 }

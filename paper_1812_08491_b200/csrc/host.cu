@@ -16,6 +16,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <memory>
+#include <mutex>
 #include <new>
 #include <string>
 #include <utility>
@@ -272,26 +273,47 @@ pcs_status validate_config(const pcs_config* c) {  // core.hpp:370-383
     return PCS_OK;
 }
 
+cudaError_t dev_malloc(void** ptr, size_t bytes, cudaStream_t st);
+
 template <class T>
 pcs_status realloc_dev(pcs_session* s, T** ptr, long long n) {
     if (*ptr) cudaFreeAsync(*ptr, s->st);
     *ptr = nullptr;
-    CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(ptr), sizeof(T) * (size_t)std::max<long long>(n, 1), s->st));
+    CUDA_TRY(dev_malloc(reinterpret_cast<void**>(ptr), sizeof(T) * (size_t)std::max<long long>(n, 1), s->st));
     return PCS_OK;
 }
 
 // Device buffers come from the stream-ordered pool: frees do not synchronise the device and
 // the pool keeps its memory between calls (release threshold = unlimited), so repeated runs
 // neither pay cudaMalloc/cudaFree latency nor stall on the driver's deferred reclamation.
-void keep_pool(int device) {
-    static bool done[64] = {};
-    if (device < 0 || device >= 64 || done[device]) return;
-    cudaMemPool_t pool;
-    if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
-        unsigned long long thr = ~0ull;
-        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+// A private stream-ordered pool per device: session buffers stay cached across runs (release
+// threshold = max) without touching the device's default pool, which the host application (PyTorch,
+// ...) may use with its own release policy.
+static cudaMemPool_t lib_pool(int device) {
+    static std::mutex mu;
+    static cudaMemPool_t pools[64] = {};
+    if (device < 0 || device >= 64) return nullptr;
+    std::lock_guard<std::mutex> g(mu);
+    if (!pools[device]) {
+        cudaMemPoolProps props{};
+        props.allocType = cudaMemAllocationTypePinned;
+        props.location.type = cudaMemLocationTypeDevice;
+        props.location.id = device;
+        cudaMemPool_t pool = nullptr;
+        if (cudaMemPoolCreate(&pool, &props) == cudaSuccess) {
+            unsigned long long thr = ~0ull;
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+            pools[device] = pool;
+        }
     }
-    done[device] = true;
+    return pools[device];
+}
+
+cudaError_t dev_malloc(void** ptr, size_t bytes, cudaStream_t st) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaMemPool_t pool = lib_pool(dev);
+    return pool ? cudaMallocFromPoolAsync(ptr, bytes, pool, st) : cudaMallocAsync(ptr, bytes, st);
 }
 
 pcs_status session_alloc(pcs_session* s) {
@@ -303,19 +325,18 @@ pcs_status session_alloc(pcs_session* s) {
     } else {
         CUDA_TRY(cudaStreamCreateWithFlags(&s->st, cudaStreamNonBlocking));
     }
-    keep_pool(s->device);
     CUDA_TRY(cudaEventCreate(&s->ev_begin));
     CUDA_TRY(cudaEventCreate(&s->ev_end));
     CUDA_TRY(cudaEventCreate(&s->ev_k0));
     CUDA_TRY(cudaEventCreate(&s->ev_k1));
-    CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&s->dAdj), sizeof(uint32_t) * (size_t)p * s->W, s->st));
-    CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&s->dDeg), sizeof(int32_t) * (size_t)(p + 1), s->st));
-    CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&s->dLow), sizeof(int32_t) * (size_t)(p + 1), s->st));
-    CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&s->dOff), sizeof(int32_t) * (size_t)(p + 1), s->st));
-    CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&s->dUp), sizeof(int32_t) * (size_t)(p + 1), s->st));
-    CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&s->dInfo), sizeof(SnapInfo), s->st));
-    CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&s->dCnt), sizeof(Counters), s->st));
-    CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&s->dPrefix), sizeof(unsigned long long) * (size_t)(p + 1), s->st));
+    CUDA_TRY(dev_malloc(reinterpret_cast<void**>(&s->dAdj), sizeof(uint32_t) * (size_t)p * s->W, s->st));
+    CUDA_TRY(dev_malloc(reinterpret_cast<void**>(&s->dDeg), sizeof(int32_t) * (size_t)(p + 1), s->st));
+    CUDA_TRY(dev_malloc(reinterpret_cast<void**>(&s->dLow), sizeof(int32_t) * (size_t)(p + 1), s->st));
+    CUDA_TRY(dev_malloc(reinterpret_cast<void**>(&s->dOff), sizeof(int32_t) * (size_t)(p + 1), s->st));
+    CUDA_TRY(dev_malloc(reinterpret_cast<void**>(&s->dUp), sizeof(int32_t) * (size_t)(p + 1), s->st));
+    CUDA_TRY(dev_malloc(reinterpret_cast<void**>(&s->dInfo), sizeof(SnapInfo), s->st));
+    CUDA_TRY(dev_malloc(reinterpret_cast<void**>(&s->dCnt), sizeof(Counters), s->st));
+    CUDA_TRY(dev_malloc(reinterpret_cast<void**>(&s->dPrefix), sizeof(unsigned long long) * (size_t)(p + 1), s->st));
     return PCS_OK;
 }
 
@@ -444,12 +465,12 @@ pcs_status pcs_threshold_tau(double alpha, int32_t m, int32_t ell, double* tau) 
 
 static pcs_status session_upload_corr(pcs_session* s, const double* c) {
     s->ldc = (s->p + 3) / 4 * 4;
-    CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&s->dC), sizeof(double) * (size_t)s->p * s->ldc, s->st));
+    CUDA_TRY(dev_malloc(reinterpret_cast<void**>(&s->dC), sizeof(double) * (size_t)s->p * s->ldc, s->st));
     CUDA_TRY(cudaEventRecord(s->ev_begin, s->st));
     CUDA_TRY(cudaMemcpy2DAsync(s->dC, sizeof(double) * s->ldc, c, sizeof(double) * s->p, sizeof(double) * s->p, s->p,
                                cudaMemcpyHostToDevice, s->st));
     int* dErr = nullptr;
-    CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&dErr), sizeof(int), s->st));
+    CUDA_TRY(dev_malloc(reinterpret_cast<void**>(&dErr), sizeof(int), s->st));
     CUDA_TRY(cudaMemsetAsync(dErr, 0, sizeof(int), s->st));
     launch_normalize_corr(s->dC, s->ldc, s->p, dErr, s->st);
     int err = 0;
@@ -474,13 +495,52 @@ pcs_status pcs_session_create(const double* c, int32_t p, int32_t m, const pcs_c
 
 pcs_status pcs_session_create_device(const double* d_c, int64_t ldc, int32_t p, int32_t m, const pcs_config* cfg,
                                      pcs_session** out) {
+    if (!d_c) return fail(PCS_EINVAL, "CorrelationMatrix: null device pointer");
+    if (ldc < p) return fail(PCS_EINVAL, "CorrelationMatrix: leading dimension must be >= n");
+    if ((long long)p * ldc >= (1ll << 31)) return fail(PCS_EUNSUPPORTED, "CorrelationMatrix: n * ldc must be < 2^31");
     pcs_session* s = nullptr;
     pcs_status st = session_new(p, m, cfg, &s);
     if (st) return st;
-    s->own_c = false;
-    s->dC = const_cast<double*>(d_c);
-    s->ldc = ldc;
-    cudaEventRecord(s->ev_begin, s->st);
+    // The kernels need the CorrelationMatrix invariants exactly (core.hpp:73-95): unit diagonal, bitwise
+    // symmetry, finite entries in [-1, 1].  A caller buffer that already has them (every matrix this
+    // library builds) is used in place; anything else is copied into a session buffer and run through
+    // the constructor's validation + symmetrisation, like session_upload_corr.
+    int* dFlag = nullptr;
+    int flag = 0;
+    CUDA_TRY(dev_malloc(reinterpret_cast<void**>(&dFlag), sizeof(int), s->st));
+    CUDA_TRY(cudaMemsetAsync(dFlag, 0, sizeof(int), s->st));
+    launch_check_corr(d_c, ldc, p, dFlag, s->st);
+    CUDA_TRY(cudaMemcpyAsync(&flag, dFlag, sizeof(int), cudaMemcpyDeviceToHost, s->st));
+    cudaFreeAsync(dFlag, s->st);
+    CUDA_TRY(cudaStreamSynchronize(s->st));
+    if (!flag) {
+        s->own_c = false;
+        s->dC = const_cast<double*>(d_c);
+        s->ldc = ldc;
+        cudaEventRecord(s->ev_begin, s->st);
+        *out = s;
+        return PCS_OK;
+    }
+    s->ldc = (p + 3) / 4 * 4;
+    st = [&]() -> pcs_status {
+        CUDA_TRY(dev_malloc(reinterpret_cast<void**>(&s->dC), sizeof(double) * (size_t)p * s->ldc, s->st));
+        CUDA_TRY(cudaEventRecord(s->ev_begin, s->st));
+        CUDA_TRY(cudaMemcpy2DAsync(s->dC, sizeof(double) * s->ldc, d_c, sizeof(double) * ldc, sizeof(double) * p, p,
+                                   cudaMemcpyDeviceToDevice, s->st));
+        int* dErr = nullptr;
+        CUDA_TRY(dev_malloc(reinterpret_cast<void**>(&dErr), sizeof(int), s->st));
+        CUDA_TRY(cudaMemsetAsync(dErr, 0, sizeof(int), s->st));
+        launch_normalize_corr(s->dC, s->ldc, p, dErr, s->st);
+        int err = 0;
+        CUDA_TRY(cudaMemcpyAsync(&err, dErr, sizeof(int), cudaMemcpyDeviceToHost, s->st));
+        cudaFreeAsync(dErr, s->st);
+        CUDA_TRY(cudaStreamSynchronize(s->st));
+        if (err & 2) return fail(PCS_EINVAL, "CorrelationMatrix: diagonal must be 1");
+        if (err & 4) return fail(PCS_EINVAL, "CorrelationMatrix: matrix must be symmetric");
+        if (err & 8) return fail(PCS_EINVAL, "CorrelationMatrix: entries must lie in [-1, 1]");
+        return PCS_OK;
+    }();
+    if (st) { free_session(s); return st; }
     *out = s;
     return PCS_OK;
 }
@@ -559,7 +619,7 @@ pcs_status pcs_session_level_begin(pcs_session* s, int32_t* running, int32_t* el
         if (need > s->capRec) {  // grow the record pool, keeping earlier levels' records
             const long long cap = std::max(need, s->capRec * 3 / 2);
             int32_t* np = nullptr;
-            CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&np), sizeof(int32_t) * (size_t)cap, s->st));
+            CUDA_TRY(dev_malloc(reinterpret_cast<void**>(&np), sizeof(int32_t) * (size_t)cap, s->st));
             if (s->recUsed)
                 CUDA_TRY(cudaMemcpyAsync(np, s->dRec, sizeof(int32_t) * (size_t)s->recUsed, cudaMemcpyDeviceToDevice,
                                          s->st));
@@ -590,8 +650,10 @@ static bool level1_tile(const pcs_session* s) {
     }();
     if (s->ell != 1 || mode == 0) return false;
     if (mode == 1) return true;
+    // measured (profiles/r2s03_l1tile.log): 2.2-4.8x faster than level1_kernel at p = 5000-20000 (C beyond
+    // L2), 1.3x slower at p = 1643 (C3: L2-resident, 73% dense, most pairs separate within a few k)
     const double pairs = (double)s->p * (double)(s->p - 1);
-    return (double)s->info.e_dir >= 0.5 * pairs;
+    return s->p >= 2048 && (double)s->info.e_dir >= 0.5 * pairs;
 }
 
 static bool merged_level(const pcs_session* s) {
@@ -751,6 +813,7 @@ pcs_status pcs_session_level_end(pcs_session* s) {
         L.device_ci_tests = c.gpu_tests;
         L.device_pseudo_inverses = c.gpu_pinv;
         L.device_exact_tests = c.gpu_exact;
+        L.device_near_threshold = c.near;
         if (c.rec_count) {
             s->recUsed += (long long)c.rec_count * (3 + s->ell);
         }
@@ -846,7 +909,7 @@ pcs_status pcs_run_pc_stable_device(const double* d_c, int64_t ldc, int32_t p, i
 }
 
 static pcs_status correlation_device(cudaStream_t stream, const double* x, int m, int p, double* dC, long long ldc,
-                                     int32_t* zero_var_col, bool x_on_device = false) {
+                                     int32_t* zero_var_col, bool x_on_device = false, int r0 = -1, int r1 = -1) {
     if (m < 4) return fail(PCS_EINVAL, "DataMatrix: need at least 4 samples, got " + std::to_string(m));
     if (p < 2) return fail(PCS_EINVAL, "DataMatrix: need at least 2 variables, got " + std::to_string(p));
     const int ldk = (m + 31) / 32 * 32;
@@ -859,10 +922,11 @@ static pcs_status correlation_device(cudaStream_t stream, const double* x, int m
             if (q) cudaFreeAsync(q, stream);
     };
     auto alloc = [&](auto** ptr, size_t bytes) {
-        return cudaMallocAsync(reinterpret_cast<void**>(ptr), bytes, stream) != cudaSuccess;
+        return dev_malloc(reinterpret_cast<void**>(ptr), bytes, stream) != cudaSuccess;
     };
     if ((!x_on_device && alloc(&dX, sizeof(double) * (size_t)m * p)) || alloc(&dXc, sizeof(double) * (size_t)p * ldk) ||
-        alloc(&dG, sizeof(double) * (size_t)p * ldg) || alloc(&dMean, sizeof(double) * (size_t)p) ||
+        alloc(&dG, sizeof(double) * (size_t)(r0 >= 0 ? std::min<long long>(p, (long long)(r1 - r0) + 128) : p) * ldg) ||
+        alloc(&dMean, sizeof(double) * (size_t)p) ||
         alloc(&dErr, sizeof(int) * 2)) {
         cleanup();
         return fail(PCS_ENOMEM, "cudaMalloc failed in compute_correlation");
@@ -870,7 +934,10 @@ static pcs_status correlation_device(cudaStream_t stream, const double* x, int m
     int init[2] = {0, INT32_MAX};
     if (!x_on_device) cudaMemcpyAsync(dX, x, sizeof(double) * (size_t)m * p, cudaMemcpyHostToDevice, stream);
     cudaMemcpyAsync(dErr, init, sizeof(init), cudaMemcpyHostToDevice, stream);
-    launch_correlation(x_on_device ? x : dX, m, p, dXc, dG, ldg, dMean, dC, ldc, dErr, stream);
+    if (r0 >= 0)
+        launch_correlation_rows(x_on_device ? x : dX, m, p, r0, r1, dXc, dG, ldg, dMean, dC, ldc, dErr, stream);
+    else
+        launch_correlation(x_on_device ? x : dX, m, p, dXc, dG, ldg, dMean, dC, ldc, dErr, stream);
     int err[2];
     cudaMemcpyAsync(err, dErr, sizeof(err), cudaMemcpyDeviceToHost, stream);
     cleanup();
@@ -912,7 +979,7 @@ static pcs_status run_data(const double* x, bool on_device, int32_t m, int32_t p
     pcs_status st = session_new(p, m, cfg, &s);
     if (st) return st;
     s->ldc = (p + 3) / 4 * 4;
-    if (cudaMallocAsync(reinterpret_cast<void**>(&s->dC), sizeof(double) * (size_t)p * s->ldc, s->st) != cudaSuccess) {
+    if (dev_malloc(reinterpret_cast<void**>(&s->dC), sizeof(double) * (size_t)p * s->ldc, s->st) != cudaSuccess) {
         free_session(s);
         return fail(PCS_ENOMEM, "cudaMalloc failed");
     }
@@ -933,6 +1000,15 @@ pcs_status pcs_correlation_device(const double* d_x, int32_t m, int32_t p, doubl
     int ndev = 0;
     if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) return fail(PCS_ECUDA, "no CUDA device available");
     return correlation_device(reinterpret_cast<cudaStream_t>(stream), d_x, m, p, d_c, ldc, zero_var_col, true);
+}
+
+pcs_status pcs_correlation_device_rows(const double* d_x, int32_t m, int32_t p, int32_t row_begin, int32_t row_end,
+                                       double* d_c, int64_t ldc, uint64_t stream, int32_t* zero_var_col) {
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) return fail(PCS_ECUDA, "no CUDA device available");
+    if (row_begin < 0 || row_end > p || row_begin > row_end) return fail(PCS_EINVAL, "bad row range");
+    return correlation_device(reinterpret_cast<cudaStream_t>(stream), d_x, m, p, d_c, ldc, zero_var_col, true, row_begin,
+                              row_end);
 }
 
 pcs_status pcs_run_pc_stable_data(const double* x, int32_t m, int32_t p, const pcs_config* cfg, pcs_result** out,

@@ -33,6 +33,12 @@ unsigned long long g_kernel_launches = 0;
 // copied into every step instance and crowd the hot loop out of the instruction cache.
 __device__ __noinline__ int decide_slow(double h01, double denom, Thresholds th) { return decide_fast(h01, denom, th); }
 
+// strips kNearBit off a decision and counts the near-threshold test (rare: no contention)
+__device__ __forceinline__ int take_near(int d, Counters* cnt) {
+    if (d & kNearBit) atomicAdd(&cnt->near, 1ull);
+    return d & ~kNearBit;
+}
+
 #ifndef PCS_SET_NT_SMALL
 #define PCS_SET_NT_SMALL 3  // targets per lane per set for L <= 3 (tuning knob, results identical)
 #endif
@@ -135,7 +141,7 @@ __global__ void level0_kernel(const double* __restrict__ C, long long ldc, int p
         const int j = w * 32 + lane;
         bool live = false;
         if (j < p && j != i) {
-            const int d = decide0(__ldg(C + (size_t)i * ldc + j), th);
+            const int d = take_near(decide0(__ldg(C + (size_t)i * ldc + j), th), cnt);
             nan |= d == kNanError;
             live = d == kDependent;
             if (j > i && d == kIndependent) ++removed;
@@ -525,7 +531,7 @@ __global__ void __launch_bounds__(kL1Threads) level1_kernel(LevelArgs A, int pas
 #pragma unroll
                     for (int u = 0; u < kL1Unroll; ++u) {
                         if (!((cand >> u) & 1u)) continue;
-                        const int d = decide_slow(h01[u], den[u], A.th);
+                        const int d = take_near(decide_slow(h01[u], den[u], A.th), A.cnt);
                         if (d != kDependent) {
                             active = false;
                             if (d == kNanError) nan = 1;
@@ -832,7 +838,7 @@ __device__ __forceinline__ void set_sweep_tsp(const LevelArgs& A, SetWarpSmem<L>
                     for (int k = 0; k < SP; ++k) {
                         if (((cand >> (t * SP + k)) & 1u) && g[k] < lim[t]) {
                             const double h01 = 0.5 * cij2[t] - 0.5 * s01[t][k];
-                            const int d = decide_slow(h01, den[t][k], A.th);
+                            const int d = take_near(decide_slow(h01, den[t][k], A.th), A.cnt);
                             if (d != kDependent) {
                                 const int kk = t * 32 + lane;
                                 const bool dir1 = q[t] < lc;
@@ -1059,7 +1065,7 @@ __device__ __forceinline__ void set_sweep(const LevelArgs& A, SetWarpSmem<L>& S,
                 for (int t = 0; t < NT; ++t) {
                     if ((cand >> t) & 1u) {
                         const double h01 = 0.5 * cij2[t] - 0.5 * s01[t];  // == c_ij - 0.5 * (d01 + d10)
-                        const int d = decide_slow(h01, den[t], A.th);
+                        const int d = take_near(decide_slow(h01, den[t], A.th), A.cnt);
                         if (d != kDependent) {
                             if (d == kNanError) nan = 1;
                             else {
@@ -1298,11 +1304,9 @@ template <int L>
 static int launch_set_L(const LevelArgs& A, int pass, const unsigned long long* prefix, unsigned long long u_begin,
                         unsigned long long u_end, int num_sms, cudaStream_t s) {
     const size_t smem = sizeof(SetWarpSmem<L>) * kSetWarps;
-    static bool attr_set = false;
-    if (!attr_set) {
-        cudaFuncSetAttribute(level_set_kernel<L>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        attr_set = true;
-    }
+    // per launch (the attribute is per device; one launch per level pass, so the call is negligible)
+    if (cudaFuncSetAttribute(level_set_kernel<L>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+        return -2;
     int per_sm = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, level_set_kernel<L>, kSetWarps * 32, smem);
     if (per_sm < 1) per_sm = 1;
@@ -1374,7 +1378,7 @@ __global__ void __launch_bounds__(128) level_edge_kernel(LevelArgs A, int pass, 
                 pinv<L>(m2, minv);
                 p0_terms<L>(minv, ciS, p0, h00);
                 h_terms<L>(minv, ciS, p0, h00, cjS, cij, h01, denom);
-                d = decide_fast(h01, denom, A.th);
+                d = take_near(decide_fast(h01, denom, A.th), A.cnt);
                 ++tests;
                 ++pinvs;
             }
@@ -1515,7 +1519,7 @@ __global__ void __launch_bounds__(128) level_set_rt_kernel(LevelArgs A, int pass
                 for (int a = 0; a < n; ++a) cjS[a] = __ldg(C + (size_t)Spos[n + a] * ldc + j);
                 double h01, denom;
                 h_terms_rt(Sminv, SciS, SciS + n, SciS[2 * n], cjS, n, cij, P1, h01, denom);
-                const int d = decide_fast(h01, denom, A.th);
+                const int d = take_near(decide_fast(h01, denom, A.th), A.cnt);
                 if (d != kDependent) {
                     live = false;
                     if (d == kNanError) nan = 1;

@@ -12,17 +12,21 @@
 // i < j, dir 1 when i > j; keys are MIN-merged) and walks k in chunks of 32:
 //   * TMA (cp.async.bulk.tensor.2d) brings C(k0:k0+32, j0:j0+64) and C(i0:i0+32, k0:k0+32) into
 //     shared memory, one chunk ahead of the compute (mbarrier transaction counts);
-//   * a transform pass builds (c_jk, 1 - c_jk^2) per (k, j) and (c_ik, RN(hi2' (1 - c_ik^2))) per (i, k),
-//     each reused by all 32 rows / 64 targets of the tile;
+//   * a transform pass builds (c_jk, h11 = 1 - c_jk^2) per (k, j) and (c_ik, g_ik = RN(hi2' (1 - c_ik^2)))
+//     per (i, k), each reused by all 32 rows / 64 targets of the tile; a factor that is exactly 0 is
+//     stored as NaN;
 //   * every thread owns 8 rows x 2 targets and per k evaluates, in the reference's rounding,
-//     h01 = RN(c_ij - RN(c_ik c_jk)) and the certified-dependent filter  RN(h01^2) >= RN(g_ik h11 + 1e-240)
+//     h01 = RN(c_ij - RN(c_ik c_jk)) and the certified-dependent filter  !(RN(h01^2) < RN(g_ik h11 + 1e-240))
 //     (5 FP64 instructions per test); tests that the filter cannot certify are decided exactly, in k
 //     order, after the chunk (decide_fast, the same code as the other kernels).
 // Certification: g_ik = RN(h00 * hi2 (1 + 1e-14)) makes RN(g h11 + 1e-240) >= RN(RN(h00 h11) hi2) whenever
 // h00, h11 > 0 (three roundings lose < 4 ulp << 1e-14), so the filter implies decide_fast's "A >= denom
-// hi2" branch, as in surely_dependent (pcs_device.cuh).  A degenerate factor (h00 <= 0 xor h11 <= 0)
-// makes the right-hand side <= 1e-240 and is certified as the reference's degenerate "dependent";
-// both <= 0 falls to the exact path.  Compiled with -fmad=false like level.cu.
+// hi2" branch, as in surely_dependent (pcs_device.cuh).  Degenerate denominators (stats.hpp:301-305:
+// !(h00 h11 > 0), "dependent") are certified too: a zero factor is NaN, so the comparison is false;
+// one negative factor makes the right-hand side negative (|h| >= 2^-53 when nonzero, no underflow);
+// two negative factors give the true positive product and are tested like positive ones.  On
+// rank-truncated inputs (C2, the C5 generator: most |c| round to 1) zero factors are the common case.
+// Compiled with -fmad=false like level.cu.
 //
 // Roofline: 5 FP64 instructions per test on the FP64 pipe; C is read from HBM about once per 32-row
 // band (0.25 B per test) and otherwise served by L2 (blocks of the same target band run together).
@@ -39,6 +43,7 @@ constexpr int kTJ = 64;        // target columns per tile
 constexpr int kKC = 32;        // k per chunk
 constexpr int kThreads = 128;  // 4 warps x (8 rows x 2 targets per lane)
 constexpr int kRowsPerWarp = 8;
+constexpr int kJG = 16;        // target bands per L2 group (16 x 64 columns of C: 8 KB x p)
 
 __device__ __noinline__ int decide_slow1(double h01, double denom, Thresholds th) { return decide_fast(h01, denom, th); }
 
@@ -98,8 +103,14 @@ __global__ void __launch_bounds__(kThreads, 3)
     extern __shared__ __align__(128) unsigned char smem_raw[];
     L1TSmem& S = *reinterpret_cast<L1TSmem*>(smem_raw);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    // consecutive blocks share the target band: their C(k, J) tiles are L2 hits
-    const int jb = blockIdx.x / nI, ib = ib_begin + blockIdx.x % nI;
+    // block order: groups of kJG target bands; inside a group the kJG blocks of one row band run
+    // back to back (its C(I, k) tiles are L2 hits for all but the first) and the group's target bands
+    // C(k, J) stay L2-resident while the row bands stream past: C is read from HBM about
+    // (p / (kJG * kTJ)) + 1 times per pass instead of once per target band
+    const int nJ = (A.p + kTJ - 1) / kTJ;
+    const int grp = blockIdx.x / (nI * kJG), in = blockIdx.x % (nI * kJG);
+    const int gw = min(kJG, nJ - grp * kJG);  // bands in this (possibly last, narrower) group
+    const int jb = grp * kJG + in % gw, ib = ib_begin + in / gw;
     const int i0 = ib * kTI, j0 = jb * kTJ;
     const int p = A.p;
     const int nchunks = (p + kKC - 1) / kKC;
@@ -168,13 +179,14 @@ __global__ void __launch_bounds__(kThreads, 3)
         for (int q = tid; q < kKC * kTJ; q += kThreads) {
             const int kk = q / kTJ, jj = q % kTJ;
             const double c = S.rawJ[kk][jj];
-            S.J2[kk][jj] = make_double2(c, 1.0 - c * c);
+            const double h11 = 1.0 - c * c;
+            S.J2[kk][jj] = make_double2(c, h11 == 0.0 ? __longlong_as_double(0x7ff8000000000000ll) : h11);
         }
         for (int q = tid; q < kTI * kKC; q += kThreads) {
             const int r = q / kKC, kk = q % kKC;
             const double c = S.rawI[r][kk];
             const double h00 = 1.0 - c * c;
-            S.I2[kk][r] = make_double2(c, h00 * g_scale);
+            S.I2[kk][r] = make_double2(c, h00 == 0.0 ? __longlong_as_double(0x7ff8000000000000ll) : h00 * g_scale);
         }
         if (tid < kTI && kc + 1 < nchunks) {
             const int i = i0 + tid;
@@ -208,8 +220,8 @@ __global__ void __launch_bounds__(kThreads, 3)
                         const double2 iv = S.I2[kk][warp * kRowsPerWarp + a];
                         const double x0 = iv.x * jv0.x, x1 = iv.x * jv1.x;
                         const double h0 = cij[a][0] - x0, h1 = cij[a][1] - x1;
-                        const bool d0 = h0 * h0 >= fma(iv.y, jv0.y, kTiny);
-                        const bool d1 = h1 * h1 >= fma(iv.y, jv1.y, kTiny);
+                        const bool d0 = !(h0 * h0 < fma(iv.y, jv0.y, kTiny));
+                        const bool d1 = !(h1 * h1 < fma(iv.y, jv1.y, kTiny));
                         if (!d0) g[a * 2 + 0] |= 1u << u;
                         if (!d1) g[a * 2 + 1] |= 1u << u;
                     }
@@ -236,8 +248,10 @@ __global__ void __launch_bounds__(kThreads, 3)
                         const double2 iv = S.I2[kk][r];
                         const double2 jv = S.J2[kk][lane + 32 * b];
                         const double h01 = cij[a][b] - iv.x * jv.x;
-                        const double den = (1.0 - iv.x * iv.x) * jv.y;
-                        const int d = decide_slow1(h01, den, A.th);
+                        const double den = (1.0 - iv.x * iv.x) * (1.0 - jv.x * jv.x);
+                        int d = decide_slow1(h01, den, A.th);
+                        if (d & kNearBit) atomicAdd(&A.cnt->near, 1ull);
+                        d &= ~kNearBit;
                         if (d == kDependent) continue;
                         tested = valid & ((2u << kk) - 1u);
                         live &= ~(1u << q);

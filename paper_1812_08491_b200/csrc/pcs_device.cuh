@@ -265,6 +265,9 @@ __device__ __forceinline__ void pinv(const double (&a)[L * L], double (&out)[L *
 // --------------------------------------------------------- decision
 // Outcome codes of one CI test.
 enum : int { kDependent = 0, kIndependent = 1, kNanError = 2 };
+// decide_fast / decide0 set this bit when the outcome came from the exact comparison inside the
+// +-1e-9 band around the threshold (the near-threshold tests the parity protocol lists)
+constexpr int kNearBit = 8;
 
 // Exact reference decision from (h01, denom) (stats.hpp:301-306 + 345-351).
 __device__ __forceinline__ int decide_exact(double h01, double denom, double tau, double* z_out = nullptr,
@@ -292,7 +295,7 @@ __device__ __forceinline__ int decide_fast(double h01, double denom, const Thres
         if (A <= denom * th.lo2) return kIndependent;
         if (A >= denom * th.hi2) return kDependent;
     }
-    return decide_exact(h01, denom, th.tau);
+    return decide_exact(h01, denom, th.tau) | kNearBit;
 }
 
 // Branch-free common-case filter: true only when decide_fast() is certainly
@@ -340,7 +343,7 @@ __device__ __forceinline__ int decide0(double c, const Thresholds& th) {
     double v = c < -kRhoClamp ? -kRhoClamp : (c > kRhoClamp ? kRhoClamp : c);
     if (!(v > -1.0 && v < 1.0)) return kNanError;
     const double z = fabs(0.5 * log((1.0 + v) / (1.0 - v)));
-    return z <= th.tau ? kIndependent : kDependent;
+    return (z <= th.tau ? kIndependent : kDependent) | kNearBit;
 }
 
 // Partial-correlation pieces with a shared inverse (stats.hpp:292-307):

@@ -26,6 +26,7 @@ struct Counters {
     unsigned long long rec_count;   // sepset records written
     unsigned long long units[2];    // persistent-grid work cursors (pass A / B)
     unsigned long long dbg[4];      // diagnostics builds only (PCS_COUNT_CAND)
+    unsigned long long near;        // decisions taken by the exact comparison inside the threshold band
     int err_nan;                    // fisher_z would throw (NaN statistic)
     int err_other;
 };
@@ -64,6 +65,11 @@ struct LevelArgs {
 
 // ---- corr.cu
 void launch_normalize_corr(double* C, long long ldc, int p, int* err, cudaStream_t s);
+// rows [r0, r1) of C only (multi-GPU split); G holds the row band's tiles: ((r1 - r0) + 2 * 64) x ldg
+void launch_correlation_rows(const double* X, int m, int p, int r0, int r1, double* Xc, double* G, long long ldg,
+                             double* mean, double* C, long long ldc, int* err_flags, cudaStream_t s);
+// flag |= 1 unless C has a unit diagonal, bitwise symmetry and finite entries in [-1, 1]
+void launch_check_corr(const double* C, long long ldc, int p, int* flag, cudaStream_t s);
 void launch_correlation(const double* X, int m, int p, double* Xc, double* G, long long ldg, double* mean,
                         double* C, long long ldc, int* err_flags, cudaStream_t s);
 

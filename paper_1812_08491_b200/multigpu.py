@@ -70,6 +70,50 @@ def host_staged_allreduce_min(group=None):
     return _reduce
 
 
+def row_band(p: int, rank: int, world: int) -> tuple[int, int, int]:
+    """(row_begin, row_end, band) of this rank's correlation rows: equal bands of ceil(p / world) rows
+    (all_gather_into_tensor needs equal chunks; the last band may be short or empty)."""
+    band = (p + world - 1) // world
+    r0 = min(p, rank * band)
+    return r0, min(p, r0 + band), band
+
+
+def correlation_sharded(x_ptr: int, m: int, p: int, c, group=None, stream: int = 0, gather=None):
+    """compute_correlation split over the ranks: rank r builds rows
+    [r * B, (r + 1) * B) of C (B = ceil(p / N)) with its own Gram row band, then the bands are
+    all-gathered into every rank's copy (NCCL over NVLink by default).  `c` is a torch float64 tensor
+    of shape (N * B, ldc) on this rank's device; rows >= p are scratch.  The assembled rows are
+    bit-identical to a one-GPU correlation_device (tests/test_gpu_multiproc.py)."""
+    import torch
+    import torch.distributed as dist
+
+    from . import correlation_device_rows
+
+    rank = dist.get_rank(group) if dist.is_initialized() else 0
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    r0, r1, band = row_band(p, rank, world)
+    ldc = c.shape[1]
+    assert c.shape[0] >= band * world and c.dtype == torch.float64
+    correlation_device_rows(x_ptr, m, p, r0, r1, c.data_ptr(), ldc, stream)
+    if world > 1:
+        torch.cuda.synchronize()
+        mine = c[rank * band:(rank + 1) * band].clone()
+        (gather or dist.all_gather_into_tensor)(c[:band * world], mine, group=group)
+        torch.cuda.synchronize()
+    return c
+
+
+def host_staged_all_gather(out, inp, group=None):
+    """all_gather_into_tensor through host memory (gloo: ranks sharing one GPU in tests)."""
+    import torch
+    import torch.distributed as dist
+
+    world = dist.get_world_size(group)
+    parts = [torch.empty_like(inp, device="cpu") for _ in range(world)]
+    dist.all_gather(parts, inp.cpu(), group=group)
+    out.copy_(torch.cat(parts).to(out.device))
+
+
 def run_pc_stable_sharded(c_ptr: int, ldc: int, p: int, sample_count: int, cfg=None, group=None,
                           with_sepsets: bool = True, allreduce_min=None):
     """run_pc_stable over all ranks of `group` (torch.distributed initialised, one GPU per rank).

@@ -36,7 +36,7 @@ def test_two_ranks_report_the_single_rank_work(pcs):
     two = _bench({"PCS_BENCH_BACKEND": "gloo"},
                  [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
                   "--master-addr", "127.0.0.1", "--master-port", str(_free_port())])
-    assert two["n_gpus"] == 2 and two["config"]["multi_gpu"]["ranks"] == 2
+    assert two["n_gpus"] == 2 and two["detail"]["multi_gpu"]["ranks"] == 2
     for k in ("serial_ci_tests", "levels_run", "stop_reason", "edges_left"):
-        assert two["config"][k] == one["config"][k], k
+        assert two["detail"][k] == one["detail"][k], k
     assert two["value"] > 0 and two["gpu_launches"] > 0

@@ -59,3 +59,36 @@ def test_two_ranks_on_one_gpu_match_single_process(pcs, oracle, variant):
         assert [x[3] for x in levels] == [l.edges_removed for l in ref.levels], f"rank {r}: removed"
         assert [x[1] for x in levels] == [l.ci_tests for l in ref.levels], f"rank {r}: ci_tests"
         assert stop == ref.stop_reason
+
+
+def _corr_worker(rank, world, port, x, out):
+    import torch
+    import torch.distributed as dist
+
+    from paper_1812_08491_b200.multigpu import correlation_sharded, host_staged_all_gather, row_band
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    p, m = x.shape
+    ldc = (p + 3) // 4 * 4
+    band = row_band(p, rank, world)[2]
+    xd = torch.from_numpy(np.ascontiguousarray(x)).cuda()  # (p, m): column-major m x p data
+    c = torch.full((band * world, ldc), float("nan"), dtype=torch.float64, device="cuda")
+    correlation_sharded(xd.data_ptr(), m, p, c, gather=host_staged_all_gather)
+    out[rank] = c[:p, :p].cpu().numpy().copy()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("p,world", [(203, 2), (150, 3)])
+def test_correlation_row_split_matches_single_gpu(pcs, oracle, p, world):
+    """Each rank builds its row band of C; after the all-gather every rank holds the single-GPU
+    matrix bit for bit (and the oracle's FMA-order restatement)."""
+    w = oracle.random_dag(p, 0.05, 3)
+    x = oracle.sample_linear_gaussian(w, 777, 4)  # (p, m), m not a multiple of the k tile
+    full = pcs.compute_correlation(x.T)
+    assert np.array_equal(full.view(np.int64), oracle.compute_correlation_fma(x, threads=4).view(np.int64))
+    out = mp.Manager().dict()
+    mp.start_processes(_corr_worker, args=(world, _free_port(), x, out), nprocs=world, join=True,
+                       start_method="spawn")
+    for r in range(world):
+        assert np.array_equal(out[r].view(np.int64), full.view(np.int64)), f"rank {r}"
