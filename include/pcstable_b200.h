@@ -102,6 +102,14 @@ pcs_status pcs_correlation(const double* x, int32_t m, int32_t p, double* c_out,
 /* run_pc_stable (skeleton.hpp:341-391).  c: p x p host correlation matrix, validated and normalised
    exactly like the CorrelationMatrix constructor (core.hpp:73-95). */
 pcs_status pcs_run_pc_stable(const double* c, int32_t p, int32_t m, const pcs_config* cfg, pcs_result** out);
+/* One level on a given live graph (skeleton.hpp:262-333: run_level_zero for ell = 0, run_level_serial /
+   run_level_edge_parallel / run_level_set_shared for ell >= 1 by cfg->variant): graph_cells is the p x p
+   symmetric 0/1 adjacency (core.hpp:109-194) and doubles as the level-start snapshot (compact(),
+   core.hpp:227-239); tau is the caller's threshold; graph_cells is updated in place and *out holds the
+   level's LevelStats (one entry) and the sepsets of the pairs it removed.  Counters follow
+   Strategy::Serial's definition for every variant (include/pcstable_b200.hpp). */
+pcs_status pcs_run_level(const double* c, int32_t p, int32_t ell, double tau, const pcs_config* cfg,
+                         uint8_t* graph_cells, pcs_result** out);
 /* compute_correlation from device-resident m x p column-major data into a device p x ldc buffer,
    enqueued on `stream` (0 = legacy default stream); synchronous */
 pcs_status pcs_correlation_device(const double* d_x, int32_t m, int32_t p, double* d_c, int64_t ldc, uint64_t stream,

@@ -454,6 +454,101 @@ inline SkeletonResult run_pc_stable(const CorrelationMatrix& c, Index sample_cou
     return detail::collect(r);
 }
 
+namespace detail {
+
+// one level on the device from the caller's live graph (pcs_run_level); the graph doubles as the
+// level-start snapshot, so a separate snapshot must equal compact(graph)
+inline LevelStats run_level_device(const CorrelationMatrix& c, AdjacencyMatrix& graph, SeparationSets& sepsets,
+                                   double tau, int ell, SkeletonConfig cfg, Strategy strategy) {
+    const Index n = c.size();
+    if (graph.size() != n || sepsets.size() != n) throw std::invalid_argument("run_level: size mismatch");
+    cfg.strategy = strategy;
+    cfg.validate();
+    const pcs_config abi = to_abi(cfg);
+    const std::vector<uint8_t> before(graph.raw(), graph.raw() + static_cast<std::size_t>(n) * n);
+    pcs_result* raw = nullptr;
+    check(pcs_run_level(c.data(), n, ell, tau, &abi, graph.raw(), &raw));
+    ResultPtr r(raw);
+    const std::size_t slots = static_cast<std::size_t>(n) * (n - 1) / 2;
+    std::vector<int32_t> level(slots);
+    std::vector<int64_t> offset(slots);
+    std::vector<int32_t> members(static_cast<std::size_t>(std::max<int64_t>(pcs_result_member_total(r.get()), 1)));
+    pcs_result_sepsets(r.get(), level.data(), offset.data(), members.data());
+    std::size_t s = 0;
+    for (Index i = 0; i < n; ++i)
+        for (Index j = i + 1; j < n; ++j, ++s)
+            if (before[static_cast<std::size_t>(i) * n + j] && !graph.at(i, j))  // removed by this level
+                sepsets.store(i, j, level[s] == ell ? std::vector<Index>(members.begin() + offset[s],
+                                                                         members.begin() + offset[s] + ell)
+                                                    : std::vector<Index>{});
+    LevelStats out;
+    out.level = ell;
+    pcs_level_stats L{};
+    if (pcs_result_levels(r.get(), &L, 1) == 1) {
+        out.ci_tests = L.ci_tests;
+        out.pseudo_inverses = L.pseudo_inverses;
+        out.edges_removed = L.edges_removed;
+        out.elapsed = std::chrono::nanoseconds(static_cast<std::int64_t>(L.elapsed_s * 1e9));
+        out.device_ci_tests = L.device_ci_tests;
+        out.device_pseudo_inverses = L.device_pseudo_inverses;
+        out.kernel_ms = L.kernel_ms;
+        out.device_exact_tests = L.device_exact_tests;
+        out.device_near_threshold = L.device_near_threshold;
+    }
+    return out;
+}
+
+inline void check_snapshot(const CompactedAdjacency& snapshot, const AdjacencyMatrix& graph) {
+    const Index n = graph.size();
+    bool same = snapshot.size() == n;
+    for (Index i = 0; same && i < n; ++i) {
+        Index k = 0;
+        for (Index j = 0; j < n && same; ++j)
+            if (graph.at(i, j)) same = k < snapshot.count(i) && snapshot.row(i)[k++] == j;
+        same = same && k == snapshot.count(i);
+    }
+    if (!same) throw std::invalid_argument("run_level: the device takes the snapshot from the live graph; "
+                                           "snapshot must equal compact(graph)");
+}
+
+}  // namespace detail
+
+/// run_level_zero (skeleton.hpp:262-288): one unconditional test per unordered pair; `workers` is
+/// accepted for signature parity (the device schedule has no worker count).
+inline LevelStats run_level_zero(const CorrelationMatrix& c, double tau0, AdjacencyMatrix& graph,
+                                 SeparationSets& sepsets, int workers = 1) {
+    if (sepsets.size() != graph.size()) throw std::invalid_argument("run_level_zero: size mismatch");
+    (void)workers;
+    return detail::run_level_device(c, graph, sepsets, tau0, 0, SkeletonConfig{}, Strategy::Serial);
+}
+
+/// run_level_serial (skeleton.hpp:292-307): Strategy::Serial's level (cuPC-S kernels, serial-rule result).
+inline LevelStats run_level_serial(const CorrelationMatrix& c, const CompactedAdjacency& snapshot,
+                                   AdjacencyMatrix& graph, SeparationSets& sepsets, double tau, int ell,
+                                   const SkeletonConfig& cfg) {
+    if (ell < 1) throw std::invalid_argument("run_level_serial: need ell >= 1");
+    detail::check_snapshot(snapshot, graph);
+    return detail::run_level_device(c, graph, sepsets, tau, ell, cfg, Strategy::Serial);
+}
+
+/// run_level_edge_parallel (skeleton.hpp:311-320): the cuPC-E kernels.
+inline LevelStats run_level_edge_parallel(const CorrelationMatrix& c, const CompactedAdjacency& snapshot,
+                                          AdjacencyMatrix& graph, SeparationSets& sepsets, double tau, int ell,
+                                          const SkeletonConfig& cfg) {
+    if (ell < 1) throw std::invalid_argument("run_level_edge_parallel: need ell >= 1");
+    detail::check_snapshot(snapshot, graph);
+    return detail::run_level_device(c, graph, sepsets, tau, ell, cfg, Strategy::EdgeParallel);
+}
+
+/// run_level_set_shared (skeleton.hpp:325-333): the cuPC-S kernels.
+inline LevelStats run_level_set_shared(const CorrelationMatrix& c, const CompactedAdjacency& snapshot,
+                                       AdjacencyMatrix& graph, SeparationSets& sepsets, double tau, int ell,
+                                       const SkeletonConfig& cfg) {
+    if (ell < 1) throw std::invalid_argument("run_level_set_shared: need ell >= 1");
+    detail::check_snapshot(snapshot, graph);
+    return detail::run_level_device(c, graph, sepsets, tau, ell, cfg, Strategy::SetShared);
+}
+
 /// compute_correlation + run_pc_stable in one device pipeline (the pair bench.hpp:107-113 times).
 inline SkeletonResult run_pc_stable(const DataMatrix& data, const SkeletonConfig& cfg) {
     cfg.validate();

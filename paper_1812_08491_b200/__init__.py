@@ -135,6 +135,8 @@ def library():
     L.pcs_result_record_ints.restype = ct.c_int64
     L.pcs_result_records.argtypes = [vp, ip]
     L.pcs_correlation_device.argtypes = [vp, ct.c_int32, ct.c_int32, vp, ct.c_int64, ct.c_uint64, ip]
+    L.pcs_run_level.argtypes = [dp, ct.c_int32, ct.c_int32, ct.c_double, ct.POINTER(_Config), ct.POINTER(ct.c_uint8),
+                                ct.POINTER(vp)]
     L.pcs_correlation_device_rows.argtypes = [vp, ct.c_int32, ct.c_int32, ct.c_int32, ct.c_int32, vp, ct.c_int64,
                                               ct.c_uint64, ip]
     L.pcs_kernel_launches.restype = ct.c_ulonglong
@@ -282,20 +284,26 @@ class SeparationSets:
         self.n = n
         self._skel = skeleton
         self.records = np.ascontiguousarray(records, np.int32)  # (a, b, ell, members...) of levels >= 1
-        self._blocks = []
-        at = 0
-        for lv in levels:
-            if lv.level < 1 or lv.edges_removed == 0 or at >= len(records):
-                continue
-            ell, cnt = lv.level, lv.edges_removed
-            blk = np.asarray(records[at:at + cnt * (3 + ell)]).reshape(cnt, 3 + ell)
-            at += cnt * (3 + ell)
-            a = np.minimum(blk[:, 0], blk[:, 1]).astype(np.int64)
-            b = np.maximum(blk[:, 0], blk[:, 1]).astype(np.int64)
-            key = a * n + b
-            order = np.argsort(key, kind="stable")
-            self._blocks.append((ell, key[order], np.ascontiguousarray(blk[order, 3:])))
+        self._levels = [(lv.level, lv.edges_removed) for lv in levels]
+        self._sorted = None  # per-level (ell, sorted pair keys, members), built on first lookup
         self._dict = None
+
+    @property
+    def _blocks(self):
+        if self._sorted is None:
+            blocks, at, n, records = [], 0, self.n, self.records
+            for ell, cnt in self._levels:
+                if ell < 1 or cnt == 0 or at >= len(records):
+                    continue
+                blk = np.asarray(records[at:at + cnt * (3 + ell)]).reshape(cnt, 3 + ell)
+                at += cnt * (3 + ell)
+                a = np.minimum(blk[:, 0], blk[:, 1]).astype(np.int64)
+                b = np.maximum(blk[:, 0], blk[:, 1]).astype(np.int64)
+                key = a * n + b
+                order = np.argsort(key, kind="stable")
+                blocks.append((ell, key[order], np.ascontiguousarray(blk[order, 3:])))
+            self._sorted = blocks
+        return self._sorted
 
     def size(self) -> int:
         return self.n
@@ -463,6 +471,35 @@ def correlation_device(x_ptr: int, m: int, p: int, c_ptr: int, ldc: int, stream:
     rc = library().pcs_correlation_device(ct.c_void_p(x_ptr), m, p, ct.c_void_p(c_ptr), ldc, stream, ct.byref(col))
     if rc:
         _raise(rc, col.value)
+
+
+def run_level(c, graph_cells, ell: int, tau: float, cfg: Optional[SkeletonConfig] = None):
+    """One level on a given live graph (run_level_zero / run_level_serial / run_level_edge_parallel /
+    run_level_set_shared, skeleton.hpp:262-333; cfg.strategy picks the kernels).  graph_cells: (p, p)
+    0/1 symmetric, the level-start snapshot.  Returns (graph after the level, LevelStats, {(i, j): sepset}
+    of the pairs this level removed)."""
+    cfg = cfg or SkeletonConfig()
+    c = np.ascontiguousarray(c, np.float64)
+    p = c.shape[0]
+    g = np.ascontiguousarray(np.asarray(graph_cells, np.uint8)).copy()
+    before = g.copy()
+    h = ct.c_void_p()
+    abi = cfg._abi()
+    rc = library().pcs_run_level(_dp(c), p, ell, tau, ct.byref(abi), g.ctypes.data_as(ct.POINTER(ct.c_uint8)),
+                                 ct.byref(h))
+    if rc:
+        _raise(rc)
+    try:
+        res = _collect(h)
+    finally:
+        library().pcs_result_free(h)
+    lv = res.levels[0] if res.levels else LevelStats(ell, 0, 0, 0, 0.0)
+    removed = np.argwhere(np.triu(before.astype(bool) & ~g.astype(bool), 1))
+    sep = {}
+    for i, j in removed:
+        got = res.sepsets.find(int(i), int(j))
+        sep[(int(i), int(j))] = tuple(got) if (got is not None and ell > 0) else ()
+    return g, lv, sep
 
 
 def correlation_device_rows(x_ptr: int, m: int, p: int, row_begin: int, row_end: int, c_ptr: int, ldc: int,

@@ -220,6 +220,8 @@ struct pcs_session {
     // level state
     int ell = -1;
     bool stopped = false, in_level = false;
+    double tau_override = NAN;     // pcs_run_level: the caller's threshold instead of threshold_tau
+    bool level0_and = false;       // pcs_run_level at ell = 0: the input graph may be incomplete
     int stop_reason = PCS_STOP_MAX_DEGREE;
     SnapInfo info{};
     Thresholds th{};
@@ -556,9 +558,13 @@ pcs_status pcs_session_level_begin(pcs_session* s, int32_t* running, int32_t* el
     *ell_out = ell;
     if (s->cfg.max_level >= 0 && ell > s->cfg.max_level) { stop(s, PCS_STOP_LEVEL_CAP); return PCS_OK; }
     double tau;
-    pcs_status st = threshold_tau(s->cfg.alpha, s->m, ell, &tau);
-    if (st == PCS_ELEVEL) { stop(s, PCS_STOP_SAMPLE_SIZE); return PCS_OK; }
-    if (st) return st;
+    pcs_status st = PCS_OK;
+    if (!std::isnan(s->tau_override)) tau = s->tau_override;
+    else {
+        st = threshold_tau(s->cfg.alpha, s->m, ell, &tau);
+        if (st == PCS_ELEVEL) { stop(s, PCS_STOP_SAMPLE_SIZE); return PCS_OK; }
+        if (st) return st;
+    }
     s->ell = ell;
     s->th = make_thresholds(tau);
     s->t_level = now_s();
@@ -566,7 +572,7 @@ pcs_status pcs_session_level_begin(pcs_session* s, int32_t* running, int32_t* el
     CUDA_TRY(cudaMemsetAsync(s->dCnt, 0, sizeof(Counters), s->st));
     if (ell == 0) {
         CUDA_TRY(cudaEventRecord(s->ev_k0, s->st));
-        launch_level0(s->dC, s->ldc, s->p, s->W, s->dAdj, s->th, s->dCnt, s->st);
+        launch_level0(s->dC, s->ldc, s->p, s->W, s->dAdj, s->th, s->dCnt, s->st, s->level0_and);
         CUDA_TRY(cudaEventRecord(s->ev_k1, s->st));
         s->kernel_timing = true;
         CUDA_TRY(cudaGetLastError());
@@ -894,6 +900,55 @@ pcs_status pcs_run_pc_stable(const double* c, int32_t p, int32_t m, const pcs_co
     if (st) return st;
     st = run_session(s, out);
     free_session(s);
+    return st;
+}
+
+// One level on a caller-given live graph (run_level_zero / run_level_serial / run_level_edge_parallel /
+// run_level_set_shared, skeleton.hpp:262-333): the session starts at that graph instead of the complete
+// one, takes the caller's tau, and runs exactly level ell.
+pcs_status pcs_run_level(const double* c, int32_t p, int32_t ell, double tau, const pcs_config* cfg,
+                         uint8_t* graph_cells, pcs_result** out) {
+    *out = nullptr;
+    if (!c || !graph_cells || !cfg) return fail(PCS_EINVAL, "null argument");
+    if (ell < 0) return fail(PCS_EINVAL, "run_level: ell must be >= 0");
+    if (!(tau >= 0.0)) return fail(PCS_EINVAL, "run_level: tau must be >= 0");
+    pcs_config c2 = *cfg;
+    c2.max_level = -1;
+    pcs_session* s = nullptr;
+    pcs_status st = pcs_session_create(c, p, 1 << 30, &c2, &s);
+    if (st) return st;
+    st = [&]() -> pcs_status {
+        std::vector<uint32_t> bits((size_t)p * s->W, 0u);
+        for (int i = 0; i < p; ++i)
+            for (int j = 0; j < p; ++j) {
+                if (i == j) continue;
+                const uint8_t a = graph_cells[(size_t)i * p + j], b = graph_cells[(size_t)j * p + i];
+                if (a != b) return fail(PCS_EINVAL, "AdjacencyMatrix: graph must be symmetric");
+                if (a) bits[(size_t)i * s->W + j / 32] |= 1u << (j % 32);
+            }
+        CUDA_TRY(cudaMemcpyAsync(s->dAdj, bits.data(), sizeof(uint32_t) * bits.size(), cudaMemcpyHostToDevice, s->st));
+        s->tau_override = tau;
+        s->level0_and = true;
+        s->ell = ell - 1;
+        int32_t running = 0, e = 0;
+        int64_t nk = 0;
+        pcs_status q = pcs_session_level_begin(s, &running, &e, &nk);
+        if (q) return q;
+        if (running) {
+            if ((q = pcs_session_level_pass(s, 0))) return q;
+            if ((q = pcs_session_level_pass(s, 1))) return q;
+            if ((q = pcs_session_level_end(s))) return q;
+        }
+        if ((q = pcs_session_finish(s, out))) return q;
+        (*out)->stop_reason = PCS_STOP_LEVEL_CAP;
+        const int W = (*out)->W;
+        for (int i = 0; i < p; ++i)
+            for (int j = 0; j < p; ++j)
+                graph_cells[(size_t)i * p + j] = (uint8_t)(((*out)->adj[(size_t)i * W + j / 32] >> (j % 32)) & 1u);
+        return PCS_OK;
+    }();
+    free_session(s);
+    if (st && *out) { pcs_result_free(*out); *out = nullptr; }
     return st;
 }
 

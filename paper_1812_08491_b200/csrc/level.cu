@@ -129,8 +129,10 @@ __device__ unsigned long long rank_rt(const BinomTable& C, int w, int ell, const
 }  // namespace
 
 // =========================================================== level 0
+// and_live: keep only pairs already live in adj (pcs_run_level on an incomplete graph; run_pc_stable
+// starts from the complete graph and overwrites)
 __global__ void level0_kernel(const double* __restrict__ C, long long ldc, int p, int W, uint32_t* __restrict__ adj,
-                              Thresholds th, Counters* cnt) {
+                              Thresholds th, Counters* cnt, int and_live) {
     const int lane = threadIdx.x & 31;
     const long long warp = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const long long nwarps = ((long long)gridDim.x * blockDim.x) >> 5;
@@ -139,13 +141,15 @@ __global__ void level0_kernel(const double* __restrict__ C, long long ldc, int p
     for (long long item = warp; item < (long long)p * W; item += nwarps) {
         const int i = (int)(item / W), w = (int)(item % W);
         const int j = w * 32 + lane;
+        const bool was = and_live ? ((adj[(size_t)i * W + w] >> lane) & 1u) != 0 : true;
         bool live = false;
         if (j < p && j != i) {
             const int d = take_near(decide0(__ldg(C + (size_t)i * ldc + j), th), cnt);
             nan |= d == kNanError;
-            live = d == kDependent;
-            if (j > i && d == kIndependent) ++removed;
+            live = d == kDependent && was;
+            if (j > i && d == kIndependent && was) ++removed;
         }
+        __syncwarp();
         const unsigned word = __ballot_sync(0xffffffffu, live);
         if (lane == 0) adj[(size_t)i * W + w] = word;
     }
@@ -154,12 +158,12 @@ __global__ void level0_kernel(const double* __restrict__ C, long long ldc, int p
 }
 
 void launch_level0(const double* C, long long ldc, int p, int W, uint32_t* adj, Thresholds th, Counters* cnt,
-                   cudaStream_t s) {
+                   cudaStream_t s, bool and_live) {
     const long long items = (long long)p * W;
     long long blocks = (items * 32 + 255) / 256;
     if (blocks > 148 * 16) blocks = 148 * 16;
     ++g_kernel_launches;
-    level0_kernel<<<(int)blocks, 256, 0, s>>>(C, ldc, p, W, adj, th, cnt);
+    level0_kernel<<<(int)blocks, 256, 0, s>>>(C, ldc, p, W, adj, th, cnt, and_live ? 1 : 0);
 }
 
 // =========================================================== snapshot

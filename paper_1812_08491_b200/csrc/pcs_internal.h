@@ -75,7 +75,7 @@ void launch_correlation(const double* X, int m, int p, double* Xc, double* G, lo
 
 // ---- level.cu
 void launch_level0(const double* C, long long ldc, int p, int W, uint32_t* adj, Thresholds th, Counters* cnt,
-                   cudaStream_t s);
+                   cudaStream_t s, bool and_live = false);
 void launch_snapshot_degrees(const uint32_t* adj, int p, int W, int32_t* deg, int32_t* lowcnt, cudaStream_t s);
 void launch_snapshot_scan(const int32_t* deg, const int32_t* lowcnt, int p, int32_t* off, int32_t* upoff,
                           SnapInfo* info, cudaStream_t s);

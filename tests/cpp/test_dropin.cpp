@@ -247,6 +247,60 @@ static void test_orientation() {
     }
 }
 
+// test_skeleton.cpp:342-358 (EdgeParallelStrategy.StopsAtFirstSeparatingSet) through run_level_*,
+// plus run_level_zero and the set-shared dense-row pin (test_skeleton.cpp:300-317) with the
+// drop-in's documented counter semantics.
+static void test_run_level_entry_points() {
+    const double s = 1.0 / std::sqrt(3.0), t = std::sqrt(3.0) / 2.0;
+    const CorrelationMatrix c =
+        make_correlation(4, {{0, 1, s}, {0, 2, s}, {0, 3, t}, {1, 2, 0.0}, {1, 3, 0.5}, {2, 3, 0.5}});
+    {  // level 0 on the complete graph removes (1, 2) with the empty set
+        AdjacencyMatrix graph = AdjacencyMatrix::complete(4);
+        SeparationSets sepsets(4);
+        const LevelStats l0 = run_level_zero(c, stats::threshold_tau(0.05, 1000, 0), graph, sepsets, 2);
+        EXPECT(l0.ci_tests == 6u && l0.edges_removed == 1u);
+        EXPECT(!graph.at(1, 2) && sepsets.find(1, 2) && sepsets.find(1, 2)->empty());
+    }
+    for (Strategy st : {Strategy::EdgeParallel, Strategy::SetShared, Strategy::Serial}) {
+        AdjacencyMatrix graph = AdjacencyMatrix::complete(4);
+        SeparationSets sepsets(4);
+        graph.clear_edge(1, 2);
+        const CompactedAdjacency snapshot = compact(graph);
+        SkeletonConfig cfg;
+        cfg.strategy = st;
+        const double tau1 = stats::threshold_tau(0.05, 1000, 1);
+        const LevelStats tally =
+            st == Strategy::EdgeParallel ? run_level_edge_parallel(c, snapshot, graph, sepsets, tau1, 1, cfg)
+            : st == Strategy::SetShared  ? run_level_set_shared(c, snapshot, graph, sepsets, tau1, 1, cfg)
+                                         : run_level_serial(c, snapshot, graph, sepsets, tau1, 1, cfg);
+        EXPECT(tally.edges_removed == 2u);
+        EXPECT(!graph.at(1, 3) && !graph.at(2, 3));
+        EXPECT(sepsets.find(1, 3) && *sepsets.find(1, 3) == std::vector<Index>{0});
+        EXPECT(sepsets.find(2, 3) && *sepsets.find(2, 3) == std::vector<Index>{0});
+        // a snapshot that is not compact(graph) is rejected (the device reads the live graph)
+        AdjacencyMatrix other = AdjacencyMatrix::complete(4);
+        EXPECT_THROW(run_level_serial(c, compact(other), graph, sepsets, tau1, 1, cfg), std::invalid_argument);
+    }
+    {  // test_skeleton.cpp:300-317: complete 6-vertex graph, all c = 0.9, tau ~ 0 -> nothing separates
+        std::vector<std::tuple<Index, Index, double>> e;
+        for (Index i = 0; i < 6; ++i)
+            for (Index j = i + 1; j < 6; ++j) e.push_back({i, j, 0.9});
+        const CorrelationMatrix c6 = make_correlation(6, e);
+        AdjacencyMatrix graph = AdjacencyMatrix::complete(6);
+        SeparationSets sepsets(6);
+        SkeletonConfig cfg;
+        cfg.strategy = Strategy::SetShared;
+        const LevelStats tally = run_level_set_shared(c6, compact(graph), graph, sepsets, 1e-9, 2, cfg);
+        // ci_tests: 15 edges x 2 directions x C(4, 2) sets = 180, the same for every strategy when
+        // nothing separates (the reference's SetShared also reports 6 * C(5, 2) * 3 = 180).
+        EXPECT(tally.ci_tests == 180u);
+        // pseudo_inverses follow Strategy::Serial (one per test: 180); the reference's SetShared
+        // reports one per (row, set): 6 * C(5, 2) = 60 -- the documented deviation.
+        EXPECT(tally.pseudo_inverses == 180u);
+        EXPECT(tally.edges_removed == 0u && graph.edge_count() == 15u);
+    }
+}
+
 int main() {
     const std::vector<std::pair<std::string, std::function<void()>>> tests = {
         {"star_graph_set", [] { test_star_graph(Strategy::SetShared); }},
@@ -259,6 +313,7 @@ int main() {
         {"oracle_p100_edge", [] { test_against_oracle(100, 2.0 / 99.0, 1000, 0, Strategy::EdgeParallel); }},
         {"oracle_p120_set", [] { test_against_oracle(120, 0.1, 500, 15838, Strategy::SetShared); }},
         {"orientation", test_orientation},
+        {"run_level_entry_points", test_run_level_entry_points},
     };
     for (const auto& [name, fn] : tests) {
         const int before = g_failed;

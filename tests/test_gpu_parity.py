@@ -243,3 +243,24 @@ def test_data_pipeline_matches(pcs, oracle):
     dev = pcs.run_pc_stable_data(x.T, pcs.SkeletonConfig(alpha=0.01))
     ref = oracle.run_pc_stable(oracle.compute_correlation(x), 2000, alpha=0.01)
     assert dev.edge_set() == ref.edge_set()
+
+
+@pytest.mark.parametrize("variant", ["set", "edge"])
+def test_run_level_chain_equals_run_pc_stable(pcs, oracle, variant):
+    """pcs_run_level (run_level_zero / run_level_serial / run_level_edge_parallel / run_level_set_shared,
+    skeleton.hpp:262-333) applied level by level with threshold_tau reproduces the oracle's whole run:
+    same graph after every level, same sepsets, same per-level counters."""
+    m, alpha = 400, 0.05
+    c = instance(oracle, 40, 0.25, m, 5)
+    ref = oracle.run_pc_stable(c, m, alpha=alpha)
+    p = c.shape[0]
+    g = np.ones((p, p), np.uint8) - np.eye(p, dtype=np.uint8)
+    cfg = pcs.SkeletonConfig(alpha=alpha, strategy=pcs.Strategy(variant))
+    sep = {}
+    for lv in ref.levels:
+        tau = oracle.threshold_tau(alpha, m, lv.level)
+        g, st, removed = pcs.run_level(c, g, lv.level, tau, cfg)
+        sep.update(removed)
+        assert (st.level, st.ci_tests, st.edges_removed) == (lv.level, lv.ci_tests, lv.edges_removed)
+    assert np.array_equal(g, ref.adjacency)
+    assert sep == ref.sepsets
