@@ -980,7 +980,7 @@ static pcs_status correlation_device(cudaStream_t stream, const double* x, int m
         return dev_malloc(reinterpret_cast<void**>(ptr), bytes, stream) != cudaSuccess;
     };
     if ((!x_on_device && alloc(&dX, sizeof(double) * (size_t)m * p)) || alloc(&dXc, sizeof(double) * (size_t)p * ldk) ||
-        alloc(&dG, sizeof(double) * (size_t)(r0 >= 0 ? std::min<long long>(p, (long long)(r1 - r0) + 128) : p) * ldg) ||
+        alloc(&dG, sizeof(double) * (size_t)(r0 >= 0 ? std::min<long long>(p, (long long)(r1 - r0) + 256) : p) * ldg) ||
         alloc(&dMean, sizeof(double) * (size_t)p) ||
         alloc(&dErr, sizeof(int) * 2)) {
         cleanup();

@@ -65,7 +65,7 @@ struct LevelArgs {
 
 // ---- corr.cu
 void launch_normalize_corr(double* C, long long ldc, int p, int* err, cudaStream_t s);
-// rows [r0, r1) of C only (multi-GPU split); G holds the row band's tiles: ((r1 - r0) + 2 * 64) x ldg
+// rows [r0, r1) of C only (multi-GPU split); G holds the row band's tiles: ((r1 - r0) + 256) x ldg
 void launch_correlation_rows(const double* X, int m, int p, int r0, int r1, double* Xc, double* G, long long ldg,
                              double* mean, double* C, long long ldc, int* err_flags, cudaStream_t s);
 // flag |= 1 unless C has a unit diagonal, bitwise symmetry and finite entries in [-1, 1]

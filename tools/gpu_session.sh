@@ -95,6 +95,11 @@ for s in $STEPS; do
       PCS_L1_TILE=1 timeout 900 ncu --set full --clock-control none --import-source on -k regex:level1_tile -c 1 -f -o $OUT/l1t \
         python tools/explore.py C5b set 1 > $OUT/ncu_l1t.log 2>&1
       ;;
+    gram)
+      for v in 1 2; do PCS_GRAM=$v timeout 900 python tools/time_corr.py C2,C3,C5b,C5e 5 >> $OUT/gram_ab.log 2>&1; done
+      timeout 900 ncu --set full --clock-control none --import-source on -k regex:gram_dmma2 -c 1 -f -o $OUT/gram2 \
+        python tools/time_corr.py C2 1 > $OUT/ncu_gram2.log 2>&1
+      ;;
     bench)
       timeout 900 python bench.py > $OUT/bench.json 2> $OUT/bench.err
       ;;
