@@ -1305,267 +1305,6 @@ __global__ void __launch_bounds__(kSetWarps * 32, PCS_SET_MINB) level_set_kernel
     if (nan) atomicOr(&A.cnt->err_nan, 1);
 }
 
-// =========================================================== ell = 2, 3: warp-specialised cuPC-S
-// The same units, results and counters as level_set_kernel<L>, with phase 1 taken off the testing
-// warps: one producer warp per block grabs units from the work cursor, computes their 32 pseudo-
-// inverses lane-parallel (latency-bound chains of correctly rounded divisions / square roots) and
-// publishes them into a shared-memory ring; the block's other warps (consumers) take ring entries in
-// ticket order, copy the slots into their own SetWarpSmem and run staging + phase 2 exactly as
-// level_set_kernel does.  The producer's latency then overlaps the consumers' FP64-bound sweeps.
-#ifndef PCS_WS_CONS
-#define PCS_WS_CONS 7       // consumer warps per block (+ 1 producer)
-#endif
-#ifndef PCS_WS_RING
-#define PCS_WS_RING 8       // published units in flight per block
-#endif
-#ifndef PCS_WS_MINB
-#define PCS_WS_MINB 2       // resident blocks per SM the warp-specialised kernel is budgeted for
-#endif
-#ifndef PCS_SET_WS_DEFAULT
-#define PCS_SET_WS_DEFAULT 0  // measured slower than the single-role kernel; PCS_SET_WS=1 enables
-#endif
-constexpr int kWsConsumers = PCS_WS_CONS;
-constexpr int kWsRing = PCS_WS_RING;
-
-template <int L>
-struct WsEntry {
-    SetSlot<L> slot[32];
-    unsigned long long u;   // unit, or ~0 (end of work)
-    int row, nvalid;
-    volatile int state;     // 0 free, 1 full
-    volatile int seq;       // ticket of the unit it holds
-};
-
-template <int L>
-struct WsSmem {
-    WsEntry<L> ring[kWsRing];
-    SetWarpSmem<L> warp[kWsConsumers];
-    int ticket;             // consumer-side ticket counter
-};
-
-// phase 1 of one set (lane-parallel), as in level_set_kernel
-template <int L>
-__device__ __forceinline__ void compute_slot(const LevelArgs& A, int i, int oi, int w, unsigned long long rank,
-                                             SetSlot<L>& sl) {
-    const double* __restrict__ C = A.C;
-    const long long ldc = A.ldc;
-    int pos[L];
-#if PCS_UNRANK_BSEARCH
-    unrank<L>(A.binom, w, rank, pos);
-#else
-    unrank_est<L>(A.binom, w, rank, pos);
-#endif
-    int mem[L];
-    double m2[L * L], minv[L * L], ciS[L], p0[L], h00;
-#pragma unroll
-    for (int a = 0; a < L; ++a) {
-        mem[a] = A.nbr[oi + pos[a]];
-        ciS[a] = __ldg(C + (size_t)i * ldc + mem[a]);
-    }
-#pragma unroll
-    for (int a = 0; a < L; ++a)
-#pragma unroll
-        for (int b = 0; b < L; ++b) m2[a * L + b] = __ldg(C + (size_t)mem[a] * ldc + mem[b]);
-    pinv<L>(m2, minv);
-    p0_terms<L>(minv, ciS, p0, h00);
-#pragma unroll
-    for (int c = 0; c < L; ++c) {
-#pragma unroll
-        for (int k = 0; k < L; ++k) sl.col[c][k] = minv[k * L + c];
-        sl.col[c][L] = ciS[c];
-        sl.col[c][L + 1] = p0[c];
-    }
-#pragma unroll
-    for (int a = 0; a < L; ++a) {
-        sl.pos[a] = pos[a];
-        sl.roff[a] = mem[a] * (int)ldc;
-    }
-    sl.h00 = h00;
-}
-
-template <int L>
-__global__ void __launch_bounds__((kWsConsumers + 1) * 32, PCS_WS_MINB) level_set_ws_kernel(LevelArgs A, int pass,
-                                                                                const unsigned long long* prefix,
-                                                                                unsigned long long u_begin,
-                                                                                unsigned long long u_end) {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    WsSmem<L>& W = *reinterpret_cast<WsSmem<L>*>(smem_raw);
-    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-    unsigned long long* cursor = &A.cnt->units[pass & 1];
-    if (threadIdx.x < kWsRing) W.ring[threadIdx.x].state = 0;
-    if (threadIdx.x == 0) W.ticket = 0;
-    __syncthreads();
-    if (wib == kWsConsumers) {
-        // ---------------- producer
-        unsigned long long pinvs = 0;
-        int row_hint = 0, ends = 0;
-        for (int e = 0; ends < kWsConsumers; ++e) {
-            WsEntry<L>& E = W.ring[e % kWsRing];
-            while (E.state != 0) __nanosleep(64);
-            __threadfence_block();
-            unsigned long long u = 0;
-            if (lane == 0) u = atomicAdd(cursor, 1ull);
-            u = u_begin + __shfl_sync(0xffffffffu, u, 0);
-            if (u >= u_end) {
-                if (lane == 0) E.u = ~0ull;
-                ++ends;
-            } else {
-                const int i = find_row_from(prefix, A.p, u, row_hint);
-                row_hint = i;
-                const unsigned long long t0 = (u - prefix[i]) * kSetBand;
-                const int oi = A.off[i], w = A.off[i + 1] - oi;
-                const int nvalid = (int)min(32ull, A.binom(w, L) - t0);
-                if (lane < nvalid) compute_slot<L>(A, i, oi, w, t0 + lane, E.slot[lane]);
-                if (lane == 0) {
-                    E.u = u;
-                    E.row = i;
-                    E.nvalid = nvalid;
-                    pinvs += nvalid;
-                }
-            }
-            __syncwarp();
-            __threadfence_block();
-            if (lane == 0) {
-                E.seq = e;
-                E.state = 1;
-            }
-            __syncwarp();
-        }
-        if (lane == 0 && pinvs) atomicAdd(&A.cnt->gpu_pinv, pinvs);
-        return;
-    }
-    // ---------------- consumers
-    constexpr int kStage = SetCfg<L>::kStage;
-    SetWarpSmem<L>& S = W.warp[wib];
-    const unsigned long long dirbits = pass == 1 ? (1ull << kDirShift) : 0ull;
-    const unsigned lt_mask = (1u << lane) - 1u;
-    unsigned long long tests = 0, degen = 0;
-    int nan = 0;
-    for (;;) {
-        int t = 0;
-        if (lane == 0) t = atomicAdd(&W.ticket, 1);
-        t = __shfl_sync(0xffffffffu, t, 0);
-        WsEntry<L>& E = W.ring[t % kWsRing];
-        while (!(E.state == 1 && E.seq == t)) __nanosleep(32);
-        __threadfence_block();
-        const unsigned long long u = E.u;
-        if (u == ~0ull) {
-            __syncwarp();
-            if (lane == 0) E.state = 0;
-            break;
-        }
-        const int i = E.row, nvalid = E.nvalid;
-        S.slot[lane] = E.slot[lane];  // lanes >= nvalid copy unused slots (never read)
-        __syncwarp();
-        __threadfence_block();
-        if (lane == 0) E.state = 0;
-        const unsigned long long t0 = (u - prefix[i]) * kSetBand;
-        const int oi = A.off[i], w = A.off[i + 1] - oi, lc = A.lowcnt[i];
-        (void)w;
-        const int qbeg = pass == 2 ? 0 : (pass == 0 ? lc : 0), qend = pass == 2 ? w : (pass == 0 ? w : lc);
-        const unsigned long long K0 = dirbits | t0;
-        // runs of consecutive sets with equal leading L-1 members, live sets (h00 != 0)
-        bool starts = lane == 0;
-        {
-            const int prev = lane > 0 ? lane - 1 : 0;
-#pragma unroll
-            for (int a = 0; a < L - 1; ++a) {
-                const int mine = lane < nvalid ? S.slot[lane].pos[a] : -1;
-                const int theirs = __shfl_sync(0xffffffffu, mine, prev);
-                starts = starts || mine != theirs;
-            }
-        }
-        const unsigned segmask = __ballot_sync(0xffffffffu, starts);
-        const unsigned livemask = __ballot_sync(0xffffffffu, lane < nvalid && S.slot[lane].h00 != 0.0);
-        bool any_live = false;
-        for (int tb = qbeg; tb < qend; tb += kStage) {
-            const int tend = min(tb + kStage, qend);
-            int nlive = 0;
-            {
-                constexpr int NC = kStage / 32;
-                unsigned long long kk[NC];
-                int ee[NC], jj[NC];
-                double cc[NC];
-#pragma unroll
-                for (int c = 0; c < NC; ++c) {
-                    const int q = tb + c * 32 + lane;
-                    kk[c] = 0;
-                    if (q < tend) {
-                        kk[c] = A.kdir[oi + q];
-                        ee[c] = A.eid[oi + q];
-                        jj[c] = A.nbr[oi + q];
-                        cc[c] = A.cnbr[oi + q];
-                    }
-                }
-#pragma unroll
-                for (int c = 0; c < NC; ++c) {
-                    const bool live = kk[c] > (K0 | (tb + c * 32 + lane < lc ? (1ull << kDirShift) : 0ull));
-                    const unsigned bal = __ballot_sync(0xffffffffu, live);
-                    if (live) {
-                        const int at = nlive + __popc(bal & lt_mask);
-                        S.tkey[at] = kk[c];
-                        S.tq[at] = tb + c * 32 + lane;
-                        S.tj[at] = jj[c];
-                        S.te[at] = ee[c];
-                        S.tcij[at] = cc[c];
-                    }
-                    nlive += __popc(bal);
-                }
-            }
-            if (nlive == 0) continue;
-            any_live = true;
-            __syncwarp();
-            const int nt = (nlive + 31) >> 5;
-            if constexpr (SetCfg<L>::NT == 3) {
-                if (nt == 3) set_sweep<L, 3>(A, S, lane, oi, lc, nlive, nvalid, segmask, livemask, K0, tests, degen, nan);
-#if PCS_NT2_SP > 1
-                else if (nt == 2) set_sweep_tsp<L, 2, PCS_NT2_SP>(A, S, lane, oi, lc, nlive, nvalid, segmask, livemask, K0, tests, degen, nan);
-#else
-                else if (nt == 2) set_sweep<L, 2>(A, S, lane, oi, lc, nlive, nvalid, segmask, livemask, K0, tests, degen, nan);
-#endif
-                else set_sweep_tsp<L, 1, PCS_SET_SP>(A, S, lane, oi, lc, nlive, nvalid, segmask, livemask, K0, tests, degen, nan);
-            } else {
-                if (nt == 2) set_sweep<L, 2>(A, S, lane, oi, lc, nlive, nvalid, segmask, livemask, K0, tests, degen, nan);
-                else set_sweep_tsp<L, 1, 2>(A, S, lane, oi, lc, nlive, nvalid, segmask, livemask, K0, tests, degen, nan);
-            }
-            __syncwarp();
-        }
-        if (!any_live && lane == 0) {
-            // no live target at rank t0: none at any later rank of this row either
-            const unsigned long long next_row = prefix[i + 1] - u_begin;
-            atomicMax(cursor, next_row);
-        }
-    }
-    add_counter(&A.cnt->gpu_tests, tests);
-    add_counter(&A.cnt->gpu_exact, tests - degen);
-    if (nan) atomicOr(&A.cnt->err_nan, 1);
-}
-
-// PCS_SET_WS: 1 the warp-specialised kernel for ell = 2, 3; 0 the single-role level_set_kernel
-// (default PCS_SET_WS_DEFAULT)
-static bool set_ws() {
-    static const bool on = [] {
-        const char* e = std::getenv("PCS_SET_WS");
-        return e ? std::atoi(e) != 0 : PCS_SET_WS_DEFAULT != 0;
-    }();
-    return on;
-}
-
-template <int L>
-static int launch_set_ws_L(const LevelArgs& A, int pass, const unsigned long long* prefix, unsigned long long u_begin,
-                           unsigned long long u_end, int num_sms, cudaStream_t s) {
-    const size_t smem = sizeof(WsSmem<L>);
-    if (cudaFuncSetAttribute(level_set_ws_kernel<L>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
-        cudaSuccess)
-        return -2;
-    int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, level_set_ws_kernel<L>, (kWsConsumers + 1) * 32, smem);
-    if (per_sm < 1) per_sm = 1;
-    ++g_kernel_launches;
-    level_set_ws_kernel<L><<<num_sms * per_sm, (kWsConsumers + 1) * 32, smem, s>>>(A, pass, prefix, u_begin, u_end);
-    return 0;
-}
-
 template <int L>
 static int launch_set_L(const LevelArgs& A, int pass, const unsigned long long* prefix, unsigned long long u_begin,
                         unsigned long long u_end, int num_sms, cudaStream_t s) {
@@ -1584,10 +1323,8 @@ static int launch_set_L(const LevelArgs& A, int pass, const unsigned long long* 
 int launch_level_set(const LevelArgs& A, int pass, const unsigned long long* prefix, unsigned long long u_begin,
                      unsigned long long u_end, int num_sms, cudaStream_t s) {
     switch (A.ell) {
-        case 2: return set_ws() ? launch_set_ws_L<2>(A, pass, prefix, u_begin, u_end, num_sms, s)
-                                : launch_set_L<2>(A, pass, prefix, u_begin, u_end, num_sms, s);
-        case 3: return set_ws() ? launch_set_ws_L<3>(A, pass, prefix, u_begin, u_end, num_sms, s)
-                                : launch_set_L<3>(A, pass, prefix, u_begin, u_end, num_sms, s);
+        case 2: return launch_set_L<2>(A, pass, prefix, u_begin, u_end, num_sms, s);
+        case 3: return launch_set_L<3>(A, pass, prefix, u_begin, u_end, num_sms, s);
         case 4: return launch_set_L<4>(A, pass, prefix, u_begin, u_end, num_sms, s);
         case 5: return launch_set_L<5>(A, pass, prefix, u_begin, u_end, num_sms, s);
         case 6: return launch_set_L<6>(A, pass, prefix, u_begin, u_end, num_sms, s);

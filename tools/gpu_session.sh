@@ -100,15 +100,6 @@ for s in $STEPS; do
       timeout 900 ncu --set full --clock-control none --import-source on -k regex:gram_dmma2 -c 1 -f -o $OUT/gram2 \
         python tools/time_corr.py C2 1 > $OUT/ncu_gram2.log 2>&1
       ;;
-    setws)
-      for v in 0 1; do
-        PCS_SET_WS=$v timeout 900 python tools/explore.py C2 set 3 2 >> $OUT/setws_$v.log 2>&1
-        PCS_SET_WS=$v timeout 900 python tools/explore.py C5a set 2 2 >> $OUT/setws_$v.log 2>&1
-      done
-      ;;
-    wsvar)
-      timeout 900 python tools/variants.py run ws7 ws15 ws3 --workload C2 --max-level 3 --repeats 2 > $OUT/wsvar_c2.json 2> $OUT/wsvar.err
-      ;;
     bench)
       timeout 900 python bench.py > $OUT/bench.json 2> $OUT/bench.err
       ;;
