@@ -221,6 +221,11 @@ struct pcs_session {
     int ell = -1;
     bool stopped = false, in_level = false;
     double tau_override = NAN;     // pcs_run_level: the caller's threshold instead of threshold_tau
+    Counters* hCnt = nullptr;      // pinned copy of the level's counters (deferred level end)
+    bool pending_end = false;      // run_session: the level's counters are in flight to hCnt
+    double pending_t0 = 0.0;
+    int pending_ell = 0;
+    bool pending_timing = false;
     bool level0_and = false;       // pcs_run_level at ell = 0: the input graph may be incomplete
     int stop_reason = PCS_STOP_MAX_DEGREE;
     SnapInfo info{};
@@ -233,6 +238,28 @@ struct pcs_session {
 };
 
 namespace {
+
+// Pinned host slots for the deferred counter copies, recycled across sessions (cudaMallocHost costs
+// milliseconds; a run creates and frees a session).
+static std::mutex g_pinned_mu;
+static std::vector<Counters*> g_pinned_free;
+static Counters* pinned_counters() {
+    {
+        std::lock_guard<std::mutex> g(g_pinned_mu);
+        if (!g_pinned_free.empty()) {
+            Counters* c = g_pinned_free.back();
+            g_pinned_free.pop_back();
+            return c;
+        }
+    }
+    Counters* c = nullptr;
+    return cudaMallocHost(reinterpret_cast<void**>(&c), sizeof(Counters)) == cudaSuccess ? c : nullptr;
+}
+static void pinned_counters_release(Counters* c) {
+    if (!c) return;
+    std::lock_guard<std::mutex> g(g_pinned_mu);
+    g_pinned_free.push_back(c);
+}
 
 void free_session(pcs_session* s) {
     if (!s) return;
@@ -252,6 +279,7 @@ void free_session(pcs_session* s) {
     rel(s->dShardCost);
     rel(s->dBounds);
     if (s->st) cudaStreamSynchronize(s->st);
+    pinned_counters_release(s->hCnt);
     if (s->ev_begin) cudaEventDestroy(s->ev_begin);
     if (s->ev_end) cudaEventDestroy(s->ev_end);
     if (s->ev_k0) cudaEventDestroy(s->ev_k0);
@@ -547,22 +575,25 @@ pcs_status pcs_session_create_device(const double* d_c, int64_t ldc, int32_t p, 
     return PCS_OK;
 }
 
+static pcs_status finalize_pending(pcs_session* s);
+
+
 pcs_status pcs_session_level_begin(pcs_session* s, int32_t* running, int32_t* ell_out, int64_t* num_keys) {
     if (!s) return fail(PCS_EINVAL, "null session");
     CUDA_TRY(cudaSetDevice(s->device));
     *running = 0;
     *num_keys = 0;
-    if (s->stopped) { *ell_out = s->ell; return PCS_OK; }
+    if (s->stopped) { *ell_out = s->ell; return finalize_pending(s); }
     if (s->in_level) return fail(PCS_EINVAL, "level already started");
     const int ell = s->ell + 1;
     *ell_out = ell;
-    if (s->cfg.max_level >= 0 && ell > s->cfg.max_level) { stop(s, PCS_STOP_LEVEL_CAP); return PCS_OK; }
+    if (s->cfg.max_level >= 0 && ell > s->cfg.max_level) { stop(s, PCS_STOP_LEVEL_CAP); return finalize_pending(s); }
     double tau;
     pcs_status st = PCS_OK;
     if (!std::isnan(s->tau_override)) tau = s->tau_override;
     else {
         st = threshold_tau(s->cfg.alpha, s->m, ell, &tau);
-        if (st == PCS_ELEVEL) { stop(s, PCS_STOP_SAMPLE_SIZE); return PCS_OK; }
+        if (st == PCS_ELEVEL) { stop(s, PCS_STOP_SAMPLE_SIZE); return finalize_pending(s); }
         if (st) return st;
     }
     s->ell = ell;
@@ -585,6 +616,7 @@ pcs_status pcs_session_level_begin(pcs_session* s, int32_t* running, int32_t* el
     launch_snapshot_scan(s->dDeg, s->dLow, s->p, s->dOff, s->dUp, s->dInfo, s->st);
     CUDA_TRY(cudaMemcpyAsync(&s->info, s->dInfo, sizeof(SnapInfo), cudaMemcpyDeviceToHost, s->st));
     CUDA_TRY(cudaStreamSynchronize(s->st));
+    if ((st = finalize_pending(s))) return st;  // the previous level's statistics (record pool offset)
     const int maxw = s->info.max_width;
     if (maxw - 1 < ell) {  // skeleton.hpp:370-373 (level not recorded)
         s->ell = ell - 1;
@@ -729,13 +761,14 @@ pcs_status pcs_session_level_pass(pcs_session* s, int32_t pass) {
             u0 = b[0];
             u1 = b[1];
         } else {
+            // the kernels read the unit total (prefix[p]) on the device: no host round trip
             launch_row_work(A, kpass, s->cfg.variant, 0, s->p, s->dPrefix, s->st);
-            CUDA_TRY(cudaMemcpyAsync(&u1, s->dPrefix + s->p, sizeof(u1), cudaMemcpyDeviceToHost, s->st));
-            CUDA_TRY(cudaStreamSynchronize(s->st));
+            u1 = ~0ull;
         }
         if (u1 > u0) {
             if (s->ell == 1) {
-                launch_level1(A, pass, s->dPrefix, u0, u1, s->st);
+                // tiles of 128 targets: at most e_dir / 128 + p of them
+                launch_level1(A, pass, s->dPrefix, u0, u1, (unsigned long long)(s->info.e_dir / 128 + s->p), s->st);
             } else if (s->ell > kMaxTemplLevel) {
                 CUDA_TRY(cudaMemsetAsync(&s->dCnt->units[pass], 0, sizeof(unsigned long long), s->st));
                 if (launch_level_set_rt(A, pass, s->dPrefix, u0, u1, s->num_sms, s->dScratch, s->st))
@@ -795,20 +828,14 @@ pcs_status pcs_session_keys(pcs_session* s, void** device_ptr, int64_t* count) {
     return PCS_OK;
 }
 
-pcs_status pcs_session_level_end(pcs_session* s) {
-    if (!s || !s->in_level) return fail(PCS_EINVAL, "no level in progress");
-    CUDA_TRY(cudaSetDevice(s->device));
-    LevelArgs A = level_args(s);
-    if (s->ell >= 1) launch_commit(A, s->dAdj, s->W, s->info.e_und, s->dRec + s->recUsed, s->st);
-    Counters c{};
-    CUDA_TRY(cudaMemcpyAsync(&c, s->dCnt, sizeof(Counters), cudaMemcpyDeviceToHost, s->st));
-    CUDA_TRY(cudaStreamSynchronize(s->st));
+// LevelStats from the level's counters (after the stream has passed the counter copy)
+static pcs_status level_stats_from(pcs_session* s, const Counters& c, double t_level, int ell, bool timing) {
     CUDA_TRY(cudaGetLastError());
     pcs_status st = check_level_errors(s, c);
     if (st) return st;
     pcs_level_stats L{};
-    L.level = s->ell;
-    if (s->ell == 0) {
+    L.level = ell;
+    if (ell == 0) {
         const unsigned long long p = (unsigned long long)s->p;
         L.ci_tests = p * (p - 1) / 2;  // skeleton.hpp:274-276
         L.pseudo_inverses = 0;
@@ -821,30 +848,64 @@ pcs_status pcs_session_level_end(pcs_session* s) {
         L.device_exact_tests = c.gpu_exact;
         L.device_near_threshold = c.near;
         if (c.rec_count) {
-            s->recUsed += (long long)c.rec_count * (3 + s->ell);
+            s->recUsed += (long long)c.rec_count * (3 + ell);
         }
     }
     L.edges_removed = c.removed;
-    if (s->kernel_timing) {
+    if (timing) {
         float ms = 0.f;
         cudaEventElapsedTime(&ms, s->ev_k0, s->ev_k1);
         L.kernel_ms = ms;
     }
-    L.elapsed_s = now_s() - s->t_level;
+    L.elapsed_s = now_s() - t_level;
     if (c.dbg[0])
-        trace("level %d filter: %llu steps, %llu candidate tests, %llu steps with a candidate", s->ell,
+        trace("level %d filter: %llu steps, %llu candidate tests, %llu steps with a candidate", ell,
               (unsigned long long)c.dbg[0], (unsigned long long)c.dbg[1], (unsigned long long)c.dbg[2]);
     trace("level %d: %.3f ms host (kernels %.3f ms), %llu serial / %llu device tests, %llu removed", L.level,
           L.elapsed_s * 1e3, L.kernel_ms, (unsigned long long)L.ci_tests, (unsigned long long)L.device_ci_tests,
           (unsigned long long)L.edges_removed);
     s->levels.push_back(L);
-    s->in_level = false;
     return PCS_OK;
 }
+
+// the deferred level end of run_session: the counters were copied to pinned memory asynchronously;
+// this runs after the stream's next synchronisation (level_begin's snapshot summary or finish)
+static pcs_status finalize_pending(pcs_session* s) {
+    if (!s->pending_end) return PCS_OK;
+    CUDA_TRY(cudaStreamSynchronize(s->st));  // usually already passed
+    s->pending_end = false;
+    return level_stats_from(s, *s->hCnt, s->pending_t0, s->pending_ell, s->pending_timing);
+}
+
+// deferred = true (run_session only): commit + counter copy are enqueued and the level's statistics are
+// read at the next synchronisation point, so a level costs one host round trip (the snapshot summary)
+static pcs_status level_end_impl(pcs_session* s, bool deferred) {
+    if (!s || !s->in_level) return fail(PCS_EINVAL, "no level in progress");
+    CUDA_TRY(cudaSetDevice(s->device));
+    LevelArgs A = level_args(s);
+    if (s->ell >= 1) launch_commit(A, s->dAdj, s->W, s->info.e_und, s->dRec + s->recUsed, s->st);
+    s->in_level = false;
+    if (deferred) {
+        if (!s->hCnt && !(s->hCnt = pinned_counters())) return fail(PCS_ENOMEM, "pinned host memory");
+        CUDA_TRY(cudaMemcpyAsync(s->hCnt, s->dCnt, sizeof(Counters), cudaMemcpyDeviceToHost, s->st));
+        s->pending_end = true;
+        s->pending_t0 = s->t_level;
+        s->pending_ell = s->ell;
+        s->pending_timing = s->kernel_timing;
+        return PCS_OK;
+    }
+    Counters c{};
+    CUDA_TRY(cudaMemcpyAsync(&c, s->dCnt, sizeof(Counters), cudaMemcpyDeviceToHost, s->st));
+    CUDA_TRY(cudaStreamSynchronize(s->st));
+    return level_stats_from(s, c, s->t_level, s->ell, s->kernel_timing);
+}
+
+pcs_status pcs_session_level_end(pcs_session* s) { return level_end_impl(s, false); }
 
 pcs_status pcs_session_finish(pcs_session* s, pcs_result** out) {
     if (!s) return fail(PCS_EINVAL, "null session");
     CUDA_TRY(cudaSetDevice(s->device));
+    if (pcs_status st = finalize_pending(s)) return st;
     auto* r = new pcs_result();
     r->p = s->p;
     r->W = s->W;
@@ -883,7 +944,7 @@ static pcs_status run_session(pcs_session* s, pcs_result** out) {
         if ((st = pcs_session_level_pass(s, 1))) return st;
         tp += now_s() - t;
         t = now_s();
-        if ((st = pcs_session_level_end(s))) return st;
+        if ((st = level_end_impl(s, true))) return st;
         te += now_s() - t;
     }
     const double t = now_s();

@@ -232,6 +232,7 @@ __global__ void snapshot_scan_kernel(const int32_t* __restrict__ deg, const int3
         info->e_dir = s1[t];
         info->e_und = s2[t];
         info->max_width = smax[t];
+        info->pad = 0;  // the whole struct is copied to the host (compute-sanitizer initcheck)
     }
 }
 
@@ -466,13 +467,18 @@ void launch_edge_bounds(const LevelArgs& A, int pass, long long E, unsigned long
 constexpr int kL1Chunk = 1024;
 constexpr int kL1Unroll = 8;
 
+// Grid-stride over tiles [tile_base, min(tile_end, prefix[p])): the tile count is read on the device,
+// so the host launches without waiting for the prefix scan.
 __global__ void __launch_bounds__(kL1Threads) level1_kernel(LevelArgs A, int pass, const unsigned long long* prefix,
-                                                            unsigned long long tile_base) {
+                                                            unsigned long long tile_base, unsigned long long tile_end) {
     // per candidate set k of the chunk: the row offset k * ldc of C(k, .) and (c_ik, 1 - c_ik^2), so a
     // test costs one LDS, one LDS.128, one coalesced gather C(k, j) and its FP64 arithmetic
     __shared__ int s_koff[kL1Chunk + kL1Unroll];
     __shared__ double2 s_ch[kL1Chunk + kL1Unroll];
-    const unsigned long long tile = tile_base + blockIdx.x;
+    const unsigned long long t_end = min(tile_end, prefix[A.p]);
+    unsigned long long tests = 0;
+    int nan = 0;
+    for (unsigned long long tile = tile_base + blockIdx.x; tile < t_end; tile += gridDim.x) {
     const int i = find_row(prefix, A.p, tile);
     const int t_in_row = (int)(tile - prefix[i]);
     const int oi = A.off[i], w = A.off[i + 1] - oi, lc = A.lowcnt[i];
@@ -491,8 +497,6 @@ __global__ void __launch_bounds__(kL1Threads) level1_kernel(LevelArgs A, int pas
     }
     const unsigned long long dirbits = (unsigned long long)pass << kDirShift;
     const double hi2 = A.th.hi2;
-    unsigned long long tests = 0;
-    int nan = 0;
     const double* __restrict__ Cj = C + j;
     for (int s0 = 0; s0 < w; s0 += kL1Chunk) {
         if (!__syncthreads_or(active)) break;
@@ -551,20 +555,22 @@ __global__ void __launch_bounds__(kL1Threads) level1_kernel(LevelArgs A, int pas
         }
         __syncthreads();
     }
+    __syncthreads();  // the next tile re-stages s_koff / s_ch
+    }
     add_counter(&A.cnt->gpu_tests, tests);
     add_counter(&A.cnt->gpu_exact, tests);
     if (nan) atomicOr(&A.cnt->err_nan, 1);
 }
 
+// tiles [u_begin, min(u_end, prefix[p])); `bound` is a host upper bound of the tile count (grid size)
 void launch_level1(const LevelArgs& A, int pass, const unsigned long long* prefix, unsigned long long u_begin,
-                   unsigned long long u_end, cudaStream_t s) {
-    // one block per target tile in [u_begin, u_end); sliced to respect the grid limit
-    const unsigned long long kMaxGrid = 1ull << 30;
-    for (unsigned long long base = u_begin; base < u_end; base += kMaxGrid) {
-        const unsigned long long n = u_end - base < kMaxGrid ? u_end - base : kMaxGrid;
-        ++g_kernel_launches;
-        level1_kernel<<<(unsigned)n, kL1Threads, 0, s>>>(A, pass, prefix, base);
-    }
+                   unsigned long long u_end, unsigned long long bound, cudaStream_t s) {
+    unsigned long long n = bound;
+    if (u_end != ~0ull && u_end - u_begin < n) n = u_end - u_begin;
+    if (n > 148ull * 16) n = 148ull * 16;
+    if (n == 0) return;
+    ++g_kernel_launches;
+    level1_kernel<<<(unsigned)n, kL1Threads, 0, s>>>(A, pass, prefix, u_begin, u_end);
 }
 
 // =========================================================== ell >= 2, cuPC-S
@@ -1145,6 +1151,7 @@ __global__ void __launch_bounds__(kSetWarps * 32, PCS_SET_MINB) level_set_kernel
     unsigned long long tests = 0, pinvs = 0, degen = 0;
     int nan = 0;
     unsigned long long* cursor = &A.cnt->units[pass & 1];
+    u_end = min(u_end, prefix[A.p]);
     int row_hint = 0;
     // the next unit is grabbed one unit ahead (lane 0's atomic result is only read at the top of the
     // next iteration), so the cursor round trip overlaps the current unit's work
@@ -1461,6 +1468,7 @@ __global__ void __launch_bounds__(128) level_set_rt_kernel(LevelArgs A, int pass
     unsigned long long tests = 0, pinvs = 0, degen = 0;
     int nan = 0;
     unsigned long long* cursor = &A.cnt->units[pass];
+    u_end = min(u_end, prefix[A.p]);
     for (;;) {
         unsigned long long u = 0;
         if (lane == 0) u = u_begin + atomicAdd(cursor, 1ull);

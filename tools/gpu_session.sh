@@ -100,6 +100,18 @@ for s in $STEPS; do
       timeout 900 ncu --set full --clock-control none --import-source on -k regex:gram_dmma2 -c 1 -f -o $OUT/gram2 \
         python tools/time_corr.py C2 1 > $OUT/ncu_gram2.log 2>&1
       ;;
+    sanitize)
+      for tool in memcheck racecheck synccheck initcheck; do
+        timeout 1200 compute-sanitizer --tool $tool --error-exitcode 9 python tools/explore.py C1 set,edge -1 \
+          > $OUT/sanitizer_${tool}_C1.log 2>&1; echo "rc=$?" >> $OUT/sanitizer_${tool}_C1.log
+        timeout 1800 compute-sanitizer --tool $tool --error-exitcode 9 python tools/explore.py C3 set,edge -1 \
+          > $OUT/sanitizer_${tool}_C3.log 2>&1; echo "rc=$?" >> $OUT/sanitizer_${tool}_C3.log
+      done
+      PCS_L1_TILE=1 timeout 1800 compute-sanitizer --tool racecheck --error-exitcode 9 python tools/explore.py C3 set 1 \
+        > $OUT/sanitizer_racecheck_C3_l1tile.log 2>&1; echo "rc=$?" >> $OUT/sanitizer_racecheck_C3_l1tile.log
+      PCS_L1_TILE=1 timeout 1800 compute-sanitizer --tool synccheck --error-exitcode 9 python tools/explore.py C3 set 1 \
+        > $OUT/sanitizer_synccheck_C3_l1tile.log 2>&1; echo "rc=$?" >> $OUT/sanitizer_synccheck_C3_l1tile.log
+      ;;
     bench)
       timeout 900 python bench.py > $OUT/bench.json 2> $OUT/bench.err
       ;;

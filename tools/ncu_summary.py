@@ -13,13 +13,14 @@ import sys
 from collections import defaultdict
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-rnd = int(sys.argv[1]) if len(sys.argv) > 1 else 1
+arg = sys.argv[1] if len(sys.argv) > 1 else "1"
+rnd = int(arg) if arg.isdigit() else 0
 launches = sys.argv[2] if len(sys.argv) > 2 else os.path.join(ROOT, "gpurun_out", "launches.csv")
 rep = sys.argv[3] if len(sys.argv) > 3 else os.path.join(ROOT, "gpurun_out", "top.ncu-rep")
 bench = sys.argv[4] if len(sys.argv) > 4 else os.path.join(ROOT, "gpurun_out", "bench.json")
 out = os.path.join(ROOT, "profiles")
 os.makedirs(out, exist_ok=True)
-tag = f"r{rnd:02d}"
+tag = f"r{rnd:02d}" if arg.isdigit() else arg  # e.g. r2 -> profiles/r2_launches.md
 
 # ---- launch list
 rows = [r for r in csv.reader(open(launches)) if len(r) > 10]
