@@ -160,6 +160,17 @@ pcs_status pcs_pseudo_inverse_batch(const double* a, int32_t ell, int64_t n, dou
    j causes i, j < i); sample_linear_gaussian (datagen.hpp:62-82) -> x m x n column-major. */
 pcs_status pcs_random_dag(int32_t n, double density, uint64_t seed, double* weights);
 pcs_status pcs_sample_linear_gaussian(const double* weights, int32_t n, int32_t m, uint64_t seed, double* x);
+/* The reference generator's noise stream (rng.hpp: xoshiro256++ / Marsaglia polar, one normal per
+   (sample, variable) in sample-major order): the first `count` normals of Xoshiro256PlusPlus(seed),
+   normal n stored at out[(n % p) * m + n / p], generated in jump-ahead chunks on the host threads
+   (GF(2) jump matrix; bit-identical to the sequential stream) */
+pcs_status pcs_noise_stream(uint64_t seed, int64_t count, int32_t p, int32_t m, double* out);
+/* sample_linear_gaussian (datagen.hpp:62-82) into device memory d_x (m x n column-major): the noise
+   stream above, then the structural equations on the device (thread per sample, parents ascending);
+   rescaled != 0: pcs_sample_linear_gaussian_rescaled's overflow-safe variant (cooperative grid;
+   log_scale: host array of n, may be null).  Bit-identical to the host generators. */
+pcs_status pcs_sample_linear_gaussian_device(const double* weights, int32_t n, int32_t m, uint64_t seed,
+                                             int32_t rescaled, double* d_x, double* log_scale, uint64_t stream);
 /* Overflow-safe sample_linear_gaussian for the scaling shapes (no reference counterpart):
  * same noise stream, every variable scaled to unit RMS, log_scale[n] = log of the reference variable's RMS,
  * so x_ref[i] = x[i] * exp(log_scale[i]) and the correlation matrix is the reference generator's. */

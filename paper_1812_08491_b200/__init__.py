@@ -135,6 +135,9 @@ def library():
     L.pcs_result_record_ints.restype = ct.c_int64
     L.pcs_result_records.argtypes = [vp, ip]
     L.pcs_correlation_device.argtypes = [vp, ct.c_int32, ct.c_int32, vp, ct.c_int64, ct.c_uint64, ip]
+    L.pcs_noise_stream.argtypes = [ct.c_uint64, ct.c_int64, ct.c_int32, ct.c_int32, dp]
+    L.pcs_sample_linear_gaussian_device.argtypes = [dp, ct.c_int32, ct.c_int32, ct.c_uint64, ct.c_int32, vp, dp,
+                                                    ct.c_uint64]
     L.pcs_run_level.argtypes = [dp, ct.c_int32, ct.c_int32, ct.c_double, ct.POINTER(_Config), ct.POINTER(ct.c_uint8),
                                 ct.POINTER(vp)]
     L.pcs_correlation_device_rows.argtypes = [vp, ct.c_int32, ct.c_int32, ct.c_int32, ct.c_int32, vp, ct.c_int64,
@@ -500,6 +503,30 @@ def run_level(c, graph_cells, ell: int, tau: float, cfg: Optional[SkeletonConfig
         got = res.sepsets.find(int(i), int(j))
         sep[(int(i), int(j))] = tuple(got) if (got is not None and ell > 0) else ()
     return g, lv, sep
+
+
+def noise_stream(seed: int, count: int, p: int, m: int) -> np.ndarray:
+    """The reference generator's first `count` normals (rng.hpp), jump-ahead parallel on the host,
+    as a (p, m) variable-major array (draw n -> [n % p, n / p])."""
+    out = np.zeros((p, m), np.float64)
+    rc = library().pcs_noise_stream(seed, count, p, m, _dp(out))
+    if rc:
+        _raise(rc)
+    return out
+
+
+def sample_linear_gaussian_device(weights: np.ndarray, m: int, seed: int, x_ptr: int, rescaled: bool = False,
+                                  stream: int = 0):
+    """sample_linear_gaussian (or the rescaled variant) into device memory at x_ptr (m x n column-major,
+    i.e. a (n, m) row-major float64 buffer); returns log_scale for the rescaled variant."""
+    w = np.ascontiguousarray(weights, np.float64)
+    n = w.shape[0]
+    ls = np.zeros(n, np.float64)
+    rc = library().pcs_sample_linear_gaussian_device(_dp(w), n, m, seed, 1 if rescaled else 0, ct.c_void_p(x_ptr),
+                                                     _dp(ls), stream)
+    if rc:
+        _raise(rc)
+    return ls if rescaled else None
 
 
 def correlation_device_rows(x_ptr: int, m: int, p: int, row_begin: int, row_end: int, c_ptr: int, ldc: int,

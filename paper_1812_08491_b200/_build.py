@@ -24,6 +24,7 @@ COMMON = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xptxas", "-
 UNITS = {
     "level.cu": ["-fmad=false"],
     "level1t.cu": ["-fmad=false"],
+    "datagen_dev.cu": ["-fmad=false"],
     "corr.cu": [],
     "host.cu": ["-Xcompiler", "-ffp-contract=off"],
     "probe.cu": [],

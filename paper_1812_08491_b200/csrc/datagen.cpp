@@ -9,6 +9,9 @@
 // the dense inner loop of datagen.hpp:75-78, so the sums round identically.
 // Built with -ffp-contract=off (no FMA), like the reference's Release build.
 #include <algorithm>
+#include <array>
+#include <atomic>
+#include <mutex>
 #include <cmath>
 #include <cstdint>
 #include <cstring>
@@ -61,9 +64,133 @@ struct Xoshiro {
     }
 };
 
+// ---- the noise stream in parallel ("jump-ahead per block keeps seed
+// determinism").  xoshiro256++'s state update is linear over GF(2): one step is a 256 x 256 bit matrix
+// M, and J = M^(2^kChunkLog) jumps a whole chunk of outputs.  The polar method consumes exactly two
+// uniforms per attempt, so attempts sit at fixed even offsets of the raw stream; chunks (an even number
+// of outputs) are generated independently, their accepted attempts counted, prefix-summed, and
+// regenerated into place: normal 2a / 2a+1 of the stream = u / v times the scale of the a-th accepted
+// attempt, exactly the sequential generator's values (same uniforms, same sqrt(-2 log(s) / s) with
+// this host's libm, as the reference).
+constexpr int kChunkLog = 16;  // 65536 outputs = 32768 attempts per chunk
+
+struct M256 {
+    uint64_t c[256][4];  // column k = M e_k
+};
+
+void xo_advance(uint64_t s[4]) {
+    const uint64_t t = s[1] << 17;
+    s[2] ^= s[0];
+    s[3] ^= s[1];
+    s[1] ^= s[2];
+    s[0] ^= s[3];
+    s[2] ^= t;
+    s[3] = Xoshiro::rotl(s[3], 45);
+}
+
+void mat_vec(const M256& M, const uint64_t in[4], uint64_t out[4]) {
+    uint64_t o[4] = {0, 0, 0, 0};
+    for (int k = 0; k < 256; ++k)
+        if ((in[k >> 6] >> (k & 63)) & 1u)
+            for (int w = 0; w < 4; ++w) o[w] ^= M.c[k][w];
+    std::memcpy(out, o, sizeof o);
+}
+
+const M256& chunk_jump() {
+    static M256 J;
+    static bool built = false;
+    static std::mutex mu;
+    std::lock_guard<std::mutex> g(mu);
+    if (built) return J;
+    M256 A, B;
+    for (int k = 0; k < 256; ++k) {
+        uint64_t e[4] = {0, 0, 0, 0};
+        e[k >> 6] = 1ull << (k & 63);
+        xo_advance(e);
+        std::memcpy(A.c[k], e, sizeof e);
+    }
+    for (int sq = 0; sq < kChunkLog; ++sq) {  // A <- A^2
+        for (int k = 0; k < 256; ++k) mat_vec(A, A.c[k], B.c[k]);
+        A = B;
+    }
+    J = A;
+    built = true;
+    return J;
+}
+
+// the first `count` normals of Xoshiro(seed).normal(), normal n written to out[(n % p) * m + n / p]
+// (variable-major: the n-th draw is sample n / p, variable n % p), on up to 16 host threads
+void noise_stream(uint64_t seed, int64_t count, int p, int m, double* out) {
+    const int64_t attempts_needed = (count + 1) / 2;
+    const int64_t per_chunk = 1ll << (kChunkLog - 1);
+    const M256& J = chunk_jump();
+    std::vector<std::array<uint64_t, 4>> state;
+    std::vector<int64_t> accepted;
+    Xoshiro g0(seed);
+    std::array<uint64_t, 4> cur{g0.s[0], g0.s[1], g0.s[2], g0.s[3]};
+    unsigned nt = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+    auto run = [&](size_t c0, size_t c1, auto&& body) {
+        std::vector<std::thread> th;
+        std::atomic<size_t> next{c0};
+        for (unsigned t = 0; t < nt; ++t)
+            th.emplace_back([&] {
+                for (size_t c; (c = next.fetch_add(1)) < c1;) body(c);
+            });
+        for (auto& x : th) x.join();
+    };
+    int64_t total = 0;
+    while (total < attempts_needed) {  // extend the chunk list until enough attempts are accepted
+        const size_t c0 = state.size();
+        const int64_t more = (int64_t)((double)(attempts_needed - total) / 0.78 / per_chunk) + 1;
+        for (int64_t k = 0; k < more; ++k) {
+            state.push_back(cur);
+            uint64_t nx[4];
+            mat_vec(J, cur.data(), nx);
+            cur = {nx[0], nx[1], nx[2], nx[3]};
+        }
+        accepted.resize(state.size());
+        run(c0, state.size(), [&](size_t c) {
+            Xoshiro g(0);
+            std::memcpy(g.s, state[c].data(), sizeof g.s);
+            int64_t n = 0;
+            for (int64_t a = 0; a < per_chunk; ++a) {
+                const double u = 2.0 * g.uniform01() - 1.0, v = 2.0 * g.uniform01() - 1.0;
+                const double q = u * u + v * v;
+                n += !(q >= 1.0 || q == 0.0);
+            }
+            accepted[c] = n;
+        });
+        for (size_t c = c0; c < state.size(); ++c) total += accepted[c];
+    }
+    std::vector<int64_t> base(state.size() + 1, 0);
+    for (size_t c = 0; c < state.size(); ++c) base[c + 1] = base[c] + accepted[c];
+    run(0, state.size(), [&](size_t c) {
+        if (base[c] >= attempts_needed) return;
+        Xoshiro g(0);
+        std::memcpy(g.s, state[c].data(), sizeof g.s);
+        int64_t a = base[c];
+        for (int64_t k = 0; k < per_chunk && a < attempts_needed; ++k) {
+            const double u = 2.0 * g.uniform01() - 1.0, v = 2.0 * g.uniform01() - 1.0;
+            const double q = u * u + v * v;
+            if (q >= 1.0 || q == 0.0) continue;
+            const double scale = std::sqrt(-2.0 * std::log(q) / q);  // rng.hpp:68
+            const int64_t n0 = 2 * a;
+            out[(size_t)(n0 % p) * m + (size_t)(n0 / p)] = u * scale;
+            if (n0 + 1 < count) out[(size_t)((n0 + 1) % p) * m + (size_t)((n0 + 1) / p)] = v * scale;
+            ++a;
+        }
+    });
+}
+
 }  // namespace
 
 extern "C" {
+
+pcs_status pcs_noise_stream(uint64_t seed, int64_t count, int32_t p, int32_t m, double* out) {
+    if (count < 0 || p < 1 || m < 1 || (int64_t)p * m < count) return PCS_EINVAL;
+    noise_stream(seed, count, p, m, out);
+    return PCS_OK;
+}
 
 pcs_status pcs_random_dag(int32_t n, double density, uint64_t seed, double* weights) {
     if (n < 2 || !(density > 0.0 && density < 1.0)) return PCS_EINVAL;
@@ -91,10 +218,12 @@ pcs_status pcs_sample_linear_gaussian(const double* weights, int32_t n, int32_t 
         }
     }
     start[n] = (int64_t)par.size();
-    Xoshiro g(seed);
+    // the noise draws first (the stream's sample-major order, jump-ahead parallel), then the equations
+    // sample by sample in the reference's order (datagen.hpp:72-78): the same values as interleaving
+    noise_stream(seed, (int64_t)n * m, n, m, x);
     for (int r = 0; r < m; ++r)
         for (int i = 0; i < n; ++i) {
-            double value = g.normal();
+            double value = x[(size_t)i * m + r];
             for (int64_t e = start[i]; e < start[i + 1]; ++e) value += pw[e] * x[(size_t)par[e] * m + r];
             x[(size_t)i * m + r] = value;
         }
@@ -127,9 +256,7 @@ pcs_status pcs_sample_linear_gaussian_rescaled(const double* weights, int32_t n,
     }
     start[n] = (int64_t)par.size();
     {  // the reference's noise stream, one normal per (sample, variable) in sample-major order
-        Xoshiro g(seed);
-        for (int r = 0; r < m; ++r)
-            for (int i = 0; i < n; ++i) x[(size_t)i * m + r] = g.normal();
+        noise_stream(seed, (int64_t)n * m, n, m, x);
     }
     // Scales are carried as mant * 2^exp (mant in [0.5, 1), frexp) and combined with ldexp and IEEE
     // mul/div/sqrt only -- no exp/log, whose last bits differ between libm builds -- and the sum of
