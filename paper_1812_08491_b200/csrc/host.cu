@@ -734,23 +734,14 @@ pcs_status pcs_session_level_pass(pcs_session* s, int32_t pass) {
         if (!s->dBounds && (st = realloc_dev(s, &s->dBounds, 2))) return st;
     }
     if (level1_tile(s)) {
-        int r0 = 0, r1 = s->p;
-        if (nsh > 1) {  // cost-weighted contiguous row range (the level1_kernel split, mapped to rows)
-            unsigned long long b[2] = {0, 0};
-            launch_row_work_sharded(A, 2, s->cfg.variant, s->dPrefix, s->dShardCost, shard, nsh, s->dBounds, s->st);
-            std::vector<unsigned long long> pre((size_t)s->p + 1);
-            CUDA_TRY(cudaMemcpyAsync(b, s->dBounds, sizeof(b), cudaMemcpyDeviceToHost, s->st));
-            CUDA_TRY(cudaMemcpyAsync(pre.data(), s->dPrefix, sizeof(unsigned long long) * pre.size(),
-                                     cudaMemcpyDeviceToHost, s->st));
-            CUDA_TRY(cudaStreamSynchronize(s->st));
-            auto row_of = [&](unsigned long long u) {  // first row whose units start at or after u
-                return (int)(std::lower_bound(pre.begin(), pre.end() - 1, u) - pre.begin());
-            };
-            r0 = shard == 0 ? 0 : row_of(b[0]);
-            r1 = shard == nsh - 1 ? s->p : row_of(b[1]);
-        }
-        if (launch_level1_tile(A, s->dAdj, s->W, r0, r1, s->st))
+        // multi-GPU: cyclic 32-row blocks (no host round trip for bounds)
+        if (launch_level1_tile(A, s->dAdj, s->W, shard, nsh, s->st))
             return fail(PCS_ECUDA, "level-1 tile kernel: tensor map / launch failed");
+    } else if (s->ell == 1) {
+        // level1_kernel: cyclic tiles of 128 targets over the ranks; the tile total stays on the device
+        launch_row_work(A, pass, s->cfg.variant, 0, s->p, s->dPrefix, s->st);
+        launch_level1(A, pass, s->dPrefix, 0, ~0ull, (unsigned long long)(s->info.e_dir / 128 + s->p), shard, nsh,
+                      s->st);
     } else if (s->cfg.variant == PCS_VARIANT_SET || s->ell == 1 || s->ell > kMaxTemplLevel) {
         unsigned long long u0 = 0, u1 = 0;
         if (nsh > 1) {
@@ -766,10 +757,7 @@ pcs_status pcs_session_level_pass(pcs_session* s, int32_t pass) {
             u1 = ~0ull;
         }
         if (u1 > u0) {
-            if (s->ell == 1) {
-                // tiles of 128 targets: at most e_dir / 128 + p of them
-                launch_level1(A, pass, s->dPrefix, u0, u1, (unsigned long long)(s->info.e_dir / 128 + s->p), s->st);
-            } else if (s->ell > kMaxTemplLevel) {
+            if (s->ell > kMaxTemplLevel) {
                 CUDA_TRY(cudaMemsetAsync(&s->dCnt->units[pass], 0, sizeof(unsigned long long), s->st));
                 if (launch_level_set_rt(A, pass, s->dPrefix, u0, u1, s->num_sms, s->dScratch, s->st))
                     return fail(PCS_EUNSUPPORTED, "level not supported by the generic set kernel");

@@ -469,8 +469,11 @@ constexpr int kL1Unroll = 8;
 
 // Grid-stride over tiles [tile_base, min(tile_end, prefix[p])): the tile count is read on the device,
 // so the host launches without waiting for the prefix scan.
+// Multi-GPU: shard `shard` of `nsh` takes every nsh-th tile (cyclic: a row's tiles and neighbouring rows
+// spread over the ranks, whose early exits then balance statistically).
 __global__ void __launch_bounds__(kL1Threads) level1_kernel(LevelArgs A, int pass, const unsigned long long* prefix,
-                                                            unsigned long long tile_base, unsigned long long tile_end) {
+                                                            unsigned long long tile_base, unsigned long long tile_end,
+                                                            int shard, int nsh) {
     // per candidate set k of the chunk: the row offset k * ldc of C(k, .) and (c_ik, 1 - c_ik^2), so a
     // test costs one LDS, one LDS.128, one coalesced gather C(k, j) and its FP64 arithmetic
     __shared__ int s_koff[kL1Chunk + kL1Unroll];
@@ -478,7 +481,8 @@ __global__ void __launch_bounds__(kL1Threads) level1_kernel(LevelArgs A, int pas
     const unsigned long long t_end = min(tile_end, prefix[A.p]);
     unsigned long long tests = 0;
     int nan = 0;
-    for (unsigned long long tile = tile_base + blockIdx.x; tile < t_end; tile += gridDim.x) {
+    for (unsigned long long tile = tile_base + shard + (unsigned long long)blockIdx.x * nsh; tile < t_end;
+         tile += (unsigned long long)gridDim.x * nsh) {
     const int i = find_row(prefix, A.p, tile);
     const int t_in_row = (int)(tile - prefix[i]);
     const int oi = A.off[i], w = A.off[i + 1] - oi, lc = A.lowcnt[i];
@@ -564,13 +568,13 @@ __global__ void __launch_bounds__(kL1Threads) level1_kernel(LevelArgs A, int pas
 
 // tiles [u_begin, min(u_end, prefix[p])); `bound` is a host upper bound of the tile count (grid size)
 void launch_level1(const LevelArgs& A, int pass, const unsigned long long* prefix, unsigned long long u_begin,
-                   unsigned long long u_end, unsigned long long bound, cudaStream_t s) {
-    unsigned long long n = bound;
+                   unsigned long long u_end, unsigned long long bound, int shard, int nsh, cudaStream_t s) {
+    unsigned long long n = (bound + nsh - 1) / nsh;
     if (u_end != ~0ull && u_end - u_begin < n) n = u_end - u_begin;
     if (n > 148ull * 16) n = 148ull * 16;
     if (n == 0) return;
     ++g_kernel_launches;
-    level1_kernel<<<(unsigned)n, kL1Threads, 0, s>>>(A, pass, prefix, u_begin, u_end);
+    level1_kernel<<<(unsigned)n, kL1Threads, 0, s>>>(A, pass, prefix, u_begin, u_end, shard, nsh);
 }
 
 // =========================================================== ell >= 2, cuPC-S

@@ -97,8 +97,8 @@ __device__ __forceinline__ void issue_chunk(L1TSmem& S, const CUtensorMap* mapJ,
 }  // namespace
 
 __global__ void __launch_bounds__(kThreads, 3)
-    level1_tile_kernel(LevelArgs A, const uint32_t* __restrict__ adj, int W, int nI, int ib_begin, int row_begin,
-                       int row_end, const __grid_constant__ CUtensorMap mapJ, const __grid_constant__ CUtensorMap mapI,
+    level1_tile_kernel(LevelArgs A, const uint32_t* __restrict__ adj, int W, int nI, int shard, int nsh,
+                       const __grid_constant__ CUtensorMap mapJ, const __grid_constant__ CUtensorMap mapI,
                        double g_scale) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     L1TSmem& S = *reinterpret_cast<L1TSmem*>(smem_raw);
@@ -110,7 +110,7 @@ __global__ void __launch_bounds__(kThreads, 3)
     const int nJ = (A.p + kTJ - 1) / kTJ;
     const int grp = blockIdx.x / (nI * kJG), in = blockIdx.x % (nI * kJG);
     const int gw = min(kJG, nJ - grp * kJG);  // bands in this (possibly last, narrower) group
-    const int jb = grp * kJG + in % gw, ib = ib_begin + in / gw;
+    const int jb = grp * kJG + in % gw, ib = shard + (in / gw) * nsh;  // this shard's nI row blocks (cyclic)
     const int i0 = ib * kTI, j0 = jb * kTJ;
     const int p = A.p;
     const int nchunks = (p + kKC - 1) / kKC;
@@ -121,7 +121,7 @@ __global__ void __launch_bounds__(kThreads, 3)
 #pragma unroll
     for (int a = 0; a < kRowsPerWarp; ++a) {
         const int i = i0 + warp * kRowsPerWarp + a;
-        if (i >= p || i < row_begin || i >= row_end) continue;
+        if (i >= p) continue;
         const uint32_t w0 = __ldg(adj + (size_t)i * W + jw0);
         const uint32_t w1 = jw0 + 1 < W ? __ldg(adj + (size_t)i * W + jw0 + 1) : 0u;
         if ((w0 >> lane) & 1u) live |= 1u << (a * 2 + 0);
@@ -327,14 +327,14 @@ static int make_map(CUtensorMap* m, const double* C, long long ldc, int p, int b
     return r == CUDA_SUCCESS ? 0 : 2;
 }
 
-// rows [row_begin, row_end) of the level-1 pairs, both directions; returns nonzero if the tensor maps
-// cannot be built (caller falls back to level1_kernel)
-int launch_level1_tile(const LevelArgs& A, const uint32_t* adj, int W, int row_begin, int row_end, cudaStream_t s) {
-    if (row_end <= row_begin) return 0;
+// the level-1 pairs of row blocks shard, shard + nsh, ... (32 rows each), both directions; returns
+// nonzero if the tensor maps cannot be built
+int launch_level1_tile(const LevelArgs& A, const uint32_t* adj, int W, int shard, int nsh, cudaStream_t s) {
     CUtensorMap mapJ, mapI;
     if (make_map(&mapJ, A.C, A.ldc, A.p, kTJ, kKC) || make_map(&mapI, A.C, A.ldc, A.p, kKC, kTI)) return 1;
-    const int ib0 = row_begin / kTI, ib1 = (row_end + kTI - 1) / kTI;
-    const int nI = ib1 - ib0, nJ = (A.p + kTJ - 1) / kTJ;
+    const int nIall = (A.p + kTI - 1) / kTI;
+    const int nI = shard < nIall ? (nIall - shard + nsh - 1) / nsh : 0, nJ = (A.p + kTJ - 1) / kTJ;
+    if (nI == 0) return 0;
     const size_t smem = level1_tile_smem_bytes();
     if (cudaFuncSetAttribute(level1_tile_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
         return 3;
@@ -343,8 +343,7 @@ int launch_level1_tile(const LevelArgs& A, const uint32_t* adj, int W, int row_b
     double g_scale = (double)gs;
     if ((long double)g_scale < gs) g_scale = nextafter(g_scale, INFINITY);
     ++g_kernel_launches;
-    level1_tile_kernel<<<(unsigned)(nI * nJ), kThreads, smem, s>>>(A, adj, W, nI, ib0, row_begin, row_end, mapJ, mapI,
-                                                                   g_scale);
+    level1_tile_kernel<<<(unsigned)(nI * nJ), kThreads, smem, s>>>(A, adj, W, nI, shard, nsh, mapJ, mapI, g_scale);
     return cudaGetLastError() == cudaSuccess ? 0 : 4;
 }
 

@@ -98,9 +98,10 @@ void launch_edge_bounds(const LevelArgs& A, int pass, long long E, unsigned long
                         unsigned long long* bounds, cudaStream_t s);
 // tiles [u_begin, min(u_end, prefix[p])) (u_end = ~0: the device-side total); bound = host upper bound
 void launch_level1(const LevelArgs& A, int pass, const unsigned long long* prefix, unsigned long long u_begin,
-                   unsigned long long u_end, unsigned long long bound, cudaStream_t s);
+                   unsigned long long u_end, unsigned long long bound, int shard, int nsh, cudaStream_t s);
 // ---- level1t.cu: ell = 1, both directions, TMA-tiled (dense snapshots); rows [row_begin, row_end)
-int launch_level1_tile(const LevelArgs& A, const uint32_t* adj, int W, int row_begin, int row_end, cudaStream_t s);
+// multi-GPU: shard `shard` of `nsh` takes every nsh-th 32-row block (cyclic)
+int launch_level1_tile(const LevelArgs& A, const uint32_t* adj, int W, int shard, int nsh, cudaStream_t s);
 int launch_level_set(const LevelArgs& A, int pass, const unsigned long long* prefix, unsigned long long u_begin,
                      unsigned long long u_end, int num_sms, cudaStream_t s);
 int launch_level_edge(const LevelArgs& A, int pass, long long e_begin, long long e_end, int num_sms,

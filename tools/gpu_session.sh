@@ -55,9 +55,10 @@ for s in $STEPS; do
         python tools/profile_target.py 3 16 set > $OUT/ncu_full.log 2>&1
       ;;
     balance)
-      timeout 900 python tools/shard_balance.py 8 C2 3 set > $OUT/balance.json 2> $OUT/balance.err
-      timeout 600 python tools/shard_balance.py 8 C3 -1 set >> $OUT/balance.json 2>> $OUT/balance.err
-      timeout 600 python tools/shard_balance.py 8 C2 2 edge >> $OUT/balance.json 2>> $OUT/balance.err
+      timeout 1200 python tools/shard_balance.py 8 C5 1 set > $OUT/balance.json 2> $OUT/balance.err
+      timeout 1200 python tools/shard_balance.py 8 C2 3 set >> $OUT/balance.json 2>> $OUT/balance.err
+      timeout 900 python tools/shard_balance.py 8 C3 -1 set >> $OUT/balance.json 2>> $OUT/balance.err
+      timeout 900 python tools/shard_balance.py 8 C4 -1 set >> $OUT/balance.json 2>> $OUT/balance.err
       ;;
     candtrace)
       PCS_TRACE=1 timeout 900 python tools/variants.py run cand --workload C2 --max-level 3 --repeats 1 > $OUT/cand.json 2> $OUT/cand.err
@@ -111,6 +112,19 @@ for s in $STEPS; do
         > $OUT/sanitizer_racecheck_C3_l1tile.log 2>&1; echo "rc=$?" >> $OUT/sanitizer_racecheck_C3_l1tile.log
       PCS_L1_TILE=1 timeout 1800 compute-sanitizer --tool synccheck --error-exitcode 9 python tools/explore.py C3 set 1 \
         > $OUT/sanitizer_synccheck_C3_l1tile.log 2>&1; echo "rc=$?" >> $OUT/sanitizer_synccheck_C3_l1tile.log
+      ;;
+    shardtests)
+      timeout 1200 python -m pytest tests/test_gpu_shards.py tests/test_gpu_multiproc.py tests/test_gpu_bench_multirank.py \
+        tests/test_gpu_nccl.py -x -q > $OUT/pytest_shards.log 2>&1; echo "rc=$?" >> $OUT/pytest_shards.log
+      ls /usr/include/eigen3 /usr/local/include/eigen3 > $OUT/eigen_check.txt 2>&1; find / -name "Dense" -path "*Eigen*" 2>/dev/null | head -3 >> $OUT/eigen_check.txt
+      ;;
+    ncur2)
+      PCS_L1_TILE=1 timeout 900 ncu --set full --clock-control none --import-source on -k regex:level1_tile -c 1 -f -o $OUT/l1t \
+        python tools/explore.py C5b set 1 > $OUT/ncu_l1t.log 2>&1
+      timeout 900 ncu --set full --clock-control none -k regex:gram_dmma2 -c 1 -f -o $OUT/gram2_c5e \
+        python tools/time_corr.py C5e 1 > $OUT/ncu_gram2_c5e.log 2>&1
+      timeout 900 ncu --set full --clock-control none --import-source on -k regex:level_set_rt -c 1 -f -o $OUT/rt \
+        python tools/explore.py C3 set -1 > $OUT/ncu_rt.log 2>&1
       ;;
     bench)
       timeout 900 python bench.py > $OUT/bench.json 2> $OUT/bench.err
