@@ -14,6 +14,14 @@
  * level 1, which cover the bulk of all tests) are bit-identical to the
  * reference by construction.  Eigen-internal summation order inside the
  * |S| >= 3 small products is NOT pinned (documented in DESIGN.md).
+ *
+ * Two additions serve the whole-run fixtures (tests/golden, tools/make_golden.py):
+ *  - ORC_FAST: Strategy::Serial's result computed set-shared (one pseudo-inverse
+ *    per (row, set), lanes over the row's targets, the same per-test operation
+ *    sequence); result-identical to ORC_SERIAL (tests/test_oracle_fast.py);
+ *  - orc_compute_correlation_fma: compute_correlation in the device's pinned
+ *    order (tree column means, FMA-chain Gram over k), the order the reference
+ *    leaves to Eigen; the device's matrix equals it bit for bit.
  */
 #ifndef PCS_ORACLE_H
 #define PCS_ORACLE_H

@@ -1473,19 +1473,25 @@ __global__ void __launch_bounds__(128) level_set_rt_kernel(LevelArgs A, int pass
     int nan = 0;
     unsigned long long* cursor = &A.cnt->units[pass];
     u_end = min(u_end, prefix[A.p]);
+    int row_hint = 0;
     for (;;) {
         unsigned long long u = 0;
         if (lane == 0) u = u_begin + atomicAdd(cursor, 1ull);
         u = __shfl_sync(0xffffffffu, u, 0);
         if (u >= u_end) break;
-        const int i = find_row(prefix, A.p, u);
+        const int i = find_row_from(prefix, A.p, u, row_hint);
+        row_hint = i;
         const unsigned long long t0 = (u - prefix[i]) * kSetBand;
         const int oi = A.off[i], w = A.off[i + 1] - oi, lc = A.lowcnt[i];
         const int qbeg = pass == 0 ? lc : 0, qend = pass == 0 ? w : lc;
         const unsigned long long K0 = dirbits | t0;
         bool open = false;
         for (int q = qbeg + lane; q < qend; q += 32) open |= A.keys[A.eid[oi + q]] > K0;
-        if (!__any_sync(0xffffffffu, open)) continue;
+        if (!__any_sync(0xffffffffu, open)) {
+            // no open target at rank t0: none at any later rank of this row (keys only decrease)
+            if (lane == 0) atomicMax(cursor, prefix[i + 1] - u_begin);
+            continue;
+        }
         const unsigned long long total = A.binom(w, n);
         const unsigned long long t = t0 + lane;
         const bool valid = t < total;

@@ -126,6 +126,9 @@ for s in $STEPS; do
       timeout 900 ncu --set full --clock-control none --import-source on -k regex:level_set_rt -c 1 -f -o $OUT/rt \
         python tools/explore.py C3 set -1 > $OUT/ncu_rt.log 2>&1
       ;;
+    balance5l2)
+      PCS_BALANCE_REPEATS=1 timeout 2400 python tools/shard_balance.py 8 C5 2 set > $OUT/balance_c5l2.json 2> $OUT/balance_c5l2.err
+      ;;
     bench)
       timeout 900 python bench.py > $OUT/bench.json 2> $OUT/bench.err
       ;;
