@@ -221,6 +221,9 @@ struct pcs_session {
     int ell = -1;
     bool stopped = false, in_level = false;
     double tau_override = NAN;     // pcs_run_level: the caller's threshold instead of threshold_tau
+    double* dPinv = nullptr;       // l = 2, 3 pseudo-inverse table (level_set_kernel phase 1)
+    long long capPinv = 0;         // doubles
+    bool use_pinv = false;
     Counters* hCnt = nullptr;      // pinned copy of the level's counters (deferred level end)
     bool pending_end = false;      // run_session: the level's counters are in flight to hCnt
     double pending_t0 = 0.0;
@@ -278,6 +281,7 @@ void free_session(pcs_session* s) {
     rel(s->dScratch);
     rel(s->dShardCost);
     rel(s->dBounds);
+    rel(s->dPinv);
     if (s->st) cudaStreamSynchronize(s->st);
     pinned_counters_release(s->hCnt);
     if (s->ev_begin) cudaEventDestroy(s->ev_begin);
@@ -446,6 +450,7 @@ LevelArgs level_args(pcs_session* s) {
     A.keys = s->dKeys;
     A.kdir = s->dKdir;
     A.cnbr = s->dCnbr;
+    A.pinv_table = s->use_pinv ? s->dPinv : nullptr;
     A.binom.t = s->dBinom;
     A.binom.stride = s->binom_stride;
     A.th = s->th;
@@ -576,6 +581,7 @@ pcs_status pcs_session_create_device(const double* d_c, int64_t ldc, int32_t p, 
 }
 
 static pcs_status finalize_pending(pcs_session* s);
+static pcs_status maybe_pinv_table(pcs_session* s, int ell);
 
 
 pcs_status pcs_session_level_begin(pcs_session* s, int32_t* running, int32_t* ell_out, int64_t* num_keys) {
@@ -667,6 +673,7 @@ pcs_status pcs_session_level_begin(pcs_session* s, int32_t* running, int32_t* el
         }
     }
     if ((st = build_binomials(s, ell, maxw))) return st;
+    if ((st = maybe_pinv_table(s, ell))) return st;
     launch_snapshot_fill(s->dAdj, s->p, s->W, s->dOff, s->dNbr, s->st);
     LevelArgs A = level_args(s);
     launch_edge_index(A, s->dEid, s->dEuA, s->dEuQa, s->dEuQb, ell >= 2 ? s->dCnbr : nullptr, s->st);
@@ -692,6 +699,34 @@ static bool level1_tile(const pcs_session* s) {
     // L2), 1.3x slower at p = 1643 (C3: L2-resident, 73% dense, most pairs separate within a few k)
     const double pairs = (double)s->p * (double)(s->p - 1);
     return s->p >= 2048 && (double)s->info.e_dir >= 0.5 * pairs;
+}
+
+// PCS_PINV_TABLE: 0 never, 1 whenever it fits, unset/other: when the level's (row, set) pairs outnumber
+// the vertex l-subsets 4:1 and the table takes at most a quarter of the free device memory (32 GB cap).
+// C2: level 2 3.8e7 pairs / 5.0e5 subsets, level 3 2.7e9 / 1.7e8 (13 GB table).
+static pcs_status maybe_pinv_table(pcs_session* s, int ell) {
+    static const int mode = [] {
+        const char* e = std::getenv("PCS_PINV_TABLE");
+        return e ? std::atoi(e) : -1;
+    }();
+    s->use_pinv = false;
+    if (mode == 0 || (ell != 2 && ell != 3) || s->cfg.variant != PCS_VARIANT_SET) return PCS_OK;
+    const double n = (double)s->p;
+    const double subsets = ell == 2 ? n * (n - 1) / 2 : n * (n - 1) * (n - 2) / 6;
+    const double pairs = ell == 2 ? s->info.sets2 : s->info.sets3;
+    const double doubles = subsets * (double)pinv_table_stride(ell);
+    size_t free_b = 0, total_b = 0;
+    cudaMemGetInfo(&free_b, &total_b);
+    const double cap = std::min(32e9, 0.25 * (double)free_b) / 8.0;
+    if (doubles > cap || (mode != 1 && pairs < 4.0 * subsets)) return PCS_OK;
+    if ((long long)doubles > s->capPinv) {
+        pcs_status st = realloc_dev(s, &s->dPinv, (long long)doubles);
+        if (st) return st;
+        s->capPinv = (long long)doubles;
+    }
+    if (launch_pinv_table(s->dC, s->ldc, s->p, ell, s->dPinv, s->st)) return fail(PCS_EUNSUPPORTED, "pinv table");
+    s->use_pinv = true;
+    return PCS_OK;
 }
 
 static bool merged_level(const pcs_session* s) {

@@ -199,17 +199,28 @@ __global__ void snapshot_scan_kernel(const int32_t* __restrict__ deg, const int3
                                      int32_t* off, int32_t* upoff, SnapInfo* info) {
     __shared__ long long s1[1024], s2[1024];
     __shared__ int smax[1024];
+    __shared__ double sc2[1024], sc3[1024];
     const int t = threadIdx.x, nt = blockDim.x;
     const int per = (p + nt - 1) / nt;
     const int beg = min(t * per, p), end = min(beg + per, p);
     long long a = 0, b = 0;
     int mx = 0;
+    double c2 = 0.0, c3 = 0.0;
     for (int k = beg; k < end; ++k) {
         a += deg[k];
         b += deg[k] - lowcnt[k];
         mx = max(mx, deg[k]);
+        const double w = (double)deg[k];
+        c2 += 0.5 * w * (w - 1.0);
+        c3 += w * (w - 1.0) * (w - 2.0) / 6.0;
     }
     s1[t] = a; s2[t] = b; smax[t] = mx;
+    sc2[t] = c2; sc3[t] = c3;
+    __syncthreads();
+    for (int d = nt / 2; d > 0; d >>= 1) {  // totals only (a sizing estimate)
+        if (t < d) { sc2[t] += sc2[t + d]; sc3[t] += sc3[t + d]; }
+        __syncthreads();
+    }
     __syncthreads();
     for (int d = 1; d < nt; d <<= 1) {  // Hillis-Steele inclusive scan
         long long x1 = 0, x2 = 0;
@@ -233,6 +244,8 @@ __global__ void snapshot_scan_kernel(const int32_t* __restrict__ deg, const int3
         info->e_und = s2[t];
         info->max_width = smax[t];
         info->pad = 0;  // the whole struct is copied to the host (compute-sanitizer initcheck)
+        info->sets2 = sc2[0];
+        info->sets3 = sc3[0];
     }
 }
 
@@ -597,6 +610,79 @@ void launch_level1(const LevelArgs& A, int pass, const unsigned long long* prefi
 // A unit that finds no live target proves every later unit of the row dead
 // (keys only decrease, ranks only increase) and advances the work cursor past the
 // row.
+// ---- per-level pseudo-inverse table (l = 2, 3): M2^+ depends only on the set, and a set recurs in
+// every row that contains it (C2 level 3: 2.7e9 (row, set) pseudo-inverses over C(1000, 3) = 1.7e8
+// distinct sets), so when the level's (row, set) pairs outnumber the vertex l-subsets the host builds the
+// table of all of them once (pinv_table_kernel) and phase 1 loads its set's entry by colex rank
+// (C(c, 3) + C(b, 2) + a for a < b < c) instead of gathering M2 and running the pseudo-inverse.
+template <int L>
+struct PinvStride {
+    static constexpr int v = (L * L + 1) / 2 * 2;  // doubles per entry, 16-B aligned
+};
+
+__device__ __forceinline__ unsigned long long ch2(unsigned long long n) { return n * (n - 1) / 2; }
+__device__ __forceinline__ unsigned long long ch3(unsigned long long n) { return n * (n - 1) * (n - 2) / 6; }
+
+template <int L>
+__device__ __forceinline__ unsigned long long colex_rank(const int (&mem)[L]) {
+    if constexpr (L == 2) return ch2((unsigned long long)mem[1]) + (unsigned long long)mem[0];
+    else return ch3((unsigned long long)mem[2]) + ch2((unsigned long long)mem[1]) + (unsigned long long)mem[0];
+}
+
+// largest n with f(n) <= t, starting from a floating estimate (f = C(., k), k = 2, 3)
+template <int K>
+__device__ __forceinline__ int colex_top(unsigned long long t) {
+    double est = K == 2 ? sqrt(2.0 * (double)t) : cbrt(6.0 * (double)t);
+    long long n = (long long)est + K - 1;
+    auto f = [](long long x) -> unsigned long long {
+        if (x < K) return 0ull;
+        return K == 2 ? ch2((unsigned long long)x) : ch3((unsigned long long)x);
+    };
+    while (n > 0 && f(n) > t) --n;
+    while (f(n + 1) <= t) ++n;
+    return (int)n;
+}
+
+template <int L>
+__global__ void __launch_bounds__(128) pinv_table_kernel(const double* __restrict__ C, long long ldc,
+                                                         unsigned long long count, double* __restrict__ table) {
+    for (unsigned long long t = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; t < count;
+         t += (unsigned long long)gridDim.x * blockDim.x) {
+        int mem[L];
+        unsigned long long r = t;
+        if constexpr (L == 3) {
+            mem[2] = colex_top<3>(r);
+            r -= ch3((unsigned long long)mem[2]);
+        }
+        mem[1] = colex_top<2>(r);
+        r -= ch2((unsigned long long)mem[1]);
+        mem[0] = (int)r;
+        double m2[L * L], minv[L * L];
+#pragma unroll
+        for (int a = 0; a < L; ++a)
+#pragma unroll
+            for (int b = 0; b < L; ++b) m2[a * L + b] = __ldg(C + (size_t)mem[a] * ldc + mem[b]);
+        pinv<L>(m2, minv);
+        double* e = table + t * (unsigned long long)PinvStride<L>::v;
+#pragma unroll
+        for (int q = 0; q < L * L; ++q) e[q] = minv[q];
+    }
+}
+
+int pinv_table_stride(int ell) { return ell == 2 ? PinvStride<2>::v : PinvStride<3>::v; }
+
+int launch_pinv_table(const double* C, long long ldc, int p, int ell, double* table, cudaStream_t s) {
+    const unsigned long long n = (unsigned long long)p;
+    const unsigned long long count = ell == 2 ? n * (n - 1) / 2 : n * (n - 1) * (n - 2) / 6;
+    unsigned long long blocks = (count + 127) / 128;
+    if (blocks > 148ull * 64) blocks = 148ull * 64;
+    ++g_kernel_launches;
+    if (ell == 2) pinv_table_kernel<2><<<(unsigned)blocks, 128, 0, s>>>(C, ldc, count, table);
+    else if (ell == 3) pinv_table_kernel<3><<<(unsigned)blocks, 128, 0, s>>>(C, ldc, count, table);
+    else return -1;
+    return 0;
+}
+
 template <int L>
 struct alignas(16) SetSlot {
     // column c of the set's test data, 16 B aligned for LDS.128:
@@ -1242,11 +1328,25 @@ __global__ void __launch_bounds__(kSetWarps * 32, PCS_SET_MINB) level_set_kernel
                         mem[a] = A.nbr[oi + pos[a]];
                         ciS[a] = __ldg(C + (size_t)i * ldc + mem[a]);
                     }
+                    if (L <= 3 && A.pinv_table) {  // the set's M2^+ from the per-level table (same bits)
+                        const double* e = A.pinv_table + colex_rank<L>(mem) * (unsigned long long)PinvStride<L>::v;
 #pragma unroll
-                    for (int a = 0; a < L; ++a)
+                        for (int q = 0; q < L * L; q += 2) {
+                            if (q + 1 < L * L) {
+                                const double2 v2 = __ldg(reinterpret_cast<const double2*>(e + q));
+                                minv[q] = v2.x;
+                                minv[q + 1] = v2.y;
+                            } else {
+                                minv[q] = __ldg(e + q);
+                            }
+                        }
+                    } else {
 #pragma unroll
-                        for (int b = 0; b < L; ++b) m2[a * L + b] = __ldg(C + (size_t)mem[a] * ldc + mem[b]);
-                    pinv<L>(m2, minv);
+                        for (int a = 0; a < L; ++a)
+#pragma unroll
+                            for (int b = 0; b < L; ++b) m2[a * L + b] = __ldg(C + (size_t)mem[a] * ldc + mem[b]);
+                        pinv<L>(m2, minv);
+                    }
                     p0_terms<L>(minv, ciS, p0, h00);
                     SetSlot<L>& sl = S.slot[lane];
 #pragma unroll

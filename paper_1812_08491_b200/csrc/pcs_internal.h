@@ -37,6 +37,7 @@ struct SnapInfo {
     long long e_und;      // undirected edges (E)
     int max_width;
     int pad;
+    double sets2, sets3;  // sum over rows of C(w, 2), C(w, 3): the level's (row, set) pairs at l = 2, 3
 };
 
 // Everything a level kernel reads.
@@ -57,6 +58,7 @@ struct LevelArgs {
     unsigned long long* kdir;  // 2E: keys[eid[k]] mirrored per directed entry (cuPC-S staging reads it
                                //     coalesced, no dependent gather); refreshed before every pass
     const double* cnbr;        // 2E: C(i, nbr[k]) of the directed entry k of row i (filled per level)
+    const double* pinv_table;  // l = 2, 3: M2^+ of every vertex l-subset by colex rank (null: compute per set)
     BinomTable binom;
     Thresholds th;
     Counters* cnt;
@@ -102,6 +104,10 @@ void launch_level1(const LevelArgs& A, int pass, const unsigned long long* prefi
 // ---- level1t.cu: ell = 1, both directions, TMA-tiled (dense snapshots); rows [row_begin, row_end)
 // multi-GPU: shard `shard` of `nsh` takes every nsh-th 32-row block (cyclic)
 int launch_level1_tile(const LevelArgs& A, const uint32_t* adj, int W, int shard, int nsh, cudaStream_t s);
+// l = 2, 3: the pseudo-inverse of every l-subset {a < b (< c)} of the p vertices into table[colex rank *
+// pinv_table_stride(l)], the same pinv<L> as the per-set path (bit-identical entries)
+int pinv_table_stride(int ell);
+int launch_pinv_table(const double* C, long long ldc, int p, int ell, double* table, cudaStream_t s);
 int launch_level_set(const LevelArgs& A, int pass, const unsigned long long* prefix, unsigned long long u_begin,
                      unsigned long long u_end, int num_sms, cudaStream_t s);
 int launch_level_edge(const LevelArgs& A, int pass, long long e_begin, long long e_end, int num_sms,

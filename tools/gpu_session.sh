@@ -129,6 +129,12 @@ for s in $STEPS; do
     balance5l2)
       PCS_BALANCE_REPEATS=1 timeout 2400 python tools/shard_balance.py 8 C5 2 set > $OUT/balance_c5l2.json 2> $OUT/balance_c5l2.err
       ;;
+    pinvtab)
+      for v in 0 2; do
+        PCS_PINV_TABLE=$v timeout 900 python tools/explore.py C2 set 3 2 >> $OUT/pinvtab_$v.log 2>&1
+        PCS_PINV_TABLE=$v timeout 900 python tools/explore.py C5a,C5c set 2 2 >> $OUT/pinvtab_$v.log 2>&1
+      done
+      ;;
     bench)
       timeout 900 python bench.py > $OUT/bench.json 2> $OUT/bench.err
       ;;
