@@ -140,6 +140,17 @@ int64_t pcs_result_member_total(const pcs_result* r);
 /* per unordered pair, triangular slot index of core.hpp:329-335: level (-1 = kept), offset into members */
 void pcs_result_sepsets(const pcs_result* r, int32_t* level, int64_t* offset, int32_t* members);
 double pcs_result_device_seconds(const pcs_result* r); /* CUDA-event time of the whole device pipeline */
+/* Near-threshold tests (BASELINE parity protocol: "listed, not hidden"): every CI decision whose
+   statistic fell inside the +-1e-9 band around the threshold and was taken by the exact fisher_z
+   comparison (stats.hpp:345-351).  These are the only decisions that could differ from the reference's
+   if a libm log differed in the last ulp.  count = all of the run, records = the first 4096. */
+typedef struct {
+    int32_t level, i, j;     /* level, tested row i and target j (unordered pair for level 0) */
+    int32_t independent;     /* the decision */
+    double rho, z;           /* the partial correlation and fisher_z(rho); tau is threshold_tau(level) */
+} pcs_near_record;
+int64_t pcs_result_near_count(const pcs_result* r);
+int64_t pcs_result_near_records(const pcs_result* r, pcs_near_record* out, int64_t cap);
 /* compact forms: live bitmask p x ceil(p/32) uint32 (bit j of word i*W + j/32), and the removal records
    of levels >= 1 as consecutive (a, b, ell, members[ell]) int32 tuples (level-0 removals are implied) */
 void pcs_result_bitmask(const pcs_result* r, uint32_t* out);

@@ -83,6 +83,11 @@ class _Config(ct.Structure):
     ]
 
 
+class _NearRec(ct.Structure):
+    _fields_ = [("level", ct.c_int32), ("i", ct.c_int32), ("j", ct.c_int32), ("independent", ct.c_int32),
+                ("rho", ct.c_double), ("z", ct.c_double)]
+
+
 class _Level(ct.Structure):
     _fields_ = [
         ("level", ct.c_int32), ("pad", ct.c_int32), ("ci_tests", ct.c_uint64), ("pseudo_inverses", ct.c_uint64),
@@ -135,6 +140,10 @@ def library():
     L.pcs_result_record_ints.restype = ct.c_int64
     L.pcs_result_records.argtypes = [vp, ip]
     L.pcs_correlation_device.argtypes = [vp, ct.c_int32, ct.c_int32, vp, ct.c_int64, ct.c_uint64, ip]
+    L.pcs_result_near_count.argtypes = [vp]
+    L.pcs_result_near_count.restype = ct.c_int64
+    L.pcs_result_near_records.argtypes = [vp, ct.POINTER(_NearRec), ct.c_int64]
+    L.pcs_result_near_records.restype = ct.c_int64
     L.pcs_noise_stream.argtypes = [ct.c_uint64, ct.c_int64, ct.c_int32, ct.c_int32, dp]
     L.pcs_sample_linear_gaussian_device.argtypes = [dp, ct.c_int32, ct.c_int32, ct.c_uint64, ct.c_int32, vp, dp,
                                                     ct.c_uint64]
@@ -351,6 +360,8 @@ class SkeletonResult:  # skeleton.hpp:33-40
     levels: list = field(default_factory=list)
     stop_reason: StopReason = StopReason.MaxDegreeReached
     device_seconds: float = 0.0
+    near_threshold_count: int = 0   # decisions inside the +-1e-9 threshold band (exact comparison)
+    near_threshold: list = field(default_factory=list)  # first 4096: dicts level, i, j, independent, rho, z
 
     def levels_run(self) -> int:
         return len(self.levels)
@@ -385,7 +396,15 @@ def _collect(h, with_sepsets: bool = True) -> SkeletonResult:
         L.pcs_result_records(h, _ip(rec))
     adj = AdjacencyMatrix(bits, p)
     sep = SeparationSets(p, adj, rec[:nrec] if with_sepsets else np.empty(0, np.int32), levels)
-    return SkeletonResult(adj, sep, levels, _STOP[L.pcs_result_stop_reason(h)], L.pcs_result_device_seconds(h))
+    nn = L.pcs_result_near_count(h)
+    near = []
+    if nn:
+        buf = (_NearRec * min(nn, 4096))()
+        got = L.pcs_result_near_records(h, buf, len(buf))
+        near = [dict(level=b.level, i=b.i, j=b.j, independent=bool(b.independent), rho=b.rho, z=b.z)
+                for b in buf[:got]]
+    return SkeletonResult(adj, sep, levels, _STOP[L.pcs_result_stop_reason(h)], L.pcs_result_device_seconds(h),
+                          nn, near)
 
 
 # ----------------------------------------------------------------- API

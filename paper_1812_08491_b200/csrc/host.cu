@@ -184,6 +184,8 @@ struct pcs_result {
     // (default-initialised elements: no zero fill before the copy)
     std::vector<int32_t, NoInitAlloc<int32_t>> recs;
     double device_seconds = 0.0;
+    unsigned long long near_total = 0;         // near-threshold decisions of the run (all levels)
+    std::vector<NearRec> near;                 // the first kNearCap of them
 };
 
 // ================================================================ session
@@ -222,6 +224,8 @@ struct pcs_session {
     bool stopped = false, in_level = false;
     double tau_override = NAN;     // pcs_run_level: the caller's threshold instead of threshold_tau
     double* dPinv = nullptr;       // l = 2, 3 pseudo-inverse table (level_set_kernel phase 1)
+    NearRec* dNear = nullptr;      // near-threshold list of the run
+    unsigned long long* dNearTotal = nullptr;
     long long capPinv = 0;         // doubles
     bool use_pinv = false;
     Counters* hCnt = nullptr;      // pinned copy of the level's counters (deferred level end)
@@ -282,6 +286,8 @@ void free_session(pcs_session* s) {
     rel(s->dShardCost);
     rel(s->dBounds);
     rel(s->dPinv);
+    rel(s->dNear);
+    rel(s->dNearTotal);
     if (s->st) cudaStreamSynchronize(s->st);
     pinned_counters_release(s->hCnt);
     if (s->ev_begin) cudaEventDestroy(s->ev_begin);
@@ -371,6 +377,9 @@ pcs_status session_alloc(pcs_session* s) {
     CUDA_TRY(dev_malloc(reinterpret_cast<void**>(&s->dInfo), sizeof(SnapInfo), s->st));
     CUDA_TRY(dev_malloc(reinterpret_cast<void**>(&s->dCnt), sizeof(Counters), s->st));
     CUDA_TRY(dev_malloc(reinterpret_cast<void**>(&s->dPrefix), sizeof(unsigned long long) * (size_t)(p + 1), s->st));
+    CUDA_TRY(dev_malloc(reinterpret_cast<void**>(&s->dNear), sizeof(NearRec) * kNearCap, s->st));
+    CUDA_TRY(dev_malloc(reinterpret_cast<void**>(&s->dNearTotal), sizeof(unsigned long long), s->st));
+    CUDA_TRY(cudaMemsetAsync(s->dNearTotal, 0, sizeof(unsigned long long), s->st));
     return PCS_OK;
 }
 
@@ -451,6 +460,8 @@ LevelArgs level_args(pcs_session* s) {
     A.kdir = s->dKdir;
     A.cnbr = s->dCnbr;
     A.pinv_table = s->use_pinv ? s->dPinv : nullptr;
+    A.near_rec = s->dNear;
+    A.near_total = s->dNearTotal;
     A.binom.t = s->dBinom;
     A.binom.stride = s->binom_stride;
     A.th = s->th;
@@ -609,7 +620,8 @@ pcs_status pcs_session_level_begin(pcs_session* s, int32_t* running, int32_t* el
     CUDA_TRY(cudaMemsetAsync(s->dCnt, 0, sizeof(Counters), s->st));
     if (ell == 0) {
         CUDA_TRY(cudaEventRecord(s->ev_k0, s->st));
-        launch_level0(s->dC, s->ldc, s->p, s->W, s->dAdj, s->th, s->dCnt, s->st, s->level0_and);
+        launch_level0(s->dC, s->ldc, s->p, s->W, s->dAdj, s->th, s->dCnt, s->st, s->level0_and, s->dNear,
+                      s->dNearTotal);
         CUDA_TRY(cudaEventRecord(s->ev_k1, s->st));
         s->kernel_timing = true;
         CUDA_TRY(cudaGetLastError());
@@ -939,6 +951,12 @@ pcs_status pcs_session_finish(pcs_session* s, pcs_result** out) {
         CUDA_TRY(cudaMemcpyAsync(r->recs.data(), s->dRec, sizeof(int32_t) * r->recs.size(), cudaMemcpyDeviceToHost,
                                  s->st));
     }
+    CUDA_TRY(cudaMemcpyAsync(&r->near_total, s->dNearTotal, sizeof(unsigned long long), cudaMemcpyDeviceToHost, s->st));
+    CUDA_TRY(cudaStreamSynchronize(s->st));
+    if (r->near_total) {
+        r->near.resize((size_t)std::min<unsigned long long>(r->near_total, kNearCap));
+        CUDA_TRY(cudaMemcpyAsync(r->near.data(), s->dNear, sizeof(NearRec) * r->near.size(), cudaMemcpyDeviceToHost, s->st));
+    }
     r->adj.resize((size_t)s->p * s->W);
     CUDA_TRY(cudaMemcpyAsync(r->adj.data(), s->dAdj, sizeof(uint32_t) * r->adj.size(), cudaMemcpyDeviceToHost, s->st));
     CUDA_TRY(cudaEventRecord(s->ev_end, s->st));
@@ -1230,6 +1248,22 @@ void pcs_result_sepsets(const pcs_result* r, int32_t* level, int64_t* offset, in
         }
 }
 double pcs_result_device_seconds(const pcs_result* r) { return r->device_seconds; }
+
+int64_t pcs_result_near_count(const pcs_result* r) { return (int64_t)r->near_total; }
+
+int64_t pcs_result_near_records(const pcs_result* r, pcs_near_record* out, int64_t cap) {
+    const int64_t n = std::min<int64_t>((int64_t)r->near.size(), cap);
+    for (int64_t k = 0; k < n; ++k) {
+        const NearRec& x = r->near[(size_t)k];
+        out[k].level = x.level;
+        out[k].i = x.i;
+        out[k].j = x.j;
+        out[k].independent = x.decision == kIndependent;
+        out[k].rho = x.rho;
+        out[k].z = x.z;
+    }
+    return n;
+}
 void pcs_result_free(pcs_result* r) { delete r; }
 
 pcs_status pcs_ci_test_batch(const double* c, int32_t p, int32_t ell, int64_t n, const int32_t* ij,

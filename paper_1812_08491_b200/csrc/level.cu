@@ -34,9 +34,22 @@ unsigned long long g_kernel_launches = 0;
 // copied into every step instance and crowd the hot loop out of the instruction cache.
 __device__ __noinline__ int decide_slow(double h01, double denom, Thresholds th) { return decide_fast(h01, denom, th); }
 
-// strips kNearBit off a decision and counts the near-threshold test (rare: no contention)
-__device__ __forceinline__ int take_near(int d, Counters* cnt) {
-    if (d & kNearBit) atomicAdd(&cnt->near, 1ull);
+// A near-threshold decision (rare): counted per level and listed per run with its statistic
+__device__ __noinline__ void record_near(NearRec* rec, unsigned long long* total, unsigned long long* level_count,
+                                         int level, int i, int j, int d, double h01, double denom, double tau) {
+    atomicAdd(level_count, 1ull);
+    if (!rec || !total) return;
+    const unsigned long long k = atomicAdd(total, 1ull);
+    if (k >= (unsigned long long)kNearCap) return;
+    double z = 0.0, rho = 0.0;
+    decide_exact(h01, denom, tau, &z, &rho);
+    rec[k] = NearRec{level, i, j, d, rho, z};
+}
+
+// strips kNearBit off a decision and records the near-threshold test
+__device__ __forceinline__ int take_near(int d, const LevelArgs& A, int i, int j, double h01, double denom) {
+    if (d & kNearBit)
+        record_near(A.near_rec, A.near_total, &A.cnt->near, A.ell, i, j, d & ~kNearBit, h01, denom, A.th.tau);
     return d & ~kNearBit;
 }
 
@@ -133,7 +146,8 @@ __device__ unsigned long long rank_rt(const BinomTable& C, int w, int ell, const
 // and_live: keep only pairs already live in adj (pcs_run_level on an incomplete graph; run_pc_stable
 // starts from the complete graph and overwrites)
 __global__ void level0_kernel(const double* __restrict__ C, long long ldc, int p, int W, uint32_t* __restrict__ adj,
-                              Thresholds th, Counters* cnt, int and_live) {
+                              Thresholds th, Counters* cnt, int and_live, NearRec* near_rec,
+                              unsigned long long* near_total) {
     const int lane = threadIdx.x & 31;
     const long long warp = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const long long nwarps = ((long long)gridDim.x * blockDim.x) >> 5;
@@ -145,7 +159,12 @@ __global__ void level0_kernel(const double* __restrict__ C, long long ldc, int p
         const bool was = and_live ? ((adj[(size_t)i * W + w] >> lane) & 1u) != 0 : true;
         bool live = false;
         if (j < p && j != i) {
-            const int d = take_near(decide0(__ldg(C + (size_t)i * ldc + j), th), cnt);
+            const double cv = __ldg(C + (size_t)i * ldc + j);
+            int d = decide0(cv, th);
+            if (d & kNearBit) {  // level 0: rho = clamp(c_ij), i.e. h01 = c_ij over denom = 1
+                d &= ~kNearBit;
+                if (j > i) record_near(near_rec, near_total, &cnt->near, 0, i, j, d, cv, 1.0, th.tau);
+            }
             nan |= d == kNanError;
             live = d == kDependent && was;
             if (j > i && d == kIndependent && was) ++removed;
@@ -159,12 +178,12 @@ __global__ void level0_kernel(const double* __restrict__ C, long long ldc, int p
 }
 
 void launch_level0(const double* C, long long ldc, int p, int W, uint32_t* adj, Thresholds th, Counters* cnt,
-                   cudaStream_t s, bool and_live) {
+                   cudaStream_t s, bool and_live, NearRec* near_rec, unsigned long long* near_total) {
     const long long items = (long long)p * W;
     long long blocks = (items * 32 + 255) / 256;
     if (blocks > 148 * 16) blocks = 148 * 16;
     ++g_kernel_launches;
-    level0_kernel<<<(int)blocks, 256, 0, s>>>(C, ldc, p, W, adj, th, cnt, and_live ? 1 : 0);
+    level0_kernel<<<(int)blocks, 256, 0, s>>>(C, ldc, p, W, adj, th, cnt, and_live ? 1 : 0, near_rec, near_total);
 }
 
 // =========================================================== snapshot
@@ -557,7 +576,7 @@ __global__ void __launch_bounds__(kL1Threads) level1_kernel(LevelArgs A, int pas
 #pragma unroll
                     for (int u = 0; u < kL1Unroll; ++u) {
                         if (!((cand >> u) & 1u)) continue;
-                        const int d = take_near(decide_slow(h01[u], den[u], A.th), A.cnt);
+                        const int d = take_near(decide_slow(h01[u], den[u], A.th), A, i, j, h01[u], den[u]);
                         if (d != kDependent) {
                             active = false;
                             if (d == kNanError) nan = 1;
@@ -836,7 +855,7 @@ __device__ __forceinline__ void h_terms_tsp(const SetSlot<L>* const (&sl)[SP], c
 // order per target: the first separating set among a step's SP wins and later ones are discarded.
 // Same results and counters as set_sweep<L, NT>.
 template <int L, int NT, int SP>
-__device__ __forceinline__ void set_sweep_tsp(const LevelArgs& A, SetWarpSmem<L>& S, int lane, int oi, int lc,
+__device__ __forceinline__ void set_sweep_tsp(const LevelArgs& A, SetWarpSmem<L>& S, int lane, int row, int oi, int lc,
                                               int nlive, int nvalid, unsigned segmask, unsigned livemask,
                                               unsigned long long K0, unsigned long long& tests,
                                               unsigned long long& degen, int& nan) {
@@ -939,7 +958,7 @@ __device__ __forceinline__ void set_sweep_tsp(const LevelArgs& A, SetWarpSmem<L>
                     for (int k = 0; k < SP; ++k) {
                         if (((cand >> (t * SP + k)) & 1u) && g[k] < lim[t]) {
                             const double h01 = 0.5 * cij2[t] - 0.5 * s01[t][k];
-                            const int d = take_near(decide_slow(h01, den[t][k], A.th), A.cnt);
+                            const int d = take_near(decide_slow(h01, den[t][k], A.th), A, row, S.tj[t * 32 + lane], h01, den[t][k]);
                             if (d != kDependent) {
                                 const int kk = t * 32 + lane;
                                 const bool dir1 = q[t] < lc;
@@ -1050,7 +1069,7 @@ __device__ __forceinline__ void h_terms_stream_sa(uint32_t sla, const double (&c
 // (rank-truncated inputs hit this often: ~29% of C2's level-3 sets), and the last-member
 // prefetch always targets the next LIVE set, so skipped sets cost no L2 round trip either.
 template <int L, int NT>
-__device__ __forceinline__ void set_sweep(const LevelArgs& A, SetWarpSmem<L>& S, int lane, int oi, int lc, int nlive,
+__device__ __forceinline__ void set_sweep(const LevelArgs& A, SetWarpSmem<L>& S, int lane, int row, int oi, int lc, int nlive,
                                           int nvalid, unsigned segmask, unsigned livemask, unsigned long long K0,
                                           unsigned long long& tests, unsigned long long& degen, int& nan) {
     const double* __restrict__ C = A.C;
@@ -1166,7 +1185,7 @@ __device__ __forceinline__ void set_sweep(const LevelArgs& A, SetWarpSmem<L>& S,
                 for (int t = 0; t < NT; ++t) {
                     if ((cand >> t) & 1u) {
                         const double h01 = 0.5 * cij2[t] - 0.5 * s01[t];  // == c_ij - 0.5 * (d01 + d10)
-                        const int d = take_near(decide_slow(h01, den[t], A.th), A.cnt);
+                        const int d = take_near(decide_slow(h01, den[t], A.th), A, row, S.tj[t * 32 + lane], h01, den[t]);
                         if (d != kDependent) {
                             if (d == kNanError) nan = 1;
                             else {
@@ -1386,21 +1405,21 @@ __global__ void __launch_bounds__(kSetWarps * 32, PCS_SET_MINB) level_set_kernel
             const int nt = (nlive + 31) >> 5;
             if constexpr (SetCfg<L>::NT >= 4) {
                 constexpr int NTM = SetCfg<L>::NT;
-                if (nt > 3) set_sweep<L, NTM>(A, S, lane, oi, lc, nlive, nvalid, segmask, livemask, K0, tests, degen, nan);
-                else if (nt == 3) set_sweep<L, 3>(A, S, lane, oi, lc, nlive, nvalid, segmask, livemask, K0, tests, degen, nan);
-                else if (nt == 2) set_sweep<L, 2>(A, S, lane, oi, lc, nlive, nvalid, segmask, livemask, K0, tests, degen, nan);
-                else set_sweep<L, 1>(A, S, lane, oi, lc, nlive, nvalid, segmask, livemask, K0, tests, degen, nan);
+                if (nt > 3) set_sweep<L, NTM>(A, S, lane, i, oi, lc, nlive, nvalid, segmask, livemask, K0, tests, degen, nan);
+                else if (nt == 3) set_sweep<L, 3>(A, S, lane, i, oi, lc, nlive, nvalid, segmask, livemask, K0, tests, degen, nan);
+                else if (nt == 2) set_sweep<L, 2>(A, S, lane, i, oi, lc, nlive, nvalid, segmask, livemask, K0, tests, degen, nan);
+                else set_sweep<L, 1>(A, S, lane, i, oi, lc, nlive, nvalid, segmask, livemask, K0, tests, degen, nan);
             } else if constexpr (SetCfg<L>::NT == 3) {
-                if (nt == 3) set_sweep<L, 3>(A, S, lane, oi, lc, nlive, nvalid, segmask, livemask, K0, tests, degen, nan);
+                if (nt == 3) set_sweep<L, 3>(A, S, lane, i, oi, lc, nlive, nvalid, segmask, livemask, K0, tests, degen, nan);
 #if PCS_NT2_SP > 1
-                else if (nt == 2) set_sweep_tsp<L, 2, PCS_NT2_SP>(A, S, lane, oi, lc, nlive, nvalid, segmask, livemask, K0, tests, degen, nan);
+                else if (nt == 2) set_sweep_tsp<L, 2, PCS_NT2_SP>(A, S, lane, i, oi, lc, nlive, nvalid, segmask, livemask, K0, tests, degen, nan);
 #else
-                else if (nt == 2) set_sweep<L, 2>(A, S, lane, oi, lc, nlive, nvalid, segmask, livemask, K0, tests, degen, nan);
+                else if (nt == 2) set_sweep<L, 2>(A, S, lane, i, oi, lc, nlive, nvalid, segmask, livemask, K0, tests, degen, nan);
 #endif
-                else set_sweep_tsp<L, 1, PCS_SET_SP>(A, S, lane, oi, lc, nlive, nvalid, segmask, livemask, K0, tests, degen, nan);
+                else set_sweep_tsp<L, 1, PCS_SET_SP>(A, S, lane, i, oi, lc, nlive, nvalid, segmask, livemask, K0, tests, degen, nan);
             } else {
-                if (nt == 2) set_sweep<L, 2>(A, S, lane, oi, lc, nlive, nvalid, segmask, livemask, K0, tests, degen, nan);
-                else set_sweep_tsp<L, 1, 2>(A, S, lane, oi, lc, nlive, nvalid, segmask, livemask, K0, tests, degen, nan);
+                if (nt == 2) set_sweep<L, 2>(A, S, lane, i, oi, lc, nlive, nvalid, segmask, livemask, K0, tests, degen, nan);
+                else set_sweep_tsp<L, 1, 2>(A, S, lane, i, oi, lc, nlive, nvalid, segmask, livemask, K0, tests, degen, nan);
             }
             __syncwarp();
         }
@@ -1494,7 +1513,7 @@ __global__ void __launch_bounds__(128) level_edge_kernel(LevelArgs A, int pass, 
                 pinv<L>(m2, minv);
                 p0_terms<L>(minv, ciS, p0, h00);
                 h_terms<L>(minv, ciS, p0, h00, cjS, cij, h01, denom);
-                d = take_near(decide_fast(h01, denom, A.th), A.cnt);
+                d = take_near(decide_fast(h01, denom, A.th), A, i, j, h01, denom);
                 ++tests;
                 ++pinvs;
             }
@@ -1642,7 +1661,7 @@ __global__ void __launch_bounds__(128) level_set_rt_kernel(LevelArgs A, int pass
                 for (int a = 0; a < n; ++a) cjS[a] = __ldg(C + (size_t)Spos[n + a] * ldc + j);
                 double h01, denom;
                 h_terms_rt(Sminv, SciS, SciS + n, SciS[2 * n], cjS, n, cij, P1, h01, denom);
-                const int d = take_near(decide_fast(h01, denom, A.th), A.cnt);
+                const int d = take_near(decide_fast(h01, denom, A.th), A, i, j, h01, denom);
                 if (d != kDependent) {
                     live = false;
                     if (d == kNanError) nan = 1;

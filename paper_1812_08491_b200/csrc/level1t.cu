@@ -47,6 +47,17 @@ constexpr int kJG = 16;        // target bands per L2 group (16 x 64 columns of 
 
 __device__ __noinline__ int decide_slow1(double h01, double denom, Thresholds th) { return decide_fast(h01, denom, th); }
 
+// near-threshold decision: counted per level, listed per run (as level.cu's record_near)
+__device__ __noinline__ void record_near1(const LevelArgs& A, int i, int j, int d, double h01, double denom) {
+    atomicAdd(&A.cnt->near, 1ull);
+    if (!A.near_rec || !A.near_total) return;
+    const unsigned long long k = atomicAdd(A.near_total, 1ull);
+    if (k >= (unsigned long long)kNearCap) return;
+    double z = 0.0, rho = 0.0;
+    decide_exact(h01, denom, A.th.tau, &z, &rho);
+    A.near_rec[k] = NearRec{1, i, j, d, rho, z};
+}
+
 struct __align__(128) L1TSmem {
     double rawJ[kKC][kTJ];     // TMA destination: C(k0 + kk, j0 + jj)
     double rawI[kTI][kKC];     // TMA destination: C(i0 + r, k0 + kk)
@@ -250,8 +261,10 @@ __global__ void __launch_bounds__(kThreads, 3)
                         const double h01 = cij[a][b] - iv.x * jv.x;
                         const double den = (1.0 - iv.x * iv.x) * (1.0 - jv.x * jv.x);
                         int d = decide_slow1(h01, den, A.th);
-                        if (d & kNearBit) atomicAdd(&A.cnt->near, 1ull);
-                        d &= ~kNearBit;
+                        if (d & kNearBit) {
+                            d &= ~kNearBit;
+                            record_near1(A, i0 + r, j, d, h01, den);
+                        }
                         if (d == kDependent) continue;
                         tested = valid & ((2u << kk) - 1u);
                         live &= ~(1u << q);

@@ -31,6 +31,13 @@ struct Counters {
     int err_other;
 };
 
+// One near-threshold decision (the exact comparison inside the +-1e-9 band), listed per run
+struct NearRec {
+    int level, i, j, decision;  // decision: kDependent / kIndependent / kNanError
+    double rho, z;
+};
+constexpr int kNearCap = 4096;  // records kept per run (the count is exact beyond)
+
 // Summary of a fresh snapshot (compact(), core.hpp:227-239).
 struct SnapInfo {
     long long e_dir;      // directed entries (2E)
@@ -59,6 +66,8 @@ struct LevelArgs {
                                //     coalesced, no dependent gather); refreshed before every pass
     const double* cnbr;        // 2E: C(i, nbr[k]) of the directed entry k of row i (filled per level)
     const double* pinv_table;  // l = 2, 3: M2^+ of every vertex l-subset by colex rank (null: compute per set)
+    NearRec* near_rec;         // near-threshold list of the run (kNearCap records)
+    unsigned long long* near_total;  // records written so far in the run
     BinomTable binom;
     Thresholds th;
     Counters* cnt;
@@ -77,7 +86,8 @@ void launch_correlation(const double* X, int m, int p, double* Xc, double* G, lo
 
 // ---- level.cu
 void launch_level0(const double* C, long long ldc, int p, int W, uint32_t* adj, Thresholds th, Counters* cnt,
-                   cudaStream_t s, bool and_live = false);
+                   cudaStream_t s, bool and_live = false, NearRec* near_rec = nullptr,
+                   unsigned long long* near_total = nullptr);
 void launch_snapshot_degrees(const uint32_t* adj, int p, int W, int32_t* deg, int32_t* lowcnt, cudaStream_t s);
 void launch_snapshot_scan(const int32_t* deg, const int32_t* lowcnt, int p, int32_t* off, int32_t* upoff,
                           SnapInfo* info, cudaStream_t s);

@@ -264,3 +264,21 @@ def test_run_level_chain_equals_run_pc_stable(pcs, oracle, variant):
         assert (st.level, st.ci_tests, st.edges_removed) == (lv.level, lv.ci_tests, lv.edges_removed)
     assert np.array_equal(g, ref.adjacency)
     assert sep == ref.sepsets
+
+
+def test_near_threshold_tests_are_listed(pcs, oracle):
+    """A level-0 pair whose |rho| sits 1e-12 (relative) either side of tanh(tau): both fall inside the
+    +-1e-9 band, are decided by the exact comparison, counted and listed with their statistic; the
+    decisions equal the oracle's."""
+    m, alpha = 500, 0.05
+    tau = oracle.threshold_tau(alpha, m, 0)
+    r = math.tanh(tau)
+    c = make_correlation(5, [(0, 1, r * (1 + 1e-12)), (2, 3, -r * (1 - 1e-12)), (1, 4, 0.5)])
+    dev = pcs.run_pc_stable(c, m, pcs.SkeletonConfig(alpha=alpha, max_level=0))
+    ref = oracle.run_pc_stable(c, m, alpha=alpha, max_level=0)
+    assert np.array_equal(dev.skeleton.cells, ref.adjacency)
+    assert dev.near_threshold_count == 2 and dev.levels[0].device_near_threshold == 2
+    got = sorted((x["i"], x["j"], x["independent"]) for x in dev.near_threshold)
+    assert got == [(0, 1, False), (2, 3, True)]
+    for x in dev.near_threshold:
+        assert x["level"] == 0 and abs(abs(x["rho"]) - r) <= 2e-12 * r and abs(x["z"] - tau) < 1e-9 * tau
