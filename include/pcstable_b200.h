@@ -73,7 +73,8 @@ typedef struct {
     uint64_t edges_removed;
     double elapsed_s;                 /* host wall time of the level (includes compaction) */
     uint64_t device_ci_tests;         /* CI tests the device actually executed */
-    uint64_t device_pseudo_inverses;  /* pseudo-inverses the device actually executed */
+    uint64_t device_pseudo_inverses;  /* (row, set) pseudo-inverses the device's CI tests used (computed per
+                                         set, or read from the level's l = 2, 3 table) */
     double kernel_ms;                 /* CUDA-event time of the level's CI-test kernels */
     uint64_t device_exact_tests;      /* tests whose statistic the device evaluated (in the reference's
                                          operation order); the rest of device_ci_tests were decided

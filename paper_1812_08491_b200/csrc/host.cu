@@ -727,10 +727,12 @@ static pcs_status maybe_pinv_table(pcs_session* s, int ell) {
     const double subsets = ell == 2 ? n * (n - 1) / 2 : n * (n - 1) * (n - 2) / 6;
     const double pairs = ell == 2 ? s->info.sets2 : s->info.sets3;
     const double doubles = subsets * (double)pinv_table_stride(ell);
-    size_t free_b = 0, total_b = 0;
-    cudaMemGetInfo(&free_b, &total_b);
-    const double cap = std::min(32e9, 0.25 * (double)free_b) / 8.0;
-    if (doubles > cap || (mode != 1 && pairs < 4.0 * subsets)) return PCS_OK;
+    if ((mode != 1 && pairs < 4.0 * subsets) || doubles > 32e9 / 8.0) return PCS_OK;
+    if ((long long)doubles > s->capPinv) {  // a new allocation: leave 3/4 of the free memory alone
+        size_t free_b = 0, total_b = 0;
+        cudaMemGetInfo(&free_b, &total_b);
+        if (doubles > 0.25 * (double)free_b / 8.0) return PCS_OK;
+    }
     if ((long long)doubles > s->capPinv) {
         pcs_status st = realloc_dev(s, &s->dPinv, (long long)doubles);
         if (st) return st;
@@ -875,6 +877,7 @@ static pcs_status level_stats_from(pcs_session* s, const Counters& c, double t_l
         L.ci_tests = p * (p - 1) / 2;  // skeleton.hpp:274-276
         L.pseudo_inverses = 0;
         L.device_ci_tests = L.ci_tests;
+        L.device_near_threshold = c.near;
     } else {
         L.ci_tests = c.ci_serial;
         L.pseudo_inverses = c.ci_serial;  // skeleton.hpp:151-152
@@ -919,6 +922,7 @@ static pcs_status level_end_impl(pcs_session* s, bool deferred) {
     CUDA_TRY(cudaSetDevice(s->device));
     LevelArgs A = level_args(s);
     if (s->ell >= 1) launch_commit(A, s->dAdj, s->W, s->info.e_und, s->dRec + s->recUsed, s->st);
+    if (s->ell >= 2) launch_near_fixup(A, s->st);  // before the next snapshot replaces off[]
     s->in_level = false;
     if (deferred) {
         if (!s->hCnt && !(s->hCnt = pinned_counters())) return fail(PCS_ENOMEM, "pinned host memory");

@@ -43,7 +43,7 @@ __device__ __noinline__ void record_near(NearRec* rec, unsigned long long* total
     if (k >= (unsigned long long)kNearCap) return;
     double z = 0.0, rho = 0.0;
     decide_exact(h01, denom, tau, &z, &rho);
-    rec[k] = NearRec{level, i, j, d, rho, z};
+    rec[k] = NearRec{level, i, j, d, rho, z, 0, 0};
 }
 
 // strips kNearBit off a decision and records the near-threshold test
@@ -51,6 +51,42 @@ __device__ __forceinline__ int take_near(int d, const LevelArgs& A, int i, int j
     if (d & kNearBit)
         record_near(A.near_rec, A.near_total, &A.cnt->near, A.ell, i, j, d & ~kNearBit, h01, denom, A.th.tau);
     return d & ~kNearBit;
+}
+
+// the cuPC-S sweeps store the raw facts inline (no call in the hot loop: a call's register saves cost
+// spills there); launch_near_fixup finds the row from its CSR offset and evaluates rho / z at level end
+__device__ __forceinline__ int take_near_row(int d, const LevelArgs& A, int oi, int j, double h01, double denom) {
+    if (d & kNearBit) {
+        d &= ~kNearBit;
+        atomicAdd(&A.cnt->near, 1ull);
+        const unsigned long long k = atomicAdd(A.near_total, 1ull);
+        if (k < (unsigned long long)kNearCap) A.near_rec[k] = NearRec{A.ell, -1, j, d, h01, denom, oi, 1};
+    }
+    return d;
+}
+
+__global__ void near_fixup_kernel(LevelArgs A) {
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= kNearCap || (unsigned long long)k >= *A.near_total) return;
+    NearRec r = A.near_rec[k];
+    if (!r.raw) return;
+    int lo = 0, hi = A.p - 1;  // the row with off[row] == oi < off[row + 1]
+    while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (A.off[mid + 1] <= r.oi) lo = mid + 1; else hi = mid;
+    }
+    double z = 0.0, rho = 0.0;
+    decide_exact(r.rho, r.z, A.th.tau, &z, &rho);
+    r.i = lo;
+    r.rho = rho;
+    r.z = z;
+    r.raw = 0;
+    A.near_rec[k] = r;
+}
+
+void launch_near_fixup(const LevelArgs& A, cudaStream_t s) {
+    ++g_kernel_launches;
+    near_fixup_kernel<<<kNearCap / 128, 128, 0, s>>>(A);
 }
 
 #ifndef PCS_SET_NT_SMALL
@@ -855,7 +891,7 @@ __device__ __forceinline__ void h_terms_tsp(const SetSlot<L>* const (&sl)[SP], c
 // order per target: the first separating set among a step's SP wins and later ones are discarded.
 // Same results and counters as set_sweep<L, NT>.
 template <int L, int NT, int SP>
-__device__ __forceinline__ void set_sweep_tsp(const LevelArgs& A, SetWarpSmem<L>& S, int lane, int row, int oi, int lc,
+__device__ __forceinline__ void set_sweep_tsp(const LevelArgs& A, SetWarpSmem<L>& S, int lane, int oi, int lc,
                                               int nlive, int nvalid, unsigned segmask, unsigned livemask,
                                               unsigned long long K0, unsigned long long& tests,
                                               unsigned long long& degen, int& nan) {
@@ -958,7 +994,7 @@ __device__ __forceinline__ void set_sweep_tsp(const LevelArgs& A, SetWarpSmem<L>
                     for (int k = 0; k < SP; ++k) {
                         if (((cand >> (t * SP + k)) & 1u) && g[k] < lim[t]) {
                             const double h01 = 0.5 * cij2[t] - 0.5 * s01[t][k];
-                            const int d = take_near(decide_slow(h01, den[t][k], A.th), A, row, S.tj[t * 32 + lane], h01, den[t][k]);
+                            const int d = take_near_row(decide_slow(h01, den[t][k], A.th), A, oi, S.tj[t * 32 + lane], h01, den[t][k]);
                             if (d != kDependent) {
                                 const int kk = t * 32 + lane;
                                 const bool dir1 = q[t] < lc;
@@ -1069,7 +1105,7 @@ __device__ __forceinline__ void h_terms_stream_sa(uint32_t sla, const double (&c
 // (rank-truncated inputs hit this often: ~29% of C2's level-3 sets), and the last-member
 // prefetch always targets the next LIVE set, so skipped sets cost no L2 round trip either.
 template <int L, int NT>
-__device__ __forceinline__ void set_sweep(const LevelArgs& A, SetWarpSmem<L>& S, int lane, int row, int oi, int lc, int nlive,
+__device__ __forceinline__ void set_sweep(const LevelArgs& A, SetWarpSmem<L>& S, int lane, int oi, int lc, int nlive,
                                           int nvalid, unsigned segmask, unsigned livemask, unsigned long long K0,
                                           unsigned long long& tests, unsigned long long& degen, int& nan) {
     const double* __restrict__ C = A.C;
@@ -1185,7 +1221,7 @@ __device__ __forceinline__ void set_sweep(const LevelArgs& A, SetWarpSmem<L>& S,
                 for (int t = 0; t < NT; ++t) {
                     if ((cand >> t) & 1u) {
                         const double h01 = 0.5 * cij2[t] - 0.5 * s01[t];  // == c_ij - 0.5 * (d01 + d10)
-                        const int d = take_near(decide_slow(h01, den[t], A.th), A, row, S.tj[t * 32 + lane], h01, den[t]);
+                        const int d = take_near_row(decide_slow(h01, den[t], A.th), A, oi, S.tj[t * 32 + lane], h01, den[t]);
                         if (d != kDependent) {
                             if (d == kNanError) nan = 1;
                             else {
@@ -1405,21 +1441,21 @@ __global__ void __launch_bounds__(kSetWarps * 32, PCS_SET_MINB) level_set_kernel
             const int nt = (nlive + 31) >> 5;
             if constexpr (SetCfg<L>::NT >= 4) {
                 constexpr int NTM = SetCfg<L>::NT;
-                if (nt > 3) set_sweep<L, NTM>(A, S, lane, i, oi, lc, nlive, nvalid, segmask, livemask, K0, tests, degen, nan);
-                else if (nt == 3) set_sweep<L, 3>(A, S, lane, i, oi, lc, nlive, nvalid, segmask, livemask, K0, tests, degen, nan);
-                else if (nt == 2) set_sweep<L, 2>(A, S, lane, i, oi, lc, nlive, nvalid, segmask, livemask, K0, tests, degen, nan);
-                else set_sweep<L, 1>(A, S, lane, i, oi, lc, nlive, nvalid, segmask, livemask, K0, tests, degen, nan);
+                if (nt > 3) set_sweep<L, NTM>(A, S, lane, oi, lc, nlive, nvalid, segmask, livemask, K0, tests, degen, nan);
+                else if (nt == 3) set_sweep<L, 3>(A, S, lane, oi, lc, nlive, nvalid, segmask, livemask, K0, tests, degen, nan);
+                else if (nt == 2) set_sweep<L, 2>(A, S, lane, oi, lc, nlive, nvalid, segmask, livemask, K0, tests, degen, nan);
+                else set_sweep<L, 1>(A, S, lane, oi, lc, nlive, nvalid, segmask, livemask, K0, tests, degen, nan);
             } else if constexpr (SetCfg<L>::NT == 3) {
-                if (nt == 3) set_sweep<L, 3>(A, S, lane, i, oi, lc, nlive, nvalid, segmask, livemask, K0, tests, degen, nan);
+                if (nt == 3) set_sweep<L, 3>(A, S, lane, oi, lc, nlive, nvalid, segmask, livemask, K0, tests, degen, nan);
 #if PCS_NT2_SP > 1
-                else if (nt == 2) set_sweep_tsp<L, 2, PCS_NT2_SP>(A, S, lane, i, oi, lc, nlive, nvalid, segmask, livemask, K0, tests, degen, nan);
+                else if (nt == 2) set_sweep_tsp<L, 2, PCS_NT2_SP>(A, S, lane, oi, lc, nlive, nvalid, segmask, livemask, K0, tests, degen, nan);
 #else
-                else if (nt == 2) set_sweep<L, 2>(A, S, lane, i, oi, lc, nlive, nvalid, segmask, livemask, K0, tests, degen, nan);
+                else if (nt == 2) set_sweep<L, 2>(A, S, lane, oi, lc, nlive, nvalid, segmask, livemask, K0, tests, degen, nan);
 #endif
-                else set_sweep_tsp<L, 1, PCS_SET_SP>(A, S, lane, i, oi, lc, nlive, nvalid, segmask, livemask, K0, tests, degen, nan);
+                else set_sweep_tsp<L, 1, PCS_SET_SP>(A, S, lane, oi, lc, nlive, nvalid, segmask, livemask, K0, tests, degen, nan);
             } else {
-                if (nt == 2) set_sweep<L, 2>(A, S, lane, i, oi, lc, nlive, nvalid, segmask, livemask, K0, tests, degen, nan);
-                else set_sweep_tsp<L, 1, 2>(A, S, lane, i, oi, lc, nlive, nvalid, segmask, livemask, K0, tests, degen, nan);
+                if (nt == 2) set_sweep<L, 2>(A, S, lane, oi, lc, nlive, nvalid, segmask, livemask, K0, tests, degen, nan);
+                else set_sweep_tsp<L, 1, 2>(A, S, lane, oi, lc, nlive, nvalid, segmask, livemask, K0, tests, degen, nan);
             }
             __syncwarp();
         }

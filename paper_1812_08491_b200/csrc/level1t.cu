@@ -55,7 +55,7 @@ __device__ __noinline__ void record_near1(const LevelArgs& A, int i, int j, int 
     if (k >= (unsigned long long)kNearCap) return;
     double z = 0.0, rho = 0.0;
     decide_exact(h01, denom, A.th.tau, &z, &rho);
-    A.near_rec[k] = NearRec{1, i, j, d, rho, z};
+    A.near_rec[k] = NearRec{1, i, j, d, rho, z, 0, 0};
 }
 
 struct __align__(128) L1TSmem {

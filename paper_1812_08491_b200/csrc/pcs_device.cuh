@@ -294,8 +294,9 @@ __device__ __forceinline__ int decide_fast(double h01, double denom, const Thres
     if (denom >= 1e-250 && A >= 1e-250) {
         if (A <= denom * th.lo2) return kIndependent;
         if (A >= denom * th.hi2) return kDependent;
+        return decide_exact(h01, denom, th.tau) | kNearBit;  // inside the +-1e-9 band
     }
-    return decide_exact(h01, denom, th.tau) | kNearBit;
+    return decide_exact(h01, denom, th.tau);  // tiny h01 or denom (e.g. an exactly zero statistic)
 }
 
 // Branch-free common-case filter: true only when decide_fast() is certainly

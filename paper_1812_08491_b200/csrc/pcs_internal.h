@@ -35,6 +35,8 @@ struct Counters {
 struct NearRec {
     int level, i, j, decision;  // decision: kDependent / kIndependent / kNanError
     double rho, z;
+    int oi, raw;                // raw = 1: written by a cuPC-S sweep as (row offset oi, h01 in rho, denom in z);
+                                // finished by launch_near_fixup before the snapshot changes
 };
 constexpr int kNearCap = 4096;  // records kept per run (the count is exact beyond)
 
@@ -111,6 +113,8 @@ void launch_edge_bounds(const LevelArgs& A, int pass, long long E, unsigned long
 // tiles [u_begin, min(u_end, prefix[p])) (u_end = ~0: the device-side total); bound = host upper bound
 void launch_level1(const LevelArgs& A, int pass, const unsigned long long* prefix, unsigned long long u_begin,
                    unsigned long long u_end, unsigned long long bound, int shard, int nsh, cudaStream_t s);
+// turns the raw near-threshold records of the current level into (row, rho, z)
+void launch_near_fixup(const LevelArgs& A, cudaStream_t s);
 // ---- level1t.cu: ell = 1, both directions, TMA-tiled (dense snapshots); rows [row_begin, row_end)
 // multi-GPU: shard `shard` of `nsh` takes every nsh-th 32-row block (cyclic)
 int launch_level1_tile(const LevelArgs& A, const uint32_t* adj, int W, int shard, int nsh, cudaStream_t s);
