@@ -466,11 +466,6 @@ LevelArgs level_args(pcs_session* s) {
     A.binom.stride = s->binom_stride;
     A.th = s->th;
     A.cnt = s->dCnt;
-    static const int filter = [] {
-        const char* e = std::getenv("PCS_FILTER");
-        return e ? std::atoi(e) : 1;
-    }();
-    A.filter = filter;
     return A;
 }
 
@@ -722,7 +717,7 @@ static pcs_status maybe_pinv_table(pcs_session* s, int ell) {
         return e ? std::atoi(e) : -1;
     }();
     s->use_pinv = false;
-    if (mode == 0 || (ell != 2 && ell != 3) || s->cfg.variant != PCS_VARIANT_SET) return PCS_OK;
+    if (mode == 0 || (ell != 2 && ell != 3)) return PCS_OK;  // both variants (cuPC-E: one lookup per test)
     const double n = (double)s->p;
     const double subsets = ell == 2 ? n * (n - 1) / 2 : n * (n - 1) * (n - 2) / 6;
     const double pairs = ell == 2 ? s->info.sets2 : s->info.sets3;
@@ -847,7 +842,7 @@ pcs_status pcs_session_snapshot(pcs_session* s, int32_t* offsets, int32_t* indic
     return PCS_OK;
 }
 
-unsigned long long pcs_kernel_launches(void) { return g_kernel_launches; }
+unsigned long long pcs_kernel_launches(void) { return g_kernel_launches.load(std::memory_order_relaxed); }
 
 pcs_status pcs_session_set_shard(pcs_session* s, int32_t shard_index, int32_t shard_count) {
     if (!s || shard_count < 1 || shard_index < 0 || shard_index >= shard_count)

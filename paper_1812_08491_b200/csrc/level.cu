@@ -24,7 +24,7 @@
 
 namespace pcs {
 
-unsigned long long g_kernel_launches = 0;
+std::atomic<unsigned long long> g_kernel_launches{0};
 
 #ifndef PCS_SET_DBUF
 #define PCS_SET_DBUF 0      // 1: two unrolled step copies ping-ponging the prefetch registers
@@ -1542,11 +1542,17 @@ __global__ void __launch_bounds__(128) level_edge_kernel(LevelArgs A, int pass, 
                     ciS[k] = __ldg(C + (size_t)i * ldc + mem[k]);
                     cjS[k] = __ldg(C + (size_t)j * ldc + mem[k]);
                 }
+                if (L <= 3 && A.pinv_table) {  // the level's pseudo-inverse table (same bits)
+                    const double* te = A.pinv_table + colex_rank<L>(mem) * (unsigned long long)PinvStride<L>::v;
 #pragma unroll
-                for (int x = 0; x < L; ++x)
+                    for (int q2 = 0; q2 < L * L; ++q2) minv[q2] = __ldg(te + q2);
+                } else {
 #pragma unroll
-                    for (int y = 0; y < L; ++y) m2[x * L + y] = __ldg(C + (size_t)mem[x] * ldc + mem[y]);
-                pinv<L>(m2, minv);
+                    for (int x = 0; x < L; ++x)
+#pragma unroll
+                        for (int y = 0; y < L; ++y) m2[x * L + y] = __ldg(C + (size_t)mem[x] * ldc + mem[y]);
+                    pinv<L>(m2, minv);
+                }
                 p0_terms<L>(minv, ciS, p0, h00);
                 h_terms<L>(minv, ciS, p0, h00, cjS, cij, h01, denom);
                 d = take_near(decide_fast(h01, denom, A.th), A, i, j, h01, denom);

@@ -1,6 +1,7 @@
 // pcs_internal.h -- shared declarations between the host driver (host.cu) and
 // the kernel translation units (level.cu, corr.cu).  Not part of the ABI.
 #pragma once
+#include <atomic>
 #include <cstdint>
 #include <string>
 #include <cuda_runtime.h>
@@ -10,7 +11,8 @@
 namespace pcs {
 
 // number of kernels this library has launched (diagnostics: bench.py's gpu_launches)
-extern unsigned long long g_kernel_launches;
+// (atomic: sessions on different host threads launch concurrently)
+extern std::atomic<unsigned long long> g_kernel_launches;
 // message returned by pcs_last_error() (host.cu)
 void set_last_error(const std::string& msg);
 
@@ -73,7 +75,6 @@ struct LevelArgs {
     BinomTable binom;
     Thresholds th;
     Counters* cnt;
-    int filter;  // 1: cuPC-S may use the certified FMA filter (PCS_FILTER=0 disables; results identical)
 };
 
 // ---- corr.cu

@@ -135,6 +135,11 @@ for s in $STEPS; do
         PCS_PINV_TABLE=$v timeout 900 python tools/explore.py C5a,C5c set 2 2 >> $OUT/pinvtab_$v.log 2>&1
       done
       ;;
+    edgetab)
+      for v in 0 2; do PCS_PINV_TABLE=$v timeout 900 python tools/explore.py C2 edge 2 2 >> $OUT/edgetab_$v.log 2>&1; done
+      timeout 1200 python -m pytest tests/test_gpu_golden.py tests/test_gpu_random_sweep.py tests/test_gpu_parity.py -x -q \
+        > $OUT/pytest_edgetab.log 2>&1; echo "rc=$?" >> $OUT/pytest_edgetab.log
+      ;;
     bench)
       timeout 900 python bench.py > $OUT/bench.json 2> $OUT/bench.err
       ;;

@@ -32,6 +32,7 @@ CASES = {
     "C4": (5361, 63, 0.002, 3 * 7919, None, False, (2, 3, 4)),
     "C5_2000": (2000, 5000, 0.05, 4 * 7919, 2, True, ()),
     "C5_5000": (5000, 5000, 0.05, 4 * 7919, 1, True, ()),
+    "C5_10000": (10000, 5000, 0.05, 7 * 7919, 1, True, ()),
 }
 ALPHA = 0.01
 
