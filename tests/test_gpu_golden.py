@@ -8,7 +8,8 @@ pseudo_inverses / edges_removed, the remaining edges and the stop reason (tests/
 The device correlation matrix is first checked bit for bit against the oracle's restatement of the
 device order (pyoracle.compute_correlation_fma), so the fixtures' correlation and the device's are
 the same bits.  C2 is BASELINE configs[1] (the bench headline, capped at level 3 like the bench);
-C5_2000 / C5_5000 are scaling-sweep shapes (levels 0-2 / 0-1)."""
+C5_2000 / C5_5000 / C5_10000 are scaling-sweep shapes (levels 0-2 / 0-1 / 0-1; the last runs the tiled
+level-1 kernel over 157 target bands, i.e. ten L2 groups)."""
 import hashlib
 import os
 import time
@@ -32,7 +33,14 @@ def _load(name):
 
 def _data(pcs, oracle, g):
     p, m, d, seed = int(g["p"]), int(g["m"]), float(g["density"]), int(g["seed"])
-    if bool(g["rescaled"]):
+    if bool(g["rescaled"]) and p >= 10000:  # the device generator (bit-identical, test_gpu_datagen.py)
+        import torch
+
+        w = pcs.random_dag(p, d, seed)
+        xd = torch.empty((p, m), dtype=torch.float64, device="cuda")
+        pcs.sample_linear_gaussian_device(w, m, seed + 1, xd.data_ptr(), rescaled=True)
+        x = xd.cpu().numpy()
+    elif bool(g["rescaled"]):
         w = pcs.random_dag(p, d, seed)
         x, _ = pcs.sample_linear_gaussian_rescaled(w, m, seed + 1)
         x = np.ascontiguousarray(np.asarray(x).T)
@@ -56,7 +64,7 @@ def test_device_correlation_bits(pcs, oracle, name):
 
 @pytest.mark.parametrize("name,variant", [("C1", "set"), ("C1", "edge"), ("C3", "set"), ("C3", "edge"),
                                           ("C4", "set"), ("C4", "edge"), ("C2", "set"), ("C5_2000", "set"),
-                                          ("C5_5000", "set")])
+                                          ("C5_5000", "set"), ("C5_10000", "set")])
 def test_whole_run_matches_golden(pcs, oracle, name, variant):
     g = _load(name)
     x = _data(pcs, oracle, g)
