@@ -140,6 +140,10 @@ for s in $STEPS; do
       timeout 1200 python -m pytest tests/test_gpu_golden.py tests/test_gpu_random_sweep.py tests/test_gpu_parity.py -x -q \
         > $OUT/pytest_edgetab.log 2>&1; echo "rc=$?" >> $OUT/pytest_edgetab.log
       ;;
+    ncul2)
+      timeout 900 ncu --set full --clock-control none --import-source on -k regex:level_set_kernel -c 1 -f -o $OUT/l2 \
+        python tools/explore.py C5a set 2 > $OUT/ncu_l2.log 2>&1
+      ;;
     bench)
       timeout 900 python bench.py > $OUT/bench.json 2> $OUT/bench.err
       ;;
