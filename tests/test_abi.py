@@ -88,3 +88,16 @@ def test_rescaled_generator_is_the_reference_generator_scaled(oracle):
     x, ls = pcs.sample_linear_gaussian_rescaled(w, 8, 6)
     assert np.isfinite(x).all() and np.isfinite(ls).all() and ls.max() > 709.0
     assert np.allclose((x ** 2).mean(axis=0), 1.0, rtol=1e-12)
+
+
+@pytest.mark.parametrize("seed,p,m", [(5, 7, 11), (7919, 100, 1000), (3, 1000, 301)])
+def test_noise_stream_is_the_sequential_stream(oracle, seed, p, m):
+    """pcs_noise_stream (jump-ahead chunks of 65536 outputs on the host threads) == the reference's
+    sequential xoshiro256++ / polar stream (rng.hpp), restated by the oracle; the larger shapes cross
+    several chunk boundaries, and an odd count drops the last spare."""
+    import paper_1812_08491_b200 as pcs
+    got = pcs.noise_stream(seed, p * m, p, m)
+    want = oracle.normals(seed, p * m).reshape(m, p).T
+    assert np.array_equal(got.view(np.int64), want.view(np.int64))
+    odd = pcs.noise_stream(seed, p * m - 1, p, m)
+    assert np.array_equal(odd.T.reshape(-1)[:p * m - 1].view(np.int64), want.T.reshape(-1)[:p * m - 1].view(np.int64))
