@@ -90,7 +90,7 @@ void launch_near_fixup(const LevelArgs& A, cudaStream_t s) {
 }
 
 #ifndef PCS_SET_NT_SMALL
-#define PCS_SET_NT_SMALL 3  // targets per lane per set for L <= 3 (tuning knob, results identical)
+#define PCS_SET_NT_SMALL 4  // targets per lane per set for L = 3 (tuning knob, results identical; 4: -5% on C2 L3 with the pinv table)
 #endif
 #ifndef PCS_UNRANK_BSEARCH
 #define PCS_UNRANK_BSEARCH 0  // 1: phase-1 unrank by per-member binary search over the binomial table
@@ -1439,7 +1439,17 @@ __global__ void __launch_bounds__(kSetWarps * 32, PCS_SET_MINB) level_set_kernel
             __syncwarp();
             // ---- phase 2: sets in rank order, NT targets per lane
             const int nt = (nlive + 31) >> 5;
-            if constexpr (SetCfg<L>::NT >= 4) {
+            if constexpr (SetCfg<L>::NT >= 4 && L <= 3) {  // partially filled batches as in the NT = 3 case
+                constexpr int NTM = SetCfg<L>::NT;
+                if (nt > 3) set_sweep<L, NTM>(A, S, lane, oi, lc, nlive, nvalid, segmask, livemask, K0, tests, degen, nan);
+                else if (nt == 3) set_sweep<L, 3>(A, S, lane, oi, lc, nlive, nvalid, segmask, livemask, K0, tests, degen, nan);
+#if PCS_NT2_SP > 1
+                else if (nt == 2) set_sweep_tsp<L, 2, PCS_NT2_SP>(A, S, lane, oi, lc, nlive, nvalid, segmask, livemask, K0, tests, degen, nan);
+#else
+                else if (nt == 2) set_sweep<L, 2>(A, S, lane, oi, lc, nlive, nvalid, segmask, livemask, K0, tests, degen, nan);
+#endif
+                else set_sweep_tsp<L, 1, PCS_SET_SP>(A, S, lane, oi, lc, nlive, nvalid, segmask, livemask, K0, tests, degen, nan);
+            } else if constexpr (SetCfg<L>::NT >= 4) {
                 constexpr int NTM = SetCfg<L>::NT;
                 if (nt > 3) set_sweep<L, NTM>(A, S, lane, oi, lc, nlive, nvalid, segmask, livemask, K0, tests, degen, nan);
                 else if (nt == 3) set_sweep<L, 3>(A, S, lane, oi, lc, nlive, nvalid, segmask, livemask, K0, tests, degen, nan);

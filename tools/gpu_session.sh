@@ -145,7 +145,8 @@ for s in $STEPS; do
         python tools/explore.py C5a set 2 > $OUT/ncu_l2.log 2>&1
       ;;
     ntvar)
-      timeout 1200 python tools/variants.py run nt4 nt4m3 nt2sp1 sp1 --workload C2 --max-level 3 --repeats 2 > $OUT/ntvar_c2.json 2> $OUT/ntvar.err
+      timeout 1200 python tools/variants.py run ntl2x4 --workload C2 --max-level 2 --repeats 3 > $OUT/ntvar_c2.json 2> $OUT/ntvar.err
+      timeout 1200 python tools/variants.py run ntl2x4 --workload C5 --max-level 2 --repeats 1 > $OUT/ntvar_c5.json 2>> $OUT/ntvar.err
       ;;
     bench)
       timeout 900 python bench.py > $OUT/bench.json 2> $OUT/bench.err
