@@ -144,6 +144,10 @@ for s in $STEPS; do
       timeout 900 ncu --set full --clock-control none --import-source on -k regex:level_set_kernel -c 1 -f -o $OUT/l2 \
         python tools/explore.py C5a set 2 > $OUT/ncu_l2.log 2>&1
       ;;
+    l2wide)
+      timeout 1500 python tools/explore.py C5b set 2 > $OUT/l2wide.log 2>&1
+      timeout 1200 python -m pytest tests/test_gpu_random_sweep.py tests/test_gpu_golden.py -x -q > $OUT/pytest_l2wide.log 2>&1; echo "rc=$?" >> $OUT/pytest_l2wide.log
+      ;;
     ntvar)
       timeout 1200 python tools/variants.py run ntl2x4 --workload C2 --max-level 2 --repeats 3 > $OUT/ntvar_c2.json 2> $OUT/ntvar.err
       timeout 1200 python tools/variants.py run ntl2x4 --workload C5 --max-level 2 --repeats 1 > $OUT/ntvar_c5.json 2>> $OUT/ntvar.err
