@@ -148,6 +148,9 @@ for s in $STEPS; do
       timeout 1500 python tools/explore.py C5b set 2 > $OUT/l2wide.log 2>&1
       timeout 1200 python -m pytest tests/test_gpu_random_sweep.py tests/test_gpu_golden.py -x -q > $OUT/pytest_l2wide.log 2>&1; echo "rc=$?" >> $OUT/pytest_l2wide.log
       ;;
+    c2l4)
+      timeout 2400 python tools/explore.py C2 set 4 > $OUT/c2_level4.log 2>&1
+      ;;
     ntvar)
       timeout 1200 python tools/variants.py run ntl2x4 --workload C2 --max-level 2 --repeats 3 > $OUT/ntvar_c2.json 2> $OUT/ntvar.err
       timeout 1200 python tools/variants.py run ntl2x4 --workload C5 --max-level 2 --repeats 1 > $OUT/ntvar_c5.json 2>> $OUT/ntvar.err
