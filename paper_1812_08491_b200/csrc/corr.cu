@@ -317,15 +317,15 @@ typedef CUresult (*G2EncodeFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, vo
 
 // Xc (p x ldk, row-major) as a TMA tensor; 0 on success
 static int gram2_map(CUtensorMap* m, const double* Xc, int p, int ldk) {
-    static G2EncodeFn fn = nullptr;
-    if (!fn) {
+    static const G2EncodeFn fn = [] {  // thread-safe one-time lookup
         void* f = nullptr;
         cudaDriverEntryPointQueryResult q;
         if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) != cudaSuccess ||
             q != cudaDriverEntryPointSuccess)
-            return 1;
-        fn = reinterpret_cast<G2EncodeFn>(f);
-    }
+            return static_cast<G2EncodeFn>(nullptr);
+        return reinterpret_cast<G2EncodeFn>(f);
+    }();
+    if (!fn) return 1;
     cuuint64_t dims[2] = {(cuuint64_t)ldk, (cuuint64_t)p};
     cuuint64_t strides[1] = {(cuuint64_t)ldk * sizeof(double)};
     cuuint32_t box[2] = {(cuuint32_t)kG2Box, (cuuint32_t)kG2T};
