@@ -142,6 +142,7 @@ Thresholds make_thresholds(double tau) {
         th.hi = INFINITY;
         th.hi2 = INFINITY;
     }
+    th.hi2x4 = 4.0 * th.hi2;
     return th;
 }
 

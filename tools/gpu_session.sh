@@ -152,8 +152,7 @@ for s in $STEPS; do
       timeout 2400 python tools/explore.py C2 set 4 > $OUT/c2_level4.log 2>&1
       ;;
     ntvar)
-      timeout 1200 python tools/variants.py run ntl2x4 --workload C2 --max-level 2 --repeats 3 > $OUT/ntvar_c2.json 2> $OUT/ntvar.err
-      timeout 1200 python tools/variants.py run ntl2x4 --workload C5 --max-level 2 --repeats 1 > $OUT/ntvar_c5.json 2>> $OUT/ntvar.err
+      timeout 1200 python tools/variants.py run fsign fsignsb --workload C2 --max-level 3 --repeats 2 > $OUT/ntvar_c2.json 2> $OUT/ntvar.err
       ;;
     bench)
       timeout 900 python bench.py > $OUT/bench.json 2> $OUT/bench.err
