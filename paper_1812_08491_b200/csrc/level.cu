@@ -107,9 +107,6 @@ void launch_near_fixup(const LevelArgs& A, cudaStream_t s) {
 #define PCS_SBASE_OPAQUE 1  // the step loop's shared slot base pinned in a register (no per-step
                             // rematerialisation); 0: A/B
 #endif
-#ifndef PCS_FQ_FILTER
-#define PCS_FQ_FILTER 0     // the step loop certifies tests by the quadratic-form filter (l <= kFqMaxL); 0: A/B
-#endif
 #ifndef PCS_SMEM_PTX
 #define PCS_SMEM_PTX 1      // 1: the step loop reads the set slots by 32-bit shared addresses (inline PTX)
 #endif
@@ -758,9 +755,6 @@ struct alignas(16) SetSlot {
     // column c of the set's test data, 16 B aligned for LDS.128:
     //   {M2^+[0][c], ..., M2^+[L-1][c], C(i,S)[c], P0[c], (pad)}
     static constexpr int CW = (L + 3) / 2 * 2;
-    static constexpr bool kFq = PCS_FQ_FILTER && L <= kFqMaxL;  // the step loop's quadratic-form filter
-    static constexpr int FW = kFq ? FilterQ<L>::W : 2;
-    double fq[FW];  // filter_consts<L> (pcs_device.cuh), read every step
     double col[L][CW];
     double h00, pad;
     int pos[L];
@@ -997,37 +991,14 @@ __device__ __forceinline__ void set_sweep_tsp(const LevelArgs& A, SetWarpSmem<L>
 #pragma unroll
             for (int k = 0; k < SP; ++k) sls[k] = &S.slot[g[k] < nvalid ? g[k] : g[0]];
             double s01[NT][SP], h2[NT][SP], den[NT][SP];
+            h_terms_tsp<L, NT, SP, LP>(sls, cp, nxt, cij2, s01, h2, den);
             unsigned cand = 0;
-            if constexpr (SetSlot<L>::kFq) {  // the quadratic-form filter; reference-order terms only if needed
 #pragma unroll
-                for (int k = 0; k < SP; ++k) {
-                    double fq[FilterQ<L>::W];
+            for (int t = 0; t < NT; ++t)
 #pragma unroll
-                    for (int c = 0; c < FilterQ<L>::W; c += 2) {
-                        const double2 v = *reinterpret_cast<const double2*>(&sls[k]->fq[c]);
-                        fq[c] = v.x;
-                        fq[c + 1] = v.y;
-                    }
-#pragma unroll
-                    for (int t = 0; t < NT; ++t) {
-                        double x[L];
-#pragma unroll
-                        for (int a = 0; a < L - 1; ++a) x[a] = cp[t][a];
-                        x[L - 1] = nxt[t][k];
-                        cand |= (unsigned)((g[k] < seg_end) & (g[k] < lim[t]) & (g[k] != dm[t]) &
-                                           fq_uncertain<L>(fq, x, cij2[t])) << (t * SP + k);
-                    }
-                }
-                if (__any_sync(0xffffffffu, cand)) h_terms_tsp<L, NT, SP, LP>(sls, cp, nxt, cij2, s01, h2, den);
-            } else {
-                h_terms_tsp<L, NT, SP, LP>(sls, cp, nxt, cij2, s01, h2, den);
-#pragma unroll
-                for (int t = 0; t < NT; ++t)
-#pragma unroll
-                    for (int k = 0; k < SP; ++k)
-                        cand |= (unsigned)((g[k] < seg_end) & (g[k] < lim[t]) & (g[k] != dm[t]) &
-                                           !SURELY_DEP(h2[t][k], den[t][k], hi2x4)) << (t * SP + k);
-            }
+                for (int k = 0; k < SP; ++k)
+                    cand |= (unsigned)((g[k] < seg_end) & (g[k] < lim[t]) & (g[k] != dm[t]) &
+                                       !SURELY_DEP(h2[t][k], den[t][k], hi2x4)) << (t * SP + k);
             if (__any_sync(0xffffffffu, cand)) {
 #pragma unroll
                 for (int t = 0; t < NT; ++t) {
@@ -1136,32 +1107,6 @@ __device__ __forceinline__ void h_terms_stream_sa(uint32_t sla, const double (&c
     }
 }
 
-// The quadratic-form filter (fq_uncertain, pcs_device.cuh) for NT targets against the set at shared
-// address sla: bit t set when target t's test is NOT certified dependent.  The constants are read once
-// per set (FilterQ<L>::W / 2 16-byte loads) and shared by the NT targets.
-template <int L, int NT, int LP>
-__device__ __forceinline__ unsigned fq_uncertain_sa(uint32_t sla, const double (&cp)[NT][LP], const double (&cur)[NT],
-                                                    const double (&cij2)[NT]) {
-    constexpr int W = FilterQ<L>::W;
-    double fq[W];
-#pragma unroll
-    for (int k = 0; k < W; k += 2) {
-        const double2 v = lds_f64x2(sla + (uint32_t)offsetof(SetSlot<L>, fq) + (uint32_t)(k * sizeof(double)));
-        fq[k] = v.x;
-        fq[k + 1] = v.y;
-    }
-    unsigned un = 0;
-#pragma unroll
-    for (int t = 0; t < NT; ++t) {
-        double x[L];
-#pragma unroll
-        for (int a = 0; a < L - 1; ++a) x[a] = cp[t][a];
-        x[L - 1] = cur[t];
-        un |= (unsigned)fq_uncertain<L>(fq, x, cij2[t]) << t;
-    }
-    return un;
-}
-
 // Phase 2 for one staged batch of targets, NT (<= SetCfg<L>::NT) per lane.
 // segmask: bit s set when set s starts a new run of equal leading L-1 members.  Inside a
 // run (lexicographic order) the last member's position advances by one per set: set
@@ -1248,53 +1193,9 @@ __device__ __forceinline__ void set_sweep(const LevelArgs& A, SetWarpSmem<L>& S,
                 dm[t] = sg0 + q - base;
             }
         }
-        // the exact rule for the candidate tests of set sgx (bit t of cand), from the reference-order terms
-        auto resolve = [&](int sgx, unsigned cand, const double (&s01)[NT], const double (&den)[NT]) {
-#pragma unroll
-            for (int t = 0; t < NT; ++t) {
-                if ((cand >> t) & 1u) {
-                    const double h01 = 0.5 * cij2[t] - 0.5 * s01[t];  // == c_ij - 0.5 * (d01 + d10)
-                    const int d = take_near_row(decide_slow(h01, den[t], A.th), A, oi, S.tj[t * 32 + lane], h01, den[t]);
-                    if (d != kDependent) {
-                        if (d == kNanError) nan = 1;
-                        else {
-                            const int k = t * 32 + lane;
-                            const bool dir1 = S.tq[k] < lc;
-                            record_find(A, oi, S.tq[k], S.te[k], S.tj[k], dir1,
-                                        (dir1 ? (K0 | (1ull << kDirShift)) : K0) + (unsigned long long)sgx);
-                        }
-                        rel[t] = sgx;
-                        lim[t] = sgx;
-                        hit |= 1u << t;
-                    }
-                }
-            }
-        };
         // double-buffered last-member gathers: step(s, n, cur, pre) tests live set s with `cur` while
         // prefetching live set n (the next one, possibly in a later run) into `pre`
         auto step = [&](int sgx, int nxs, const double (&cur)[NT], double (&pre)[NT]) {
-#if PCS_SMEM_PTX
-            if constexpr (SetSlot<L>::kFq) {
-                const uint32_t sla = slot0 + (uint32_t)(sgx * (int)sizeof(SetSlot<L>));
-                {  // clamped: always a valid slot
-                    const int ro = lds_s32(slot0 + (uint32_t)(min(nxs, nvalid - 1) * (int)sizeof(SetSlot<L>)) +
-                                           (uint32_t)(offsetof(SetSlot<L>, roff) + (L - 1) * sizeof(int)));
-#pragma unroll
-                    for (int t = 0; t < NT; ++t) pre[t] = __ldg(Cj[t] + ro);
-                }
-                const unsigned un = fq_uncertain_sa<L, NT, LP>(sla, cp, cur, cij2);
-                unsigned cand = 0;
-#pragma unroll
-                for (int t = 0; t < NT; ++t) cand |= (unsigned)((sgx < lim[t]) & (sgx != dm[t])) << t;
-                cand &= un;
-                if (__any_sync(0xffffffffu, cand)) {  // rare: the reference-order terms, then the exact rule
-                    double s01[NT], h2[NT], den[NT];
-                    h_terms_stream_sa<L, NT, LP>(sla, cp, cur, cij2, s01, h2, den);
-                    resolve(sgx, cand, s01, den);
-                }
-                return;
-            }
-#endif
 #if PCS_SMEM_PTX
             {  // clamped: always a valid slot
                 const int ro = lds_s32(slot0 + (uint32_t)(min(nxs, nvalid - 1) * (int)sizeof(SetSlot<L>)) +
@@ -1330,7 +1231,27 @@ __device__ __forceinline__ void set_sweep(const LevelArgs& A, SetWarpSmem<L>& S,
                 }
             }
 #endif
-            if (__any_sync(0xffffffffu, cand)) resolve(sgx, cand, s01, den);
+            if (__any_sync(0xffffffffu, cand)) {
+#pragma unroll
+                for (int t = 0; t < NT; ++t) {
+                    if ((cand >> t) & 1u) {
+                        const double h01 = 0.5 * cij2[t] - 0.5 * s01[t];  // == c_ij - 0.5 * (d01 + d10)
+                        const int d = take_near_row(decide_slow(h01, den[t], A.th), A, oi, S.tj[t * 32 + lane], h01, den[t]);
+                        if (d != kDependent) {
+                            if (d == kNanError) nan = 1;
+                            else {
+                                const int k = t * 32 + lane;
+                                const bool dir1 = S.tq[k] < lc;
+                                record_find(A, oi, S.tq[k], S.te[k], S.tj[k], dir1,
+                                            (dir1 ? (K0 | (1ull << kDirShift)) : K0) + (unsigned long long)sgx);
+                            }
+                            rel[t] = sgx;
+                            lim[t] = sgx;
+                            hit |= 1u << t;
+                        }
+                    }
+                }
+            }
         };
 #if PCS_SET_DBUF
         while (nl < seg_end) {
@@ -1511,7 +1432,6 @@ __global__ void __launch_bounds__(kSetWarps * 32, PCS_SET_MINB) level_set_kernel
                         sl.roff[a] = mem[a] * (int)ldc;  // p * ldc < 2^31 (p <= 46340)
                     }
                     sl.h00 = h00;
-                    if constexpr (SetSlot<L>::kFq) filter_consts<L>(minv, p0, h00, A.th.hi2x4, sl.fq);
                 }
 #ifdef PCS_PHASE1_REPS
                 }

@@ -348,90 +348,6 @@ __device__ __forceinline__ bool surely_dependent3(double h2, double denom, doubl
     return h2 * h2 >= fma(denom, hi2x4, kTiny4);
 }
 
-// ---------------------------------------------------------------------------------------------
-// The quadratic-form filter (cuPC-S step loop, l <= kFqMaxL): certifies surely_dependent2 on the
-// reference-rounded (h2, denom) WITHOUT computing them, from per-set constants built once in phase 1.
-//
-// Per test (x = C(j, S) in [-1, 1]^L, cij2 = 2 c_ij):
-//   h = cij2 - 2 P0 . x                         L FMAs          (approximates h2_ref = 2 h01)
-//   g = c0 - x^T Ms x                           L(L+1)/2 + L    (approximates H denom + margin)
-//   r = RN(RN(h^2 - g) - 2E |h|)                2 FMAs; certified iff sign(r) = + (integer test)
-// with Ms = s (M + M^T)/2 stored as its upper triangle (off-diagonal doubled), s = h00 H,
-// H = hi2x4, c0 = s + K.  14 FP64 operations at l = 3 instead of h_terms' 34 + 2.
-//
-// Soundness (u = 2^-53, gamma_n <= 1.01 n u, |x|, |c_ij| <= 1 for a validated C, A = sum |M_kc|,
-// B = sum |P0_c|, Asym = sum |M_kc - M_ck|; h11* = 1 - x^T M x, den* = h00 h11*, h2* = cij2 - 2 P0 . x
-// on the stored floats):
-//   |den_ref - den*| <= |h00| (4L + 6) u (1 + A)         (P1, d11 chains + the two last roundings)
-//   |h2_ref - h2*|   <= Asym + u (2 + (3.04L + 2.04)(A + B))  (d01, d10, the P0 rounding, s01, h2)
-//   |h - h2*|        <= 1.01 L u (2 + 2B)
-//   g >= H den* + K - (2.04L + 4.01) u (K + |s| (1 + A))   (constant scaling + the FMA chains)
-// so with K = (T + (8L + 16) u |s| (1 + A))(1 + 2^-40) (T = 4e-240) g >= H den_ref + T, and with
-// E = (Asym + (8L + 8) u (1 + A + B))(1 + 2^-40) |h2_ref| >= |h| - E.  A non-negative r means
-// h^2 - g >= 2E|h| (RN is monotone and keeps the sign; the 2^-40 slack covers the rounding of
-// q): if den_ref >= 0 then g > 0, so |h| > 2E and h2_ref^2 >= (|h| - E)^2 >= g >= H den_ref + T, which
-// is surely_dependent2's comparison on the real numbers (RN monotone); if den_ref < 0 it is
-// surely_dependent2's degenerate branch.  Either way the reference decides "dependent".
-// Constants above 2^500 (near-singular M2, or hi2 = +inf) switch the set to "never certify"
-// (c0 = +inf, the rest 0: r = -inf), keeping every intermediate finite when certifying.
-constexpr int kFqMaxL = 4;
-template <int L>
-struct FilterQ {
-    static constexpr int NQ = L * (L + 1) / 2;  // upper triangle of Ms
-    static constexpr int N = L + 1 + NQ + 1;    // [-2 P0 (L), -2E, Ms (NQ), c0]
-    static constexpr int W = (N + 1) / 2 * 2;   // padded for 16-byte loads
-};
-
-template <int L>
-__device__ __forceinline__ void filter_consts(const double (&Minv)[L * L], const double (&P0)[L], double h00, double H,
-                                              double* fq) {
-    constexpr double u = 1.1102230246251565e-16, slack = 1.0 + 0x1p-40, kT = 4.0 * 1e-240, kBig = 0x1p500;
-    double A = 0.0, B = 0.0, As = 0.0;
-#pragma unroll
-    for (int k = 0; k < L; ++k) {
-        B += fabs(P0[k]);
-#pragma unroll
-        for (int c = 0; c < L; ++c) {
-            A += fabs(Minv[k * L + c]);
-            As += fabs(Minv[k * L + c] - Minv[c * L + k]);
-        }
-    }
-    const double s = h00 * H;
-    const double K = (kT + (8 * L + 16) * u * fabs(s) * (1.0 + A)) * slack;
-    const double E = (As + (8 * L + 8) * u * (1.0 + A + B)) * slack;
-    bool ok = fabs(s) * A <= kBig && K <= kBig && E <= kBig && B <= kBig && fabs(s) <= kBig;  // false on NaN / inf
-#pragma unroll
-    for (int k = 0; k < L; ++k) fq[k] = ok ? -2.0 * P0[k] : 0.0;
-    fq[L] = ok ? -2.0 * E * slack : 0.0;
-    int q = L + 1;
-#pragma unroll
-    for (int k = 0; k < L; ++k)
-#pragma unroll
-        for (int c = k; c < L; ++c, ++q)
-            fq[q] = ok ? s * (c == k ? Minv[k * L + k] : Minv[k * L + c] + Minv[c * L + k]) : 0.0;
-    fq[q] = ok ? s + K : INFINITY;
-    if (FilterQ<L>::W > FilterQ<L>::N) fq[FilterQ<L>::W - 1] = 0.0;
-}
-
-// The filter for one (set, target): true when the test is NOT certified dependent.
-template <int L>
-__device__ __forceinline__ bool fq_uncertain(const double* fq, const double (&x)[L], double cij2) {
-    double h = cij2;
-#pragma unroll
-    for (int k = 0; k < L; ++k) h = fma(fq[k], x[k], h);
-    double g = fq[FilterQ<L>::N - 1];
-#pragma unroll
-    for (int k = L - 1; k >= 0; --k) {  // row k of the triangle, Ms[k][k..L-1] at fq[L + 1 + off]
-        const int off = L + 1 + k * L - k * (k - 1) / 2;
-        double t = fq[off] * x[k];
-#pragma unroll
-        for (int c = k + 1; c < L; ++c) t = fma(fq[off + (c - k)], x[c], t);
-        g = fma(-x[k], t, g);
-    }
-    const double r = fma(fabs(h), fq[L], fma(h, h, -g));
-    return __double2hiint(r) < 0;
-}
-
 // Level-0 decision on rho = clamp(c_ij) (stats.hpp:309-312).
 __device__ __forceinline__ int decide0(double c, const Thresholds& th) {
     const double ac = fabs(c);

@@ -61,7 +61,7 @@ for s in $STEPS; do
       timeout 900 python tools/shard_balance.py 8 C4 -1 set >> $OUT/balance.json 2>> $OUT/balance.err
       ;;
     candtrace)
-      PCS_TRACE=1 timeout 900 python tools/variants.py run cand --workload C2 --max-level 3 --repeats 1 > $OUT/cand.json 2> $OUT/cand.err
+      PCS_TRACE=1 timeout 900 python tools/variants.py run ${CANDV:-cand} --workload C2 --max-level 3 --repeats 1 > $OUT/cand.json 2> $OUT/cand.err
       ;;
     variantsl2)
       timeout 1500 python tools/variants.py run --workload C5 --max-level 2 --repeats 1 > $OUT/variants_c5l2.json 2> $OUT/variants_c5l2.err
@@ -152,7 +152,11 @@ for s in $STEPS; do
       timeout 2400 python tools/explore.py C2 set 4 > $OUT/c2_level4.log 2>&1
       ;;
     ntvar)
-      timeout 1200 python tools/variants.py run fsign fsignsb --workload C2 --max-level 3 --repeats 2 > $OUT/ntvar_c2.json 2> $OUT/ntvar.err
+      timeout 1200 python tools/variants.py run $VARIANTS --workload C2 --max-level 3 --repeats 2 > $OUT/ntvar_c2.json 2> $OUT/ntvar.err
+      ;;
+    ntvar5)
+      timeout 1500 python tools/variants.py run $VARIANTS --workload C5 --max-level 2 --repeats 1 > $OUT/ntvar_c5.json 2> $OUT/ntvar5.err
+      timeout 900 python tools/variants.py run $VARIANTS --workload C3 --max-level -1 --repeats 3 > $OUT/ntvar_c3.json 2>> $OUT/ntvar5.err
       ;;
     bench)
       timeout 900 python bench.py > $OUT/bench.json 2> $OUT/bench.err
