@@ -656,7 +656,7 @@ pcs_status pcs_session_level_begin(pcs_session* s, int32_t* running, int32_t* el
         if ((st = realloc_dev(s, &s->dNbr, s->info.e_dir))) return st;
         if ((st = realloc_dev(s, &s->dEid, s->info.e_dir))) return st;
         if ((st = realloc_dev(s, &s->dKdir, s->info.e_dir))) return st;
-        if ((st = realloc_dev(s, &s->dCnbr, s->info.e_dir))) return st;
+        if ((st = realloc_dev(s, &s->dCnbr, s->info.e_dir + 2))) return st;  // +2: the staged cuPC-E bulk copy's even-aligned superset
         s->capDir = s->info.e_dir;
     }
     if (s->info.e_und > s->capUnd) {
@@ -823,7 +823,7 @@ pcs_status pcs_session_level_pass(pcs_session* s, int32_t pass) {
             e0 = (long long)b[0];
             e1 = (long long)b[1];
         }
-        if (e1 > e0 && launch_level_edge(A, pass, e0, e1, s->num_sms, s->st))
+        if (e1 > e0 && launch_level_edge(A, pass, e0, e1, s->info.max_width, s->num_sms, s->st))
             return fail(PCS_EUNSUPPORTED, "level not supported by the edge kernel");
     }
     CUDA_TRY(cudaGetLastError());

@@ -1601,10 +1601,193 @@ __global__ void __launch_bounds__(128) level_edge_kernel(LevelArgs A, int pass, 
     if (nan) atomicOr(&A.cnt->err_nan, 1);
 }
 
+// ----------------------------------------------------------- cuPC-E, staged operands
+// The same warp-per-edge schedule (lanes over the edge's conditioning sets in rank order, 32 per
+// round, ballot early exit at the first separating set), with the edge's correlation sub-block in
+// shared memory instead of 2L + 1 L2 gathers per test:
+//   ci[k] = C(i, nbr_i[k])  the contiguous C(i, nbr) segment of row i (A.cnbr), one 1-D TMA bulk copy
+//                           (cp.async.bulk, mbarrier transaction count) issued by lane 0;
+//   cj[k] = C(j, nbr_i[k])  a gather (the other lanes, concurrently with the bulk copy);
+//   nb[k] = nbr_i[k].
+// A test then reads its members, C(i, S) and C(j, S) from shared memory; its set comes from
+// unrank_est (one estimate + fix-up per member instead of a binary search) and, at l = 2, 3, its
+// M2^+ from the level's pseudo-inverse table.  Decisions, keys and counters are those of
+// level_edge_kernel (same h_terms / decide_fast, same ranks).
+namespace {
+__device__ __forceinline__ uint32_t smem_addr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void bar_init(unsigned long long* bar) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(bar)) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void bar_wait(unsigned long long* bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred P1;\n"
+        "EWAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+        "@!P1 bra EWAIT_%=;\n}" ::"r"(smem_addr(bar)),
+        "r"(parity)
+        : "memory");
+}
+// one bulk copy of `bytes` (a multiple of 16, both addresses 16-B aligned) completing on `bar`
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes, unsigned long long* bar) {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)), "r"(bytes) : "memory");
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_addr(dst)),
+                 "l"(reinterpret_cast<unsigned long long>(src)), "r"(bytes), "r"(smem_addr(bar))
+                 : "memory");
+}
+}  // namespace
+
+constexpr int kEdgeWarps = 4;
+// per-warp shared bytes for rows up to wcap entries (wcap a multiple of 4): barrier, ci (+2 for the
+// aligned superset the bulk copy brings), cj, nb
+__host__ __device__ inline size_t edge_warp_smem(int wcap) { return 16 + (size_t)(wcap + 2) * 8 + (size_t)wcap * 12; }
+constexpr size_t kEdgeSmemMax = 200 * 1024;  // per block; wider rows use level_edge_kernel
+
+#ifndef PCS_EDGE_SPL
+#define PCS_EDGE_SPL 1  // staged cuPC-E: conditioning sets per lane per round at l <= 3 (2: same time, 4: +12%)
+#endif
 template <int L>
-static int launch_edge_L(const LevelArgs& A, int pass, long long e_begin, long long e_end, int num_sms,
+struct EdgeSpl {
+    static constexpr int v = L <= 3 ? PCS_EDGE_SPL : 1;
+};
+
+#ifndef PCS_EDGE_MINB
+#define PCS_EDGE_MINB 1  // resident blocks per SM the staged cuPC-E kernel is register-budgeted for
+#endif
+
+template <int L>
+__global__ void __launch_bounds__(kEdgeWarps * 32, PCS_EDGE_MINB) level_edge_staged_kernel(LevelArgs A, int pass, long long e_begin,
+                                                                            long long e_end, int wcap) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    unsigned char* base = smem_raw + (size_t)wib * edge_warp_smem(wcap);
+    unsigned long long* bar = reinterpret_cast<unsigned long long*>(base);
+    double* cibuf = reinterpret_cast<double*>(base + 16);
+    double* cj = cibuf + wcap + 2;
+    int* nb = reinterpret_cast<int*>(cj + wcap);
+    const double* __restrict__ C = A.C;
+    const long long ldc = A.ldc;
+    const unsigned long long dirbits = (unsigned long long)pass << kDirShift;
+    unsigned long long tests = 0, pinvs = 0;
+    int nan = 0;
+    uint32_t parity = 0;
+    if (lane == 0) bar_init(bar);
+    __syncwarp();
+    unsigned long long* cursor = &A.cnt->units[pass];
+    for (;;) {
+        unsigned long long ue = 0;
+        if (lane == 0) ue = atomicAdd(cursor, 1ull);
+        ue = __shfl_sync(0xffffffffu, ue, 0);
+        const long long e = e_begin + (long long)ue;
+        if (e >= e_end) break;
+        if (pass == 1 && A.keys[e] != (unsigned long long)kNoneKey) continue;
+        const int a = A.eu_a[e], qa = A.eu_qa[e];
+        const int b = A.nbr[A.off[a] + qa];
+        const int i = pass == 0 ? a : b;
+        const int q = pass == 0 ? qa : A.eu_qb[e];
+        const int j = pass == 0 ? b : a;
+        const int oi = A.off[i], w = A.off[i + 1] - oi;
+        if (w < L + 1) continue;
+        // ---- stage: C(i, nbr_i) by bulk copy (an even-aligned superset of the segment), the rest by lanes
+        const int o0 = oi & ~1;
+        if (lane == 0) bulk_load(cibuf, A.cnbr + o0, (uint32_t)((((oi + w + 1) & ~1) - o0) * sizeof(double)), bar);
+        const double* __restrict__ Cj = C + (size_t)j * ldc;
+        for (int k = lane; k < w; k += 32) {
+            const int m = A.nbr[oi + k];
+            nb[k] = m;
+            cj[k] = __ldg(Cj + m);
+        }
+        bar_wait(bar, parity);
+        parity ^= 1u;
+        __syncwarp();
+        const double* ci = cibuf + (oi - o0);
+        const double cij = ci[q];
+        const unsigned long long total = A.binom(w - 1, L);
+        // rounds of 32 * SPL ranks: lane l tests ranks base_t + 32 s + l (s < SPL), SPL independent
+        // chains per lane; the round's first separating set in rank order wins
+        constexpr int SPL = EdgeSpl<L>::v;
+        for (unsigned long long base_t = 0; base_t < total; base_t += 32 * SPL) {
+            int d[SPL];
+            int pos[SPL][L];
+#pragma unroll
+            for (int sp = 0; sp < SPL; ++sp) {
+                const unsigned long long t = base_t + 32 * sp + lane;
+                d[sp] = kDependent;
+                if (t < total) {
+                    unrank_est<L>(A.binom, w - 1, t, pos[sp]);
+                    int mem[L];
+                    double ciS[L], cjS[L], minv[L * L], p0[L], h00, h01, denom;
+#pragma unroll
+                    for (int k = 0; k < L; ++k) {
+                        pos[sp][k] += pos[sp][k] >= q;  // skip the target position (skeleton.hpp:146-149)
+                        mem[k] = nb[pos[sp][k]];
+                        ciS[k] = ci[pos[sp][k]];
+                        cjS[k] = cj[pos[sp][k]];
+                    }
+                    if (L <= 3 && A.pinv_table) {  // the level's pseudo-inverse table (same bits)
+                        const double* te = A.pinv_table + colex_rank<L>(mem) * (unsigned long long)PinvStride<L>::v;
+#pragma unroll
+                        for (int q2 = 0; q2 < L * L; ++q2) minv[q2] = __ldg(te + q2);
+                    } else {
+                        double m2[L * L];
+#pragma unroll
+                        for (int x = 0; x < L; ++x)
+#pragma unroll
+                            for (int y = 0; y < L; ++y) m2[x * L + y] = __ldg(C + (size_t)mem[x] * ldc + mem[y]);
+                        pinv<L>(m2, minv);
+                    }
+                    p0_terms<L>(minv, ciS, p0, h00);
+                    h_terms<L>(minv, ciS, p0, h00, cjS, cij, h01, denom);
+                    d[sp] = take_near(decide_fast(h01, denom, A.th), A, i, j, h01, denom);
+                    ++tests;
+                    ++pinvs;
+                }
+            }
+            bool found = false;
+#pragma unroll
+            for (int sp = 0; sp < SPL; ++sp) {
+                const unsigned hit = __ballot_sync(0xffffffffu, d[sp] != kDependent);
+                if (hit && !found) {
+                    found = true;
+                    const int first = __ffs(hit) - 1;
+                    if (lane == first) {
+                        if (d[sp] == kNanError) nan = 1;
+                        else atomicMin(A.keys + e, dirbits | rank_of<L>(A.binom, w, pos[sp]));
+                    }
+                }
+            }
+            if (found) break;
+        }
+        __syncwarp();  // the buffers are rewritten for the next edge
+    }
+    add_counter(&A.cnt->gpu_tests, tests);
+    add_counter(&A.cnt->gpu_exact, tests);
+    add_counter(&A.cnt->gpu_pinv, pinvs);
+    if (nan) atomicOr(&A.cnt->err_nan, 1);
+}
+
+#ifndef PCS_EDGE_STAGED
+#define PCS_EDGE_STAGED 1  // 0: cuPC-E always on the unstaged kernel (A/B)
+#endif
+
+template <int L>
+static int launch_edge_L(const LevelArgs& A, int pass, long long e_begin, long long e_end, int maxw, int num_sms,
                          cudaStream_t s) {
     int per_sm = 0;
+    const int wcap = (maxw + 3) & ~3;
+    const size_t smem = edge_warp_smem(wcap) * kEdgeWarps;
+    if (PCS_EDGE_STAGED && smem <= kEdgeSmemMax) {
+        if (cudaFuncSetAttribute(level_edge_staged_kernel<L>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+            cudaSuccess)
+            return -2;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, level_edge_staged_kernel<L>, kEdgeWarps * 32, smem);
+        if (per_sm < 1) per_sm = 1;
+        ++g_kernel_launches;
+        level_edge_staged_kernel<L><<<num_sms * per_sm, kEdgeWarps * 32, smem, s>>>(A, pass, e_begin, e_end, wcap);
+        return 0;
+    }
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, level_edge_kernel<L>, 128, 0);
     if (per_sm < 1) per_sm = 1;
     ++g_kernel_launches;
@@ -1612,16 +1795,16 @@ static int launch_edge_L(const LevelArgs& A, int pass, long long e_begin, long l
     return 0;
 }
 
-int launch_level_edge(const LevelArgs& A, int pass, long long e_begin, long long e_end, int num_sms,
+int launch_level_edge(const LevelArgs& A, int pass, long long e_begin, long long e_end, int maxw, int num_sms,
                       cudaStream_t s) {
     switch (A.ell) {
-        case 2: return launch_edge_L<2>(A, pass, e_begin, e_end, num_sms, s);
-        case 3: return launch_edge_L<3>(A, pass, e_begin, e_end, num_sms, s);
-        case 4: return launch_edge_L<4>(A, pass, e_begin, e_end, num_sms, s);
-        case 5: return launch_edge_L<5>(A, pass, e_begin, e_end, num_sms, s);
-        case 6: return launch_edge_L<6>(A, pass, e_begin, e_end, num_sms, s);
-        case 7: return launch_edge_L<7>(A, pass, e_begin, e_end, num_sms, s);
-        case 8: return launch_edge_L<8>(A, pass, e_begin, e_end, num_sms, s);
+        case 2: return launch_edge_L<2>(A, pass, e_begin, e_end, maxw, num_sms, s);
+        case 3: return launch_edge_L<3>(A, pass, e_begin, e_end, maxw, num_sms, s);
+        case 4: return launch_edge_L<4>(A, pass, e_begin, e_end, maxw, num_sms, s);
+        case 5: return launch_edge_L<5>(A, pass, e_begin, e_end, maxw, num_sms, s);
+        case 6: return launch_edge_L<6>(A, pass, e_begin, e_end, maxw, num_sms, s);
+        case 7: return launch_edge_L<7>(A, pass, e_begin, e_end, maxw, num_sms, s);
+        case 8: return launch_edge_L<8>(A, pass, e_begin, e_end, maxw, num_sms, s);
         default: return -1;
     }
 }

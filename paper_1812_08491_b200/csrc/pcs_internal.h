@@ -125,7 +125,8 @@ int pinv_table_stride(int ell);
 int launch_pinv_table(const double* C, long long ldc, int p, int ell, double* table, cudaStream_t s);
 int launch_level_set(const LevelArgs& A, int pass, const unsigned long long* prefix, unsigned long long u_begin,
                      unsigned long long u_end, int num_sms, cudaStream_t s);
-int launch_level_edge(const LevelArgs& A, int pass, long long e_begin, long long e_end, int num_sms,
+// maxw: the snapshot's widest row (sizes the staged kernel's shared-memory row buffers)
+int launch_level_edge(const LevelArgs& A, int pass, long long e_begin, long long e_end, int maxw, int num_sms,
                       cudaStream_t s);
 // generic ell (> kMaxTemplLevel, <= kMaxRtLevel): cuPC-S with global per-lane scratch
 long long level_rt_scratch_bytes(int ell, int num_sms, int* blocks_out);

@@ -158,6 +158,26 @@ for s in $STEPS; do
       timeout 1500 python tools/variants.py run $VARIANTS --workload C5 --max-level 2 --repeats 1 > $OUT/ntvar_c5.json 2> $OUT/ntvar5.err
       timeout 900 python tools/variants.py run $VARIANTS --workload C3 --max-level -1 --repeats 3 > $OUT/ntvar_c3.json 2>> $OUT/ntvar5.err
       ;;
+    edgeab)
+      timeout 900 python tools/variants.py run --strategy edge --workload C2 --max-level 2 --repeats 2 > $OUT/edgeab_c2.json 2> $OUT/edgeab.err
+      timeout 900 python tools/variants.py run --strategy edge --workload C3 --max-level -1 --repeats 3 > $OUT/edgeab_c3.json 2>> $OUT/edgeab.err
+      timeout 900 python tools/variants.py run --strategy edge --workload C4 --max-level -1 --repeats 3 > $OUT/edgeab_c4.json 2>> $OUT/edgeab.err
+      timeout 1500 python -m pytest tests/test_gpu_golden.py tests/test_gpu_random_sweep.py tests/test_gpu_parity.py tests/test_gpu_configs.py -x -q \
+        > $OUT/pytest_edge.log 2>&1; echo "rc=$?" >> $OUT/pytest_edge.log
+      ;;
+    edgeab2)
+      timeout 900 python tools/variants.py run spl1 spl4 spl2m3 --strategy edge --workload C2 --max-level 2 --repeats 2 > $OUT/edgeab2_c2.json 2> $OUT/edgeab2.err
+      timeout 900 python tools/variants.py run spl1 spl4 spl2m3 --strategy edge --workload C3 --max-level -1 --repeats 3 > $OUT/edgeab2_c3.json 2>> $OUT/edgeab2.err
+      timeout 900 python tools/variants.py run stagerep2 p1rep2 dbuf --workload C2 --max-level 3 --repeats 2 > $OUT/probes_c2.json 2>> $OUT/edgeab2.err
+      timeout 900 python tools/explore.py C2 edge 3 > $OUT/explore_c2_edge.log 2>&1
+      ;;
+    edgel3)
+      PCS_PINV_TABLE=0 timeout 900 python tools/explore.py C2 edge 3 > $OUT/explore_c2_edge_notable.log 2>&1
+      timeout 900 ncu --set full --clock-control none --import-source on -k regex:level_edge_staged -c 1 -f -o $OUT/edge2 \
+        python tools/profile_target.py 2 4 edge > $OUT/ncu_edge2.log 2>&1
+      timeout 900 ncu --set full --clock-control none --import-source on -k regex:level_edge_staged -c 1 -f -o $OUT/edge3 \
+        python tools/profile_target.py 3 256 edge > $OUT/ncu_edge3.log 2>&1
+      ;;
     bench)
       timeout 900 python bench.py > $OUT/bench.json 2> $OUT/bench.err
       ;;

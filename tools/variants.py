@@ -44,7 +44,7 @@ def cmd_build(specs):
             print("built", lib)
 
 
-def cmd_run(names, workload, max_level, repeats):
+def cmd_run(names, workload, max_level, repeats, strategy="set"):
     import numpy as np
 
     import paper_1812_08491_b200 as pcs
@@ -55,7 +55,7 @@ def cmd_run(names, workload, max_level, repeats):
     del w
     c = pcs.compute_correlation(x)
     names = names or sorted(f[len("libpcstable_b200_"):-3] for f in os.listdir(VDIR) if f.endswith(".so"))
-    cfg = pcs.SkeletonConfig(alpha=0.01, max_level=None if max_level < 0 else max_level)
+    cfg = pcs.SkeletonConfig(alpha=0.01, strategy=pcs.Strategy(strategy), max_level=None if max_level < 0 else max_level)
     best = None
     for _ in range(repeats):  # best of `repeats`, like the variants (the first run pays lazy module loading)
         base = pcs.run_pc_stable(c, m, cfg)
@@ -85,8 +85,9 @@ if __name__ == "__main__":
     ap.add_argument("--workload", default="C2")
     ap.add_argument("--max-level", type=int, default=3)
     ap.add_argument("--repeats", type=int, default=2)
+    ap.add_argument("--strategy", default="set", help="set (cuPC-S) or edge (cuPC-E)")
     a = ap.parse_args()
     if a.cmd == "build":
         cmd_build(a.items)
     else:
-        cmd_run(a.items, a.workload, a.max_level, a.repeats)
+        cmd_run(a.items, a.workload, a.max_level, a.repeats, a.strategy)
