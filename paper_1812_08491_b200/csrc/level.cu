@@ -1639,6 +1639,38 @@ __device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t b
 }
 }  // namespace
 
+// Advance a lexicographic L-subset {pos[0] < ... < pos[L-1]} of {0..n-1} by k ranks (L = 2, 3): the last
+// member absorbs k, and each overflow past n - 1 carries into the next block of the member before it
+// (block (a, b) holds c in [b + 1, n - 1]).  The same map as comb.hpp:50-67's unrank of rank t + k;
+// past the last subset the positions are left unspecified (callers check the rank).
+template <int L>
+__device__ __forceinline__ void advance_lex(int (&pos)[L], int n, int k) {
+    if constexpr (L == 2) {
+        int a = pos[0], b = pos[1] + k;
+        while (b >= n && a < n - 2) {
+            a += 1;
+            b = b - n + a + 1;
+        }
+        pos[0] = a;
+        pos[1] = b;
+    } else {
+        int a = pos[0], b = pos[1], c = pos[2] + k;
+        while (c >= n) {
+            const int o = c - n;
+            b += 1;
+            if (b > n - 2) {
+                a += 1;
+                b = a + 1;
+                if (a > n - 3) break;
+            }
+            c = b + 1 + o;
+        }
+        pos[0] = a;
+        pos[1] = b;
+        pos[2] = c;
+    }
+}
+
 constexpr int kEdgeWarps = 4;
 // per-warp shared bytes for rows up to wcap entries (wcap a multiple of 4): barrier, ci (+2 for the
 // aligned superset the bulk copy brings), cj, nb
@@ -1706,8 +1738,17 @@ __global__ void __launch_bounds__(kEdgeWarps * 32, PCS_EDGE_MINB) level_edge_sta
         const double cij = ci[q];
         const unsigned long long total = A.binom(w - 1, L);
         // rounds of 32 * SPL ranks: lane l tests ranks base_t + 32 s + l (s < SPL), SPL independent
-        // chains per lane; the round's first separating set in rank order wins
+        // chains per lane; the round's first separating set in rank order wins.  At l = 2, 3 a lane
+        // unranks its first set once per edge and then steps its positions by 32 SPL ranks per round
+        // (advance_lex), no binomial-table loads in the loop.
         constexpr int SPL = EdgeSpl<L>::v;
+        constexpr bool kIncr = L <= 3;
+        int cur[SPL][L];
+        if (kIncr) {
+#pragma unroll
+            for (int sp = 0; sp < SPL; ++sp)
+                if ((unsigned long long)(32 * sp + lane) < total) unrank_est<L>(A.binom, w - 1, 32 * sp + lane, cur[sp]);
+        }
         for (unsigned long long base_t = 0; base_t < total; base_t += 32 * SPL) {
             int d[SPL];
             int pos[SPL][L];
@@ -1716,7 +1757,13 @@ __global__ void __launch_bounds__(kEdgeWarps * 32, PCS_EDGE_MINB) level_edge_sta
                 const unsigned long long t = base_t + 32 * sp + lane;
                 d[sp] = kDependent;
                 if (t < total) {
-                    unrank_est<L>(A.binom, w - 1, t, pos[sp]);
+                    if (kIncr) {
+#pragma unroll
+                        for (int k = 0; k < L; ++k) pos[sp][k] = cur[sp][k];
+                        advance_lex<L>(cur[sp], w - 1, 32 * SPL);
+                    } else {
+                        unrank_est<L>(A.binom, w - 1, t, pos[sp]);
+                    }
                     int mem[L];
                     double ciS[L], cjS[L], minv[L * L], p0[L], h00, h01, denom;
 #pragma unroll

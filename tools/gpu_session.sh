@@ -178,6 +178,13 @@ for s in $STEPS; do
       timeout 900 ncu --set full --clock-control none --import-source on -k regex:level_edge_staged -c 1 -f -o $OUT/edge3 \
         python tools/profile_target.py 3 256 edge > $OUT/ncu_edge3.log 2>&1
       ;;
+    edgeab3)
+      timeout 900 python tools/variants.py run spl2 spl2m4 unstaged --strategy edge --workload C2 --max-level 2 --repeats 2 > $OUT/edgeab3_c2.json 2> $OUT/edgeab3.err
+      timeout 900 python tools/variants.py run spl2 spl2m4 unstaged --strategy edge --workload C3 --max-level -1 --repeats 3 > $OUT/edgeab3_c3.json 2>> $OUT/edgeab3.err
+      timeout 1500 python -m pytest tests/test_gpu_golden.py tests/test_gpu_random_sweep.py tests/test_gpu_parity.py tests/test_gpu_configs.py -x -q \
+        > $OUT/pytest_edge.log 2>&1; echo "rc=$?" >> $OUT/pytest_edge.log
+      timeout 900 python tools/explore.py C2 edge 3 > $OUT/explore_c2_edge.log 2>&1
+      ;;
     bench)
       timeout 900 python bench.py > $OUT/bench.json 2> $OUT/bench.err
       ;;
