@@ -1822,10 +1822,15 @@ __global__ void __launch_bounds__(kEdgeWarps * 32, PCS_EDGE_MINB) level_edge_sta
 template <int L>
 static int launch_edge_L(const LevelArgs& A, int pass, long long e_begin, long long e_end, int maxw, int num_sms,
                          cudaStream_t s) {
+    // PCS_EDGE_STAGED=0 in the environment forces the unstaged kernel (tests cover both)
+    static const bool staged = [] {
+        const char* e = std::getenv("PCS_EDGE_STAGED");
+        return PCS_EDGE_STAGED && !(e && std::atoi(e) == 0);
+    }();
     int per_sm = 0;
     const int wcap = (maxw + 3) & ~3;
     const size_t smem = edge_warp_smem(wcap) * kEdgeWarps;
-    if (PCS_EDGE_STAGED && smem <= kEdgeSmemMax) {
+    if (staged && smem <= kEdgeSmemMax) {
         if (cudaFuncSetAttribute(level_edge_staged_kernel<L>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
             cudaSuccess)
             return -2;

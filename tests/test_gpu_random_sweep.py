@@ -50,6 +50,28 @@ def test_random_shapes(pcs, oracle, variant):
     print(f"{variant}: 24 random shapes identical, deepest level {deepest}")
 
 
+def _sweep_subprocess(env_extra, variant, n, seed):
+    code = (
+        "import sys, json; sys.path.insert(0, %r)\n"
+        "import paper_1812_08491_b200 as pcs\n"
+        "from oracle import pyoracle as O\n"
+        "from tests.test_gpu_random_sweep import _cases, _check\n"
+        "bad = []\n"
+        "for case in _cases(%d, %d):\n"
+        "    errs, _ = _check(pcs, O, *case, %r)\n"
+        "    if errs: bad.append([list(case), errs])\n"
+        "print(json.dumps(bad))\n" % (ROOT, n, seed, variant))
+    env = dict(os.environ, **env_extra)
+    out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env, cwd=ROOT, timeout=900)
+    assert out.returncode == 0, out.stderr[-2000:]
+    return json.loads(out.stdout.strip().splitlines()[-1])
+
+
+def test_random_shapes_unstaged_edge():
+    """cuPC-E on the unstaged level_edge_kernel (the fallback for rows too wide for shared memory)."""
+    assert _sweep_subprocess({"PCS_EDGE_STAGED": "0"}, "edge", 10, 11) == []
+
+
 def test_random_shapes_tiled_level1():
     code = (
         "import sys, json; sys.path.insert(0, %r)\n"

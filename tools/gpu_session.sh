@@ -185,6 +185,14 @@ for s in $STEPS; do
         > $OUT/pytest_edge.log 2>&1; echo "rc=$?" >> $OUT/pytest_edge.log
       timeout 900 python tools/explore.py C2 edge 3 > $OUT/explore_c2_edge.log 2>&1
       ;;
+    l2links)
+      timeout 900 python tools/variants.py run old dbuf ntl24 --workload C5a --max-level 2 --repeats 2 > $OUT/l2links_c5a.json 2> $OUT/l2links.err
+      timeout 900 python tools/variants.py run old dbuf ntl24 --workload C5c --max-level 2 --repeats 1 > $OUT/l2links_c5c.json 2>> $OUT/l2links.err
+      timeout 900 python tools/variants.py run old --workload C2 --max-level 3 --repeats 2 > $OUT/l2links_c2.json 2>> $OUT/l2links.err
+      timeout 1800 python tools/variants.py run old --workload C5 --max-level 2 --repeats 1 > $OUT/l2links_c5.json 2>> $OUT/l2links.err
+      timeout 1500 python -m pytest tests/test_gpu_golden.py tests/test_gpu_random_sweep.py tests/test_gpu_parity.py tests/test_gpu_configs.py -x -q \
+        > $OUT/pytest_l2links.log 2>&1; echo "rc=$?" >> $OUT/pytest_l2links.log
+      ;;
     bench)
       timeout 900 python bench.py > $OUT/bench.json 2> $OUT/bench.err
       ;;

@@ -16,7 +16,8 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 VDIR = os.path.join(ROOT, "paper_1812_08491_b200", "variants")
 SHAPES = {"C2": (1000, 10000, 0.1, 1), "C3": (1643, 850, 0.01, 2), "C4": (5361, 63, 0.002, 3),
-          "C5": (5000, 5000, 0.05, 4)}  # C5: rescaled generator
+          "C5": (5000, 5000, 0.05, 4),  # C5*: rescaled generator
+          "C5a": (2000, 5000, 0.05, 4), "C5c": (2000, 5000, 0.2, 6)}
 
 
 def cmd_build(specs):
@@ -51,7 +52,7 @@ def cmd_run(names, workload, max_level, repeats, strategy="set"):
     p, m, d, case = SHAPES[workload]
     seed = 7919 * case
     w = pcs.random_dag(p, d, seed)
-    x = pcs.sample_linear_gaussian_rescaled(w, m, seed + 1)[0] if workload == "C5" else pcs.sample_linear_gaussian(w, m, seed + 1)
+    x = pcs.sample_linear_gaussian_rescaled(w, m, seed + 1)[0] if workload.startswith("C5") else pcs.sample_linear_gaussian(w, m, seed + 1)
     del w
     c = pcs.compute_correlation(x)
     names = names or sorted(f[len("libpcstable_b200_"):-3] for f in os.listdir(VDIR) if f.endswith(".so"))
