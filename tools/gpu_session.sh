@@ -193,6 +193,22 @@ for s in $STEPS; do
       timeout 1500 python -m pytest tests/test_gpu_golden.py tests/test_gpu_random_sweep.py tests/test_gpu_parity.py tests/test_gpu_configs.py -x -q \
         > $OUT/pytest_l2links.log 2>&1; echo "rc=$?" >> $OUT/pytest_l2links.log
       ;;
+    dbuf2)
+      timeout 900 python tools/variants.py run dbuf2 --workload C5a --max-level 2 --repeats 3 > $OUT/dbuf2_c5a.json 2> $OUT/dbuf2.err
+      timeout 900 python tools/variants.py run dbuf2 --workload C5c --max-level 2 --repeats 2 > $OUT/dbuf2_c5c.json 2>> $OUT/dbuf2.err
+      timeout 900 python tools/variants.py run dbuf2 --workload C2 --max-level 3 --repeats 2 > $OUT/dbuf2_c2.json 2>> $OUT/dbuf2.err
+      timeout 900 ncu --set full --clock-control none --import-source on -k regex:level_edge_staged -c 1 -f -o $OUT/edge2 \
+        python tools/profile_target.py 2 4 edge > $OUT/ncu_edge2.log 2>&1
+      ;;
+    edgepf)
+      timeout 900 python tools/variants.py run prev --strategy edge --workload C2 --max-level 2 --repeats 2 > $OUT/edgepf_c2.json 2> $OUT/edgepf.err
+      timeout 900 python tools/variants.py run prev --strategy edge --workload C3 --max-level -1 --repeats 3 > $OUT/edgepf_c3.json 2>> $OUT/edgepf.err
+      timeout 900 python tools/variants.py run l2m5 l2m6 --workload C5a --max-level 2 --repeats 3 > $OUT/l2m_c5a.json 2>> $OUT/edgepf.err
+      timeout 900 python tools/variants.py run l2m5 l2m6 --workload C5c --max-level 2 --repeats 2 > $OUT/l2m_c5c.json 2>> $OUT/edgepf.err
+      timeout 1500 python -m pytest tests/test_gpu_golden.py tests/test_gpu_random_sweep.py tests/test_gpu_parity.py tests/test_gpu_configs.py -x -q \
+        > $OUT/pytest_edgepf.log 2>&1; echo "rc=$?" >> $OUT/pytest_edgepf.log
+      timeout 900 python tools/explore.py C2 edge 3 > $OUT/explore_c2_edge.log 2>&1
+      ;;
     bench)
       timeout 900 python bench.py > $OUT/bench.json 2> $OUT/bench.err
       ;;
