@@ -209,6 +209,26 @@ for s in $STEPS; do
         > $OUT/pytest_edgepf.log 2>&1; echo "rc=$?" >> $OUT/pytest_edgepf.log
       timeout 900 python tools/explore.py C2 edge 3 > $OUT/explore_c2_edge.log 2>&1
       ;;
+    occ)
+      timeout 900 python tools/variants.py run nt3m5 nt2m6 --workload C2 --max-level 3 --repeats 2 > $OUT/occ_c2.json 2> $OUT/occ.err
+      timeout 1800 python tools/variants.py run l2m4 --workload C5 --max-level 2 --repeats 1 > $OUT/occ_c5.json 2>> $OUT/occ.err
+      ;;
+    final)
+      timeout 900 python tools/variants.py run l2m7 --workload C5a --max-level 2 --repeats 3 > $OUT/l2m7_c5a.json 2> $OUT/final.err
+      timeout 900 python tools/variants.py run l2m7 --workload C5c --max-level 2 --repeats 2 > $OUT/l2m7_c5c.json 2>> $OUT/final.err
+      timeout 900 ncu --set full --clock-control none --import-source on -k regex:level_set_kernel -c 1 -f -o $OUT/l2 \
+        python tools/explore.py C5a set 2 > $OUT/ncu_l2.log 2>&1
+      ;;
+    tracec2)
+      PCS_TRACE=1 timeout 600 python bench.py --steps 2 --warmup 1 --no-cpu-baseline --no-e2e --no-secondary > $OUT/trace_c2.json 2> $OUT/trace_c2.err
+      ;;
+    h00s)
+      timeout 900 python tools/variants.py run prev --workload C2 --max-level 3 --repeats 2 > $OUT/h00s_c2.json 2> $OUT/h00s.err
+      timeout 900 python tools/variants.py run prev --workload C5a --max-level 2 --repeats 3 > $OUT/h00s_c5a.json 2>> $OUT/h00s.err
+      timeout 900 python tools/variants.py run prev --workload C5c --max-level 2 --repeats 2 > $OUT/h00s_c5c.json 2>> $OUT/h00s.err
+      timeout 900 python tools/variants.py run prev --workload C3 --max-level -1 --repeats 3 > $OUT/h00s_c3.json 2>> $OUT/h00s.err
+      timeout 1500 python -m pytest tests -m gpu -x -q > $OUT/pytest_h00s.log 2>&1; echo "rc=$?" >> $OUT/pytest_h00s.log
+      ;;
     bench)
       timeout 900 python bench.py > $OUT/bench.json 2> $OUT/bench.err
       ;;
