@@ -277,7 +277,8 @@ class AdjacencyMatrix:
         return bool((int(self.bits[i, j >> 5]) >> (j & 31)) & 1)
 
     def edge_count(self) -> int:
-        return int(np.triu(self.cells, 1).sum())
+        # popcount of the symmetric bitmask (no diagonal bits): every edge is counted twice
+        return int(np.bitwise_count(self.bits).sum(dtype=np.int64)) // 2
 
     def edges(self) -> np.ndarray:
         """(E, 2) array of surviving edges (i < j), ascending."""
@@ -390,12 +391,12 @@ def _collect(h, with_sepsets: bool = True) -> SkeletonResult:
     W = (p + 31) // 32
     bits = np.empty((p, W), np.uint32)
     L.pcs_result_bitmask(h, bits.ctypes.data_as(ct.POINTER(ct.c_uint32)))
-    nrec = L.pcs_result_record_ints(h)
+    nrec = L.pcs_result_record_ints(h) if with_sepsets else 0  # records only when sepsets are asked for
     rec = np.empty(max(nrec, 1), np.int32)
     if nrec:
         L.pcs_result_records(h, _ip(rec))
     adj = AdjacencyMatrix(bits, p)
-    sep = SeparationSets(p, adj, rec[:nrec] if with_sepsets else np.empty(0, np.int32), levels)
+    sep = SeparationSets(p, adj, rec[:nrec], levels)
     nn = L.pcs_result_near_count(h)
     near = []
     if nn:

@@ -229,6 +229,10 @@ for s in $STEPS; do
       timeout 900 python tools/variants.py run prev --workload C3 --max-level -1 --repeats 3 > $OUT/h00s_c3.json 2>> $OUT/h00s.err
       timeout 1500 python -m pytest tests -m gpu -x -q > $OUT/pytest_h00s.log 2>&1; echo "rc=$?" >> $OUT/pytest_h00s.log
       ;;
+    tracee2e)
+      PCS_TRACE=1 timeout 600 python bench.py --workload C4 --steps 2 --warmup 1 --no-cpu-baseline --no-secondary > $OUT/trace_c4.json 2> $OUT/trace_c4.err
+      PCS_TRACE=1 timeout 600 python bench.py --workload C3 --steps 2 --warmup 1 --no-cpu-baseline --no-secondary > $OUT/trace_c3.json 2> $OUT/trace_c3.err
+      ;;
     bench)
       timeout 900 python bench.py > $OUT/bench.json 2> $OUT/bench.err
       ;;
