@@ -233,6 +233,10 @@ for s in $STEPS; do
       PCS_TRACE=1 timeout 600 python bench.py --workload C4 --steps 2 --warmup 1 --no-cpu-baseline --no-secondary > $OUT/trace_c4.json 2> $OUT/trace_c4.err
       PCS_TRACE=1 timeout 600 python bench.py --workload C3 --steps 2 --warmup 1 --no-cpu-baseline --no-secondary > $OUT/trace_c3.json 2> $OUT/trace_c3.err
       ;;
+    eocc)
+      timeout 900 python tools/variants.py run eminb5 eminb6 --strategy edge --workload C2 --max-level 2 --repeats 2 > $OUT/eocc_c2.json 2> $OUT/eocc.err
+      timeout 900 python tools/variants.py run eminb5 eminb6 --strategy edge --workload C5a --max-level 2 --repeats 2 > $OUT/eocc_c5a.json 2>> $OUT/eocc.err
+      ;;
     bench)
       timeout 900 python bench.py > $OUT/bench.json 2> $OUT/bench.err
       ;;
