@@ -740,8 +740,9 @@ static pcs_status maybe_pinv_table(pcs_session* s, int ell) {
 }
 
 static bool merged_level(const pcs_session* s) {
+    // the generic-ell kernel (l > 8) serves both variants and merges its passes too
     return (s->cfg.variant == PCS_VARIANT_SET && s->ell >= 2 && s->ell <= kMaxTemplLevel && merge_passes()) ||
-           level1_tile(s);
+           (s->ell > kMaxTemplLevel && merge_passes()) || level1_tile(s);
 }
 
 pcs_status pcs_session_level_passes(pcs_session* s, int32_t* passes) {
@@ -804,7 +805,7 @@ pcs_status pcs_session_level_pass(pcs_session* s, int32_t pass) {
         if (u1 > u0) {
             if (s->ell > kMaxTemplLevel) {
                 CUDA_TRY(cudaMemsetAsync(&s->dCnt->units[pass], 0, sizeof(unsigned long long), s->st));
-                if (launch_level_set_rt(A, pass, s->dPrefix, u0, u1, s->num_sms, s->dScratch, s->st))
+                if (launch_level_set_rt(A, kpass, s->dPrefix, u0, u1, s->num_sms, s->dScratch, s->st))
                     return fail(PCS_EUNSUPPORTED, "level not supported by the generic set kernel");
             } else {
                 launch_refresh_kdir(A, s->info.e_dir, s->st);

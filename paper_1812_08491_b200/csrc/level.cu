@@ -1892,10 +1892,12 @@ __global__ void __launch_bounds__(128) level_set_rt_kernel(LevelArgs A, int pass
     int* mem = pos + n;
     const double* __restrict__ C = A.C;
     const long long ldc = A.ldc;
-    const unsigned long long dirbits = (unsigned long long)pass << kDirShift;
+    // pass 2: both directions in one sweep (each set's pseudo-inverse once per level), a target's key
+    // base carrying its own direction bit, as in level_set_kernel
+    const unsigned long long dirbits = pass == 1 ? (1ull << kDirShift) : 0ull;
     unsigned long long tests = 0, pinvs = 0, degen = 0;
     int nan = 0;
-    unsigned long long* cursor = &A.cnt->units[pass];
+    unsigned long long* cursor = &A.cnt->units[pass & 1];
     u_end = min(u_end, prefix[A.p]);
     int row_hint = 0;
     for (;;) {
@@ -1907,10 +1909,12 @@ __global__ void __launch_bounds__(128) level_set_rt_kernel(LevelArgs A, int pass
         row_hint = i;
         const unsigned long long t0 = (u - prefix[i]) * kSetBand;
         const int oi = A.off[i], w = A.off[i + 1] - oi, lc = A.lowcnt[i];
-        const int qbeg = pass == 0 ? lc : 0, qend = pass == 0 ? w : lc;
-        const unsigned long long K0 = dirbits | t0;
+        const int qbeg = pass == 2 ? 0 : (pass == 0 ? lc : 0), qend = pass == 2 ? w : (pass == 0 ? w : lc);
+        auto dbits = [&](int q) -> unsigned long long {  // q < lc: j < i, direction 1 of edge (j, i)
+            return pass == 2 ? (q < lc ? (1ull << kDirShift) : 0ull) : dirbits;
+        };
         bool open = false;
-        for (int q = qbeg + lane; q < qend; q += 32) open |= A.keys[A.eid[oi + q]] > K0;
+        for (int q = qbeg + lane; q < qend; q += 32) open |= A.keys[A.eid[oi + q]] > (dbits(q) | t0);
         if (!__any_sync(0xffffffffu, open)) {
             // no open target at rank t0: none at any later rank of this row (keys only decrease)
             if (lane == 0) atomicMax(cursor, prefix[i + 1] - u_begin);
@@ -1946,7 +1950,7 @@ __global__ void __launch_bounds__(128) level_set_rt_kernel(LevelArgs A, int pass
                 j = A.nbr[oi + q];
                 e = A.eid[oi + q];
                 key = A.keys[e];
-                live = key > K0;
+                live = key > (dbits(q) | t0);
                 if (live) cij = __ldg(C + (size_t)i * ldc + j);
             }
             if (!__any_sync(0xffffffffu, live)) continue;
@@ -1954,7 +1958,7 @@ __global__ void __launch_bounds__(128) level_set_rt_kernel(LevelArgs A, int pass
                 if (!live) break;
                 const double* S = wbase + sg * SD;
                 const int* Spos = ibase + sg * 2 * n;
-                const unsigned long long Kc = dirbits | (t0 + sg);
+                const unsigned long long Kc = dbits(q) | (t0 + sg);
                 if (key <= Kc) { live = false; break; }
                 bool member = false;
                 for (int a = 0; a < n; ++a) member |= Spos[a] == q;

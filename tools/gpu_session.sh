@@ -237,6 +237,16 @@ for s in $STEPS; do
       timeout 900 python tools/variants.py run eminb5 eminb6 --strategy edge --workload C2 --max-level 2 --repeats 2 > $OUT/eocc_c2.json 2> $OUT/eocc.err
       timeout 900 python tools/variants.py run eminb5 eminb6 --strategy edge --workload C5a --max-level 2 --repeats 2 > $OUT/eocc_c5a.json 2>> $OUT/eocc.err
       ;;
+    c3launch)
+      timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/c3_launches.csv \
+        python tools/explore.py C3 set -1 > $OUT/c3_launch.log 2>&1
+      ;;
+    rtmerge)
+      timeout 900 python tools/variants.py run prev --workload C3 --max-level -1 --repeats 3 > $OUT/rtm_c3.json 2> $OUT/rtm.err
+      timeout 900 python tools/variants.py run prev --strategy edge --workload C3 --max-level -1 --repeats 3 > $OUT/rtm_c3e.json 2>> $OUT/rtm.err
+      timeout 1500 python -m pytest tests/test_gpu_golden.py tests/test_gpu_random_sweep.py tests/test_gpu_parity.py tests/test_gpu_configs.py tests/test_gpu_shards.py tests/test_gpu_multiproc.py -x -q \
+        > $OUT/pytest_rtm.log 2>&1; echo "rc=$?" >> $OUT/pytest_rtm.log
+      ;;
     bench)
       timeout 900 python bench.py > $OUT/bench.json 2> $OUT/bench.err
       ;;
