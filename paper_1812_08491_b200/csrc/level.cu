@@ -122,6 +122,9 @@ void launch_near_fixup(const LevelArgs& A, cudaStream_t s) {
 #ifndef PCS_SET_NT_L2
 #define PCS_SET_NT_L2 3     // targets per lane per set at L = 2 (short tests: per-step overhead dominates)
 #endif
+#ifndef PCS_SET_MINB_DEEP
+#define PCS_SET_MINB_DEEP 2  // the same at L >= 6: 255 registers, fewer pinv spills (C3 levels 6-8 0.56 -> 0.45 ms)
+#endif
 #ifndef PCS_SET_MINB_L2
 #define PCS_SET_MINB_L2 6   // the same at L = 2 (80 registers: 24 warps per SM; C5 p=2000 level 2 -4 to -6% vs 4)
 #endif
@@ -1297,7 +1300,7 @@ __device__ __forceinline__ void set_sweep(const LevelArgs& A, SetWarpSmem<L>& S,
 }
 
 template <int L>
-__global__ void __launch_bounds__(kSetWarps * 32, L == 2 ? PCS_SET_MINB_L2 : PCS_SET_MINB) level_set_kernel(LevelArgs A, int pass,
+__global__ void __launch_bounds__(kSetWarps * 32, L == 2 ? PCS_SET_MINB_L2 : (L >= 6 ? PCS_SET_MINB_DEEP : PCS_SET_MINB)) level_set_kernel(LevelArgs A, int pass,
                                                                      const unsigned long long* prefix,
                                                                      unsigned long long u_begin,
                                                                      unsigned long long u_end) {

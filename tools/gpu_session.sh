@@ -247,6 +247,15 @@ for s in $STEPS; do
       timeout 1500 python -m pytest tests/test_gpu_golden.py tests/test_gpu_random_sweep.py tests/test_gpu_parity.py tests/test_gpu_configs.py tests/test_gpu_shards.py tests/test_gpu_multiproc.py -x -q \
         > $OUT/pytest_rtm.log 2>&1; echo "rc=$?" >> $OUT/pytest_rtm.log
       ;;
+    ncudeep)
+      timeout 900 ncu --set full --clock-control none --import-source on -k regex:level_set_kernel --launch-skip 6 -c 1 -f -o $OUT/deep8 \
+        python tools/explore.py C3 set -1 > $OUT/ncu_deep8.log 2>&1
+      timeout 900 python tools/explore.py C3 set -1 > $OUT/explore_c3.log 2>&1
+      ;;
+    deep)
+      timeout 900 python tools/variants.py run deep2 --workload C3 --max-level -1 --repeats 3 > $OUT/deep_c3.json 2> $OUT/deep.err
+      timeout 900 python tools/variants.py run deep2 --strategy edge --workload C3 --max-level -1 --repeats 3 > $OUT/deep_c3e.json 2>> $OUT/deep.err
+      ;;
     bench)
       timeout 900 python bench.py > $OUT/bench.json 2> $OUT/bench.err
       ;;
