@@ -256,6 +256,9 @@ for s in $STEPS; do
       timeout 900 python tools/variants.py run deep2 --workload C3 --max-level -1 --repeats 3 > $OUT/deep_c3.json 2> $OUT/deep.err
       timeout 900 python tools/variants.py run deep2 --strategy edge --workload C3 --max-level -1 --repeats 3 > $OUT/deep_c3e.json 2>> $OUT/deep.err
       ;;
+    fp64ilp)
+      ./tools/micro/fp64_ilp > $OUT/fp64_ilp.log 2>&1
+      ;;
     bench)
       timeout 900 python bench.py > $OUT/bench.json 2> $OUT/bench.err
       ;;
