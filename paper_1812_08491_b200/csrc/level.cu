@@ -1645,38 +1645,6 @@ __device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t b
 }
 }  // namespace
 
-// Advance a lexicographic L-subset {pos[0] < ... < pos[L-1]} of {0..n-1} by k ranks (L = 2, 3): the last
-// member absorbs k, and each overflow past n - 1 carries into the next block of the member before it
-// (block (a, b) holds c in [b + 1, n - 1]).  The same map as comb.hpp:50-67's unrank of rank t + k;
-// past the last subset the positions are left unspecified (callers check the rank).
-template <int L>
-__device__ __forceinline__ void advance_lex(int (&pos)[L], int n, int k) {
-    if constexpr (L == 2) {
-        int a = pos[0], b = pos[1] + k;
-        while (b >= n && a < n - 2) {
-            a += 1;
-            b = b - n + a + 1;
-        }
-        pos[0] = a;
-        pos[1] = b;
-    } else {
-        int a = pos[0], b = pos[1], c = pos[2] + k;
-        while (c >= n) {
-            const int o = c - n;
-            b += 1;
-            if (b > n - 2) {
-                a += 1;
-                b = a + 1;
-                if (a > n - 3) break;
-            }
-            c = b + 1 + o;
-        }
-        pos[0] = a;
-        pos[1] = b;
-        pos[2] = c;
-    }
-}
-
 constexpr int kEdgeWarps = 4;
 // per-warp shared bytes for rows up to wcap entries (wcap a multiple of 4): barrier, ci (+2 for the
 // aligned superset the bulk copy brings), cj, nb
