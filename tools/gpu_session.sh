@@ -259,6 +259,12 @@ for s in $STEPS; do
     fp64ilp)
       ./tools/micro/fp64_ilp > $OUT/fp64_ilp.log 2>&1
       ;;
+    l1compact)
+      timeout 900 python tools/variants.py run nocompact --workload C3 --max-level 1 --repeats 3 > $OUT/l1c_c3.json 2> $OUT/l1c.err
+      timeout 900 python tools/variants.py run nocompact --workload C4 --max-level 1 --repeats 3 > $OUT/l1c_c4.json 2>> $OUT/l1c.err
+      timeout 900 python tools/variants.py run nocompact --workload C2 --max-level 1 --repeats 3 > $OUT/l1c_c2.json 2>> $OUT/l1c.err
+      timeout 1500 python -m pytest tests -m gpu -x -q > $OUT/pytest_l1c.log 2>&1; echo "rc=$?" >> $OUT/pytest_l1c.log
+      ;;
     bench)
       timeout 900 python bench.py > $OUT/bench.json 2> $OUT/bench.err
       ;;
