@@ -265,6 +265,11 @@ for s in $STEPS; do
       timeout 900 python tools/variants.py run nocompact --workload C2 --max-level 1 --repeats 3 > $OUT/l1c_c2.json 2>> $OUT/l1c.err
       timeout 1500 python -m pytest tests -m gpu -x -q > $OUT/pytest_l1c.log 2>&1; echo "rc=$?" >> $OUT/pytest_l1c.log
       ;;
+    links6)
+      timeout 900 python tools/variants.py run links --workload C5a --max-level 2 --repeats 3 > $OUT/links6_c5a.json 2> $OUT/links6.err
+      timeout 900 python tools/variants.py run links --workload C5c --max-level 2 --repeats 2 > $OUT/links6_c5c.json 2>> $OUT/links6.err
+      timeout 900 python tools/variants.py run links --workload C2 --max-level 2 --repeats 3 > $OUT/links6_c2.json 2>> $OUT/links6.err
+      ;;
     bench)
       timeout 900 python bench.py > $OUT/bench.json 2> $OUT/bench.err
       ;;
